@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""bench.py — PowerSGD compress + all-reduce + decompress, ms/step (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload resnet18|lstm|stress]
+
+N = 1: one B200, W = 1 (BASELINE.json configs[1], ResNet-18 rank 2: the
+compress / orthogonalise / decompress kernels, no collective).  N > 1 (under
+torchrun): one process per GPU = one data-parallel worker, NCCL all-reduces of
+the packed P and q buffers (configs[2]); per-GPU work is fixed ("weak").
+
+A step is one PowerSGD round over every parameter of the catalog with error
+feedback: delta = g + e, P = delta Q, [AR1], P-hat = MGS(P), q = delta^T P-hat,
+e = delta - P-hat q^T, [AR2], M-hat = P-hat Q-bar^T (optimizer.py:110-129).
+Inputs are resident in HBM; L2 is flushed (256 MiB write) before every timed
+step; each step is timed with CUDA events on the launching stream and the
+result is the max over ranks.  `e2e` repeats the step through the same API
+with the gradients copied in from pinned host memory and M-hat + bias mean
+copied back, inside the timed region.
+
+`--impl reference` times the reference algorithm on the host CPU (the float64
+numpy oracle in oracle/powersgd.py, the reference being pure Python), W = N
+simulated workers, rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PowerSGD compress+allreduce+decompress ms/step, ResNet-18 rank 2, 1/2/4/8 B200"
+DEFAULT_RANK = {"resnet18": 2, "lstm": 4, "stress": 8}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["resnet18", "lstm", "stress"], default="resnet18")
+    ap.add_argument("--rank", type=int, default=None)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    a = ap.parse_args()
+    a.warmup = max(3, a.warmup)
+    if a.rank is None:
+        a.rank = DEFAULT_RANK[a.workload]
+    return a
+
+
+def catalog_specs(workload):
+    from paper_1905_13727_b200 import catalogs
+    if workload == "stress":
+        return list(catalogs.stress().params)
+    return list(catalogs.get_catalog(workload).params)
+
+
+def sizes(specs, rank):
+    N = snr = smr = nb = 0
+    for s in specs:
+        if s.is_bias:
+            nb += s.size
+            continue
+        n, m = s.matrix_shape
+        r = min(n, m, rank)
+        N += n * m
+        snr += n * r
+        smr += m * r
+    return N, snr, smr, nb
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        for info in threadpool_info():
+            if info.get("internal_api") in ("openblas", "mkl", "blis"):
+                return int(info["num_threads"])
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------- CPU reference arm
+def oracle_steps(specs, rank, world, steps, budget_s, warmup=1):
+    """Time the reference algorithm (float64 oracle, optimizer.py:110-129 without the
+    momentum update) with `world` simulated workers; returns per-step seconds."""
+    import numpy as np
+    from oracle import powersgd as O
+    ospecs = [O.ParamSpec(s.name, s.shape) for s in specs]
+    grads = [[O.derive_rng(0, "grad", 0, w, i).standard_normal(s.shape).astype(np.float32)
+              for i, s in enumerate(ospecs)] for w in range(world)]
+    comp = O.PowerSGD(rank)
+    comm = O.Communicator(world)
+    workers = [O.WorkerState(w) for w in range(world)]
+    for t in range(warmup):
+        O.ef_step(workers, grads, ospecs, comp, comm, 0, t)
+    times = []
+    t_start = time.perf_counter()
+    for t in range(steps):
+        t0 = time.perf_counter()
+        O.ef_step(workers, grads, ospecs, comp, comm, 0, warmup + t)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s and len(times) >= 2:
+            break
+    return times
+
+
+def run_reference(a):
+    rank_env = int(os.environ.get("RANK", "0"))
+    if rank_env != 0:
+        return 0
+    specs = catalog_specs(a.workload)
+    world = a.gpus
+    budget = 150.0
+    times = oracle_steps(specs, a.rank, world, a.steps, budget, warmup=min(a.warmup, 2))
+    ms = 1e3 * statistics.mean(times)
+    cores = cpu_threads()
+    sample = (f"{len(times)} full steps of {a.workload} r={a.rank} with {world} simulated workers "
+              f"(float64 numpy oracle of optimizer.py:110-129, OpenBLAS {cores} threads)")
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms/step", "n_gpus": a.gpus,
+        "steps": len(times), "warmup": min(a.warmup, 2), "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{a.workload} rank {a.rank}, W={world} simulated workers (CPU)",
+                   "rank": a.rank, "world": world},
+        "cpu_baseline": {"value": round(ms, 4), "unit": "ms/step", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(ms, 4), "unit": "ms/step", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1905_13727_b200 import DistributedCommunicator, PowerSGDEngine, _lib
+    from paper_1905_13727_b200.plan import ptr, stream_ptr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = DistributedCommunicator() if world > 1 else None
+    specs = catalog_specs(a.workload)
+    N, snr, smr, nbias = sizes(specs, a.rank)
+    eng = PowerSGDEngine(specs, a.rank, comm=comm, seed=0, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    eng.g[0].normal_(generator=gen)
+    eng.bias_g[0].normal_(generator=gen)
+    use_graph = world == 1 and not a.no_graph
+    if use_graph:
+        eng.capture()
+    flush = None if a.no_flush else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---------------- warm-up
+    for _ in range(a.warmup):
+        if flush is not None:
+            flush.zero_()
+        eng.run()
+    barrier()
+    eng.check()
+
+    # ---------------- timed region: K steps, L2 flushed before each
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    for k in range(a.steps):
+        if flush is not None:
+            flush.zero_()
+        starts[k].record(stream)
+        eng.run()
+        ends[k].record(stream)
+    barrier()
+    clk = clocks.stop()
+    per = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = statistics.mean(per)
+    t = torch.tensor([ms_local, statistics.median(per)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, ms_median = float(t[0]), float(t[1])
+    eng.check()
+    info = eng.plan.info
+    launches_per_step = (info.launches_ef_p + info.launches_orthogonalize + info.launches_q_ef
+                         + (info.launches_decompress if world > 1 else 0))
+
+    # ---------------- per-kernel breakdown (eager, same stream, L2 flushed)
+    lib = _lib.lib()
+    h = eng.plan.handle
+    sp = stream_ptr(stream)
+    names = ["ef_p", "orthogonalize", "q_ef"] + (["allreduce_p", "allreduce_q", "decompress"] if world > 1 else [])
+    acc = {k: [] for k in names}
+    nb = max(5, min(a.steps, 30))
+    for _ in range(nb):
+        if flush is not None:
+            flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        eng.status.zero_()
+        ev[0].record(stream)
+        _lib.check(lib.psgd_ef_p(h, ptr(eng.g[0]), ptr(eng.e[0]), ptr(eng.work[0]), ptr(eng.Q), ptr(eng.P[0]),
+                                 ptr(eng.bias_g[0]), ptr(eng.status), sp), "ef_p")
+        ev[1].record(stream)
+        if world > 1:
+            comm.all_reduce_sum_(eng.P[0])
+        ev[2].record(stream)
+        _lib.check(lib.psgd_orthogonalize(h, ptr(eng.P[0]), world, ptr(eng.repl), ptr(eng.bias_out),
+                                          ptr(eng.status), sp), "orth")
+        ev[3].record(stream)
+        qout = eng.Q if world == 1 else eng.qbuf[0]
+        _lib.check(lib.psgd_q_ef(h, ptr(eng.work[0]), ptr(eng.P[0]), ptr(qout), ptr(eng.e[0]),
+                                 ptr(eng.status), sp), "q_ef")
+        ev[4].record(stream)
+        if world > 1:
+            comm.all_reduce_sum_(eng.qbuf[0])
+            ev[5].record(stream)
+            _lib.check(lib.psgd_decompress(h, ptr(eng.P[0]), ptr(eng.qbuf[0]), world, ptr(eng.Q),
+                                           ptr(eng.work[0]), ptr(eng.status), sp), "decomp")
+            ev[6].record(stream)
+        torch.cuda.synchronize(dev)
+        acc["ef_p"].append(ev[0].elapsed_time(ev[1]))
+        acc["orthogonalize"].append(ev[2].elapsed_time(ev[3]))
+        acc["q_ef"].append(ev[3].elapsed_time(ev[4]))
+        if world > 1:
+            acc["allreduce_p"].append(ev[1].elapsed_time(ev[2]))
+            acc["allreduce_q"].append(ev[4].elapsed_time(ev[5]))
+            acc["decompress"].append(ev[5].elapsed_time(ev[6]))
+    kern_ms = {k: statistics.mean(v) for k, v in acc.items()}
+    eng.check()
+
+    # ---------------- NCCL small-message latency (context for the latency-bound collectives)
+    nccl_us = None
+    if world > 1:
+        x = torch.zeros(2, dtype=torch.float32, device=dev)
+        for _ in range(20):
+            dist.all_reduce(x)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(100):
+            dist.all_reduce(x)
+        e1.record(stream)
+        barrier()
+        nccl_us = 1e3 * e0.elapsed_time(e1) / 100
+
+    # ---------------- e2e: host gradients in, M-hat + bias mean out, every step
+    g_host = torch.empty(eng.g[0].numel(), dtype=torch.float32, pin_memory=True)
+    g_host.copy_(eng.g[0].cpu())
+    b_host = torch.empty(eng.bias_g[0].numel(), dtype=torch.float32, pin_memory=True)
+    b_host.copy_(eng.bias_g[0].cpu())
+    m_host = torch.empty(eng.work[0].numel(), dtype=torch.float32, pin_memory=True)
+    bo_host = torch.empty(eng.bias_out.numel(), dtype=torch.float32, pin_memory=True)
+    st_host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+    ke = max(3, min(a.steps, 20))
+    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
+    e_e = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
+    barrier()
+    for k in range(ke):
+        if flush is not None:
+            flush.zero_()
+        e_s[k].record(stream)
+        eng.g[0].copy_(g_host, non_blocking=True)
+        eng.bias_g[0].copy_(b_host, non_blocking=True)
+        eng.run()
+        m_host.copy_(eng.work[0], non_blocking=True)
+        bo_host.copy_(eng.bias_out, non_blocking=True)
+        st_host.copy_(eng.status, non_blocking=True)
+        e_e[k].record(stream)
+    barrier()
+    if int(st_host.item()) != 0:
+        raise RuntimeError(f"e2e step reported status {int(st_host.item())}")
+    e2e_local = statistics.mean(s.elapsed_time(e) for s, e in zip(e_s, e_e))
+    t = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t[0])
+    h2d = 4 * (g_host.numel() + b_host.numel())
+    d2h = 4 * (m_host.numel() + bo_host.numel() + st_host.numel())
+
+    # ---------------- roofline (measured peaks)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    k1_bytes = 12 * N + 4 * snr + 4 * smr + 8 * nbias
+    k3_bytes = 12 * N + 4 * snr + 4 * smr if world == 1 else 8 * N + 4 * snr + 4 * smr
+    dom = "q_ef" if kern_ms["q_ef"] >= kern_ms["ef_p"] else "ef_p"
+    dom_bytes = k3_bytes if dom == "q_ef" else k1_bytes
+    achieved = dom_bytes / (kern_ms[dom] * 1e-3) / 1e9
+    b_alg = 24 * N + 20 * snr + 16 * smr
+    t_roof_us = b_alg / (hbm * 1e9) * 1e6
+    if world > 1:
+        t_roof_us += 2 * (world - 1) / world * 4 * (snr + nbias + smr) / 900e9 * 1e6
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        times = oracle_steps(specs, a.rank, 1, 1000, a.cpu_seconds, warmup=1)
+        cores = cpu_threads()
+        cpu = {"value": round(1e3 * statistics.median(times), 3), "unit": "ms/step", "cores": cores,
+               "kind": "port",
+               "sample": f"{len(times)} full {a.workload} r={a.rank} W=1 steps (median), float64 numpy "
+                         f"oracle of optimizer.py:110-129 on {cores} OpenBLAS threads, ~{a.cpu_seconds:.0f}s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(ms, 5), "unit": "ms/step", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: seeded N(0,1) fp32 gradients of the catalog shapes, resident in HBM",
+            "impl": "ours",
+            "config": {"workload": f"{a.workload} rank {a.rank}, one worker per GPU "
+                                   + ("(configs[1], no collective)" if world == 1 else "(configs[2], NCCL AR of packed P, q)"),
+                       "rank": a.rank, "world": world, "matrix_elems": N, "bias_elems": nbias,
+                       "l2": "flushed (256 MiB write) before every timed step" if flush is not None else "not flushed",
+                       "cuda_graph": use_graph, "median_ms": round(ms_median, 5)},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
+                         "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                         "algorithmic_bytes": dom_bytes, "peak_source": peak_src},
+            "step_roofline": {"algorithmic_bytes": b_alg, "t_roof_us": round(t_roof_us, 2),
+                              "t_measured_us": round(ms * 1e3, 2), "frac": round(t_roof_us / (ms * 1e3), 4)},
+            "kernels_ms": {k: round(v, 5) for k, v in kern_ms.items()},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_ms, 4), "unit": "ms/step", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches_per_step * a.steps,
+            "clocks": clk,
+        }
+        if nccl_us is not None:
+            line["nccl_small_allreduce_us"] = round(nccl_us, 2)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse_args()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

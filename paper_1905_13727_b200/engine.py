@@ -1,0 +1,277 @@
+"""The grouped PowerSGD step: every parameter of a model in one kernel sequence.
+
+This is the fast path behind the reference's per-parameter loop
+(optimizer.py:110-129, compressors.py:369-379).  One `PowerSGDEngine` owns,
+on one device, the packed fp32 buffers of a parameter catalog:
+
+    g[w]      flat gradients of local worker w       (caller fills; `grad_view`)
+    e[w]      error-feedback memory                  (WorkerState.error, optimizer.py:63)
+    work[w]   delta, then M-hat                      (RoundTrip.aggregated)
+    P[w]      packed P + uncompressed bias tail      (AR1 payload)
+    Q         warm-start Q of every matrix           (PowerSGD.q_memory, compressors.py:357)
+    qbuf[w]   local q_w                              (AR2 payload, W > 1)
+    bias_out  mean of the bias gradients             (optimizer.py:111-113)
+
+and runs, per step,
+
+    W == 1 (one GPU)        psgd_step_single                       -- 3 kernels
+    W > 1, distributed      K1 | all_reduce(P) | K2 | K3 | all_reduce(q) | K5
+    W > 1, simulated        K1 x W | tree_mean | K2 | K3 x W | tree_mean | K5
+
+Q is seeded exactly as the reference (derive_rng(seed, "warm_start_init",
+param_index), compressors.py:362-367) and CommStats are charged exactly as the
+reference charges them (compressors.py:248-249, 374; comm.py:96).
+"""
+
+import torch
+
+from . import _lib
+from .comm import CommStats, tree_mean_
+from .linalg import ContractViolation
+from .plan import Plan, ptr, stream_ptr
+from .seeding import warm_start_q
+
+
+class NonFiniteGradient(RuntimeError):
+    """optimizer.py:31-38: a worker produced a NaN/inf gradient; names the site."""
+
+    def __init__(self, param_name, worker):
+        super().__init__(f"non-finite gradient for parameter {param_name!r} on worker {worker}")
+        self.param_name = param_name
+        self.worker = worker
+
+
+class PowerSGDEngine:
+    """Grouped, warm-started, error-feedback PowerSGD over a parameter catalog.
+
+    specs:   ParamSpec list in catalog order (param_index = position, biases included).
+    rank:    requested rank r; each matrix uses min(n, m, r) (compressors.py:359-360).
+    workers: simulated workers on this device (the reference's W-list model);
+             must be 1 when `comm` is a DistributedCommunicator.
+    comm:    Communicator / DistributedCommunicator whose CommStats are charged.
+    """
+
+    def __init__(self, specs, rank, *, workers=1, comm=None, seed=0, device=None,
+                 error_feedback=True):
+        self.specs = list(specs)
+        self.rank = int(rank)
+        if self.rank < 1:
+            raise ContractViolation(f"rank must be >= 1, got {rank}")
+        self.distributed = bool(comm is not None and getattr(comm, "distributed", False))
+        if self.distributed and workers != 1:
+            raise ValueError("a distributed worker owns exactly one local gradient set")
+        if comm is not None and not self.distributed and comm.world_size != workers:
+            raise ValueError(f"expected {comm.world_size} workers, got {workers}")
+        self.world = comm.world_size if self.distributed else int(workers)
+        self.nlocal = 1 if self.distributed else int(workers)
+        self.comm = comm
+        self.stats = comm.stats if comm is not None else CommStats()
+        self.seed = int(seed)
+        self.error_feedback = bool(error_feedback)
+
+        self.mat_index = [i for i, s in enumerate(self.specs) if not s.is_bias]
+        self.bias_index = [i for i, s in enumerate(self.specs) if s.is_bias]
+        self.slot = {pi: k for k, pi in enumerate(self.mat_index)}
+        self.bias_off = {}
+        off = 0
+        for pi in self.bias_index:
+            self.bias_off[pi] = off
+            off += self.specs[pi].size
+        self.nbias = off
+
+        shapes = [self.specs[pi].matrix_shape for pi in self.mat_index]
+        self.plan = Plan(shapes, self.rank, self.world, self.nbias, device)
+        dev = self.device = self.plan.device
+        pl = self.plan
+        z = dict(dtype=torch.float32, device=dev)
+        L = self.nlocal
+        self.g = [torch.zeros(pl.flat_elems, **z) for _ in range(L)]
+        self.e = [torch.zeros(pl.flat_elems, **z) for _ in range(L)]
+        self.work = [torch.zeros(pl.flat_elems, **z) for _ in range(L)]
+        self.bias_g = [torch.zeros(max(1, self.nbias), **z) for _ in range(L)]
+        self.P = [torch.zeros(pl.p_elems, **z) for _ in range(L)]
+        self.Pm = torch.zeros(pl.p_elems, **z) if L > 1 else self.P[0]
+        self.Q = torch.zeros(pl.q_elems, **z)
+        self.qbuf = [torch.zeros(pl.q_elems, **z) for _ in range(L)] if self.world > 1 else None
+        self.bias_out = torch.zeros(max(1, self.nbias), **z)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        # EF off: the EF output of K3 lands in a scratch buffer nobody reads
+        self._e_scratch = None if self.error_feedback else torch.empty(pl.flat_elems, **z)
+        self.repl = pl.repl_table()
+        for k, pi in enumerate(self.mat_index):
+            mi = pl.matrices[k]
+            q0 = warm_start_q(self.seed, pi, mi.m, mi.r_eff)
+            pl.q_view(self.Q, k).copy_(torch.from_numpy(q0))
+        self.step_count = 0
+        self._graph = None
+        # host-side accounting per step (integers)
+        bits = flops = dec = 0
+        for k, pi in enumerate(self.mat_index):
+            mi = pl.matrices[k]
+            n, m, r = mi.n, mi.m, mi.r_eff
+            flops += self.world * (4 * n * m * r + 2 * n * r * r + 3 * n * r)  # compressors.py:389-391
+            dec += 2 * n * m * r                                              # compressors.py:176-182
+            if self.world > 1:
+                bits += 32 * n * r + 32 * m * r                               # compressors.py:337,340
+        if self.world > 1:
+            bits += 32 * self.nbias                                           # optimizer.py:111-113
+        self._charge = (bits, flops, dec)
+
+    # ------------------------------------------------------------------ views
+    def grad_view(self, param_index, worker=0):
+        """Where worker `worker` puts the gradient of parameter `param_index` (spec shape)."""
+        s = self.specs[param_index]
+        if s.is_bias:
+            o = self.bias_off[param_index]
+            return self.bias_g[worker][o:o + s.size]
+        return self.plan.matrix_view(self.g[worker], self.slot[param_index]).view(s.shape)
+
+    def update_view(self, param_index):
+        """Aggregated update of `param_index` after a step: M-hat or the bias mean."""
+        s = self.specs[param_index]
+        if s.is_bias:
+            o = self.bias_off[param_index]
+            return self.bias_out[o:o + s.size]
+        return self.plan.matrix_view(self.work[0], self.slot[param_index]).view(s.shape)
+
+    def error_view(self, param_index, worker=0):
+        return self.plan.matrix_view(self.e[worker], self.slot[param_index])
+
+    def p_view(self, param_index):
+        """P-hat of `param_index` after a step (RoundTrip.payload.p)."""
+        return self.plan.p_view(self.Pm, self.slot[param_index])
+
+    def q_view(self, param_index):
+        """Warm-start Q of `param_index` (= Q-bar of the last step, payload.q)."""
+        return self.plan.q_view(self.Q, self.slot[param_index])
+
+    def local_q_view(self, param_index, worker=0):
+        if self.qbuf is None:
+            return self.q_view(param_index)
+        return self.plan.q_view(self.qbuf[worker], self.slot[param_index])
+
+    # ------------------------------------------------------------------ the step
+    def _enqueue(self, stream=None):
+        lib = _lib.lib()
+        pl = self.plan
+        sp = stream_ptr(stream)
+        h = pl.handle
+        e = self.e if self.error_feedback else [None] * self.nlocal
+        if self.world == 1 and self.error_feedback:
+            _lib.check(lib.psgd_step_single(h, ptr(self.g[0]), ptr(e[0]), ptr(self.work[0]), ptr(self.Q),
+                                            ptr(self.P[0]), ptr(self.bias_g[0]), ptr(self.repl),
+                                            ptr(self.bias_out), ptr(self.status), sp), "psgd_step_single")
+            return
+        if self.world == 1:
+            # error feedback off (optimizer.py:118-119): delta = g, EF output discarded
+            self.status.zero_()
+            _lib.check(lib.psgd_ef_p(h, ptr(self.g[0]), None, ptr(self.work[0]), ptr(self.Q),
+                                     ptr(self.P[0]), ptr(self.bias_g[0]), ptr(self.status), sp), "psgd_ef_p")
+            _lib.check(lib.psgd_orthogonalize(h, ptr(self.P[0]), 1, ptr(self.repl), ptr(self.bias_out),
+                                              ptr(self.status), sp), "psgd_orthogonalize")
+            _lib.check(lib.psgd_q_ef(h, ptr(self.work[0]), ptr(self.P[0]), ptr(self.Q),
+                                     ptr(self._scratch_e()), ptr(self.status), sp), "psgd_q_ef")
+            return
+        self.status.zero_()
+        for w in range(self.nlocal):
+            _lib.check(lib.psgd_ef_p(h, ptr(self.g[w]), ptr(e[w]), ptr(self.work[w]), ptr(self.Q),
+                                     ptr(self.P[w]), ptr(self.bias_g[w]), ptr(self.status), sp),
+                       "psgd_ef_p")
+        if self.distributed:
+            self.comm.all_reduce_sum_(self.P[0])
+            div = self.world
+        else:
+            tree_mean_(self.P, self.Pm, stream)
+            div = 1
+        _lib.check(lib.psgd_orthogonalize(h, ptr(self.Pm), div, ptr(self.repl), ptr(self.bias_out),
+                                          ptr(self.status), sp), "psgd_orthogonalize")
+        # with error feedback off the EF output goes to a scratch buffer (never read)
+        for w in range(self.nlocal):
+            ew = e[w] if e[w] is not None else self._scratch_e()
+            _lib.check(lib.psgd_q_ef(h, ptr(self.work[w]), ptr(self.Pm), ptr(self.qbuf[w]), ptr(ew),
+                                     ptr(self.status), sp), "psgd_q_ef")
+        if self.distributed:
+            self.comm.all_reduce_sum_(self.qbuf[0])
+            _lib.check(lib.psgd_decompress(h, ptr(self.Pm), ptr(self.qbuf[0]), self.world, ptr(self.Q),
+                                           ptr(self.work[0]), ptr(self.status), sp), "psgd_decompress")
+        else:
+            tree_mean_(self.qbuf, self.Q, stream)
+            _lib.check(lib.psgd_decompress(h, ptr(self.Pm), ptr(self.Q), 1, None, ptr(self.work[0]),
+                                           ptr(self.status), sp), "psgd_decompress")
+
+    def _scratch_e(self):
+        return self._e_scratch
+
+    def run(self, stream=None):
+        """Enqueue one step on `stream` (default: current) without synchronising."""
+        if self._graph is not None:
+            self._graph.replay()
+        else:
+            self._enqueue(stream)
+        b, f, d = self._charge
+        self.stats.bits_allreduced += b
+        self.stats.compress_flops += f
+        self.stats.decode_ops += d
+        self.step_count += 1
+
+    def step(self, check=True):
+        self.run()
+        if check:
+            self.check()
+
+    def capture(self):
+        """Capture the step into a CUDA graph (single-device modes); later `run`s replay it."""
+        if self.distributed:
+            raise NotImplementedError("graph capture of the NCCL path is not enabled")
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self._enqueue(s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self._graph = g
+        return g
+
+    # ------------------------------------------------------------------ errors
+    def check(self):
+        """Synchronise on the status word and raise what the reference would."""
+        st = int(self.status.item())
+        if self.distributed:
+            import torch.distributed as dist
+            t = torch.tensor([st], dtype=torch.int32, device=self.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.comm.group)
+            st = int(t.item())
+        if st == 0:
+            return
+        if st & (_lib.STATUS_NONFINITE_GRAD | _lib.STATUS_NONFINITE_P):
+            site = self._first_nonfinite()
+            if site is not None:
+                raise NonFiniteGradient(*site)
+            raise ContractViolation("orthogonalize input contains non-finite entries")
+        if st & _lib.STATUS_REPLACEMENT:
+            raise RuntimeError("Gram-Schmidt needed more than one replacement draw for a column")
+
+    def _first_nonfinite(self):
+        """(param name, worker) of the first non-finite gradient, worker-major as
+        optimizer.py:72-76 scans.  Error path only."""
+        local = None
+        for w in range(self.nlocal):
+            for pi, s in enumerate(self.specs):
+                if not bool(torch.isfinite(self.grad_view(pi, w)).all()):
+                    local = (w, pi)
+                    break
+            if local is not None:
+                break
+        if not self.distributed:
+            return None if local is None else (self.specs[local[1]].name, local[0])
+        import torch.distributed as dist
+        big = len(self.specs) + 1
+        mine = torch.tensor([local[1] if local is not None else big], dtype=torch.int64,
+                            device=self.device)
+        allv = [torch.zeros_like(mine) for _ in range(self.world)]
+        dist.all_gather(allv, mine, group=self.comm.group)
+        for rank, v in enumerate(allv):
+            if int(v.item()) < big:
+                return (self.specs[int(v.item())].name, rank)
+        return None
