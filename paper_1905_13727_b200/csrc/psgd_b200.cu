@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kGsThreads) k2_gs(const MatDev* __restrict__ m
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) x[i * r + j] /= nrm;
   }
+  __syncthreads();  // rows were owned per-thread above; the copy-out mapping differs
   for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) p[idx] = (float)x[idx];
 }
 
