@@ -257,20 +257,20 @@ def run_ours(a):
     ms, ms_median = float(t[0]), float(t[1])
     eng.check()
     info = eng.plan.info
-    launches_per_step = (info.launches_ef_p + info.launches_orthogonalize + info.launches_q_ef
+    launches_per_step = (info.launches_ef_p + info.launches_q_ef
                          + (info.launches_decompress if world > 1 else 0))
 
     # ---------------- per-kernel breakdown (eager, same stream, L2 flushed)
     lib = _lib.lib()
     h = eng.plan.handle
     sp = stream_ptr(stream)
-    names = ["ef_p", "orthogonalize", "q_ef"] + (["allreduce_p", "allreduce_q", "decompress"] if world > 1 else [])
+    names = ["ef_p", "q_ef"] + (["allreduce_p", "allreduce_q", "decompress"] if world > 1 else [])
     acc = {k: [] for k in names}
     nb = max(5, min(a.steps, 30))
     for _ in range(nb):
         if flush is not None:
             flush.zero_()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         eng.status.zero_()
         ev[0].record(stream)
         _lib.check(lib.psgd_ef_p(h, ptr(eng.g[0]), ptr(eng.e[0]), ptr(eng.work[0]), ptr(eng.Q), ptr(eng.P[0]),
@@ -279,27 +279,23 @@ def run_ours(a):
         if world > 1:
             comm.all_reduce_sum_(eng.P[0])
         ev[2].record(stream)
-        _lib.check(lib.psgd_orthogonalize(h, ptr(eng.P[0]), world, ptr(eng.repl), ptr(eng.bias_out),
-                                          ptr(eng.status), sp), "orth")
-        ev[3].record(stream)
         qout = eng.Q if world == 1 else eng.qbuf[0]
-        _lib.check(lib.psgd_q_ef(h, ptr(eng.work[0]), ptr(eng.P[0]), ptr(qout), ptr(eng.e[0]),
-                                 ptr(eng.status), sp), "q_ef")
-        ev[4].record(stream)
+        _lib.check(lib.psgd_q_ef(h, ptr(eng.work[0]), ptr(eng.P[0]), world, ptr(eng.repl), ptr(eng.Phat),
+                                 ptr(qout), ptr(eng.e[0]), ptr(eng.bias_out), ptr(eng.status), sp), "q_ef")
+        ev[3].record(stream)
         if world > 1:
             comm.all_reduce_sum_(eng.qbuf[0])
-            ev[5].record(stream)
-            _lib.check(lib.psgd_decompress(h, ptr(eng.P[0]), ptr(eng.qbuf[0]), world, ptr(eng.Q),
+            ev[4].record(stream)
+            _lib.check(lib.psgd_decompress(h, ptr(eng.Phat), ptr(eng.qbuf[0]), world, ptr(eng.Q),
                                            ptr(eng.work[0]), ptr(eng.status), sp), "decomp")
-            ev[6].record(stream)
+            ev[5].record(stream)
         torch.cuda.synchronize(dev)
         acc["ef_p"].append(ev[0].elapsed_time(ev[1]))
-        acc["orthogonalize"].append(ev[2].elapsed_time(ev[3]))
-        acc["q_ef"].append(ev[3].elapsed_time(ev[4]))
+        acc["q_ef"].append(ev[2].elapsed_time(ev[3]))
         if world > 1:
             acc["allreduce_p"].append(ev[1].elapsed_time(ev[2]))
-            acc["allreduce_q"].append(ev[4].elapsed_time(ev[5]))
-            acc["decompress"].append(ev[5].elapsed_time(ev[6]))
+            acc["allreduce_q"].append(ev[3].elapsed_time(ev[4]))
+            acc["decompress"].append(ev[4].elapsed_time(ev[5]))
     kern_ms = {k: statistics.mean(v) for k, v in acc.items()}
     eng.check()
 

@@ -20,8 +20,8 @@
  * Per-step call sequence (one data-parallel worker = one GPU):
  *   psgd_ef_p            delta = g + e ; P = delta Q ; bias -> P tail   (optimizer.py:115-121, compressors.py:336)
  *   [all-reduce(sum) of P incl. bias tail over the workers]              (compressors.py:337, optimizer.py:111-113)
- *   psgd_orthogonalize   P-hat = MGS(P / W) ; bias mean                   (compressors.py:338, linalg.py:61-90)
- *   psgd_q_ef            q_w = delta^T P-hat ; e = delta - P-hat q_w^T    (compressors.py:339,376-378, optimizer.py:124-127)
+ *   psgd_q_ef            P-hat = MGS(P / W) ; q_w = delta^T P-hat ;       (compressors.py:338-339, linalg.py:61-90)
+ *                        e = delta - P-hat q_w^T ; bias mean              (compressors.py:376-378, optimizer.py:124-127)
  *                        (W == 1: also M-hat and the warm-start Q; done)
  *   [all-reduce(sum) of q over the workers]                               (compressors.py:340)
  *   psgd_decompress      Q = q_sum / W (warm start) ; M-hat = P-hat Q^T   (compressors.py:373-375)
@@ -52,7 +52,7 @@ typedef struct psgd_plan psgd_plan;
 
 typedef struct {
     int64_t flat_elems;   /* length of the g / e / work buffers (matrices packed, 16-B aligned starts) */
-    int64_t p_elems;      /* length of the packed P buffer: sum n*r_eff (aligned) + bias tail */
+    int64_t p_elems;      /* length of the packed P buffer: sum n*r_eff (aligned) + bias tail + flags */
     int64_t p_bias_off;   /* offset of the bias tail inside the P buffer */
     int64_t q_elems;      /* length of the packed Q buffers: sum m*r_eff (aligned) */
     int64_t repl_elems;   /* doubles in the degenerate-column replacement table */
@@ -98,21 +98,27 @@ int psgd_plan_matrix(const psgd_plan* plan, int32_t i, psgd_matrix_info* out);
 int psgd_ef_p(const psgd_plan* plan, const float* g, const float* e, float* work,
               const float* q, float* p, const float* bias_g, int32_t* status, void* stream);
 
-/* K2 — replaces compressors.py:337-338 after the sum: P = P_sum / divisor
- * (comm.py:97-98; divisor 1 = the W=1 copy), then orthogonalize
- * (linalg.py:61-90) in float64 with the seeded replacement columns `repl`
- * (linalg.py:54-58, table laid out per psgd_matrix_info.repl_off).
- * Writes P-hat over p and the bias mean (p tail / divisor) to bias_out. */
-int psgd_orthogonalize(const psgd_plan* plan, float* p, int32_t divisor, const double* repl,
-                       float* bias_out, int32_t* status, void* stream);
+/* K2 — standalone Gram-Schmidt: replaces compressors.py:337-338 after the sum,
+ * P = P_sum / divisor (comm.py:97-98; divisor 1 = the W=1 copy), then
+ * orthogonalize (linalg.py:61-90) in float64 with the seeded replacement
+ * columns `repl` (linalg.py:54-58, laid out per psgd_matrix_info.repl_off).
+ * Writes P-hat to p_hat (may equal p) and the bias mean to bias_out.
+ * psgd_q_ef performs the same orthogonalisation itself; this entry point
+ * serves linalg.orthogonalize and callers that want P-hat alone. */
+int psgd_orthogonalize(const psgd_plan* plan, const float* p, int32_t divisor, const double* repl,
+                       float* p_hat, float* bias_out, int32_t* status, void* stream);
 
-/* K3 (+K4 for tall matrices) — replaces compressors.py:339 (q_w = delta^T P-hat),
- * :376-378 (locals = P-hat q_w^T) and optimizer.py:124-127 (e = delta - local).
- * work: in delta; when the plan's world == 1 it is overwritten with M-hat
- * (compressors.py:375, M-hat == local at W=1) and q_out is the next warm start.
- * When world > 1, q_out receives the local q_w to be all-reduced. */
-int psgd_q_ef(const psgd_plan* plan, float* work, const float* p_hat, float* q_out,
-              float* e, const int32_t* status, void* stream);
+/* K3 (+ tall-matrix kernels) — replaces compressors.py:338 (P-hat = GS(P / W)),
+ * :339 (q_w = delta^T P-hat), :376-378 (locals = P-hat q_w^T) and
+ * optimizer.py:124-127 (e = delta - local), plus the bias mean of
+ * optimizer.py:111-113.  p: the summed P buffer from psgd_ef_p (after the
+ * all-reduce when W > 1); p_hat receives P-hat; work: in delta, and when the
+ * plan's world == 1 it is overwritten with M-hat (compressors.py:375; M-hat ==
+ * local at W=1) and q_out is the next warm start.  When world > 1, q_out
+ * receives the local q_w to be all-reduced.  A non-finite gradient on any
+ * worker (flags carried in p) leaves every buffer untouched. */
+int psgd_q_ef(const psgd_plan* plan, float* work, const float* p, int32_t divisor, const double* repl,
+              float* p_hat, float* q_out, float* e, float* bias_out, int32_t* status, void* stream);
 
 /* K5 — replaces compressors.py:340 (after the sum), :373 (warm-start store)
  * and :375 (M-hat = P-hat Q-bar^T).  Q-bar = q_sum / divisor; if q_store is
@@ -121,10 +127,10 @@ int psgd_decompress(const psgd_plan* plan, const float* p_hat, const float* q_su
                     int32_t divisor, float* q_store, float* mhat, const int32_t* status,
                     void* stream);
 
-/* One W == 1 step: psgd_ef_p + psgd_orthogonalize + psgd_q_ef. */
+/* One W == 1 step: zero status, psgd_ef_p, psgd_q_ef (2 kernel launches). */
 int psgd_step_single(const psgd_plan* plan, const float* g, float* e, float* work, float* q,
-                     float* p, const float* bias_g, const double* repl, float* bias_out,
-                     int32_t* status, void* stream);
+                     float* p, float* p_hat, const float* bias_g, const double* repl,
+                     float* bias_out, int32_t* status, void* stream);
 
 /* Simulated-worker mean — replaces comm.py:84-98 (tree_reduce :51-67 then / W)
  * for the single-GPU W-list mode: out = tree_sum(bufs[0..nbuf)) / nbuf, in the

@@ -62,10 +62,10 @@ _SIGNATURES = {
     "psgd_plan_get_info": (_I32, [_P, ctypes.POINTER(PlanInfo)]),
     "psgd_plan_matrix": (_I32, [_P, _I32, ctypes.POINTER(MatrixInfo)]),
     "psgd_ef_p": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "psgd_orthogonalize": (_I32, [_P, _P, _I32, _P, _P, _P, _P]),
-    "psgd_q_ef": (_I32, [_P, _P, _P, _P, _P, _P, _P]),
+    "psgd_orthogonalize": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P]),
+    "psgd_q_ef": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "psgd_decompress": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P]),
-    "psgd_step_single": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "psgd_step_single": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psgd_tree_mean": (_I32, [ctypes.POINTER(_P), _I32, _I64, _P, _P]),
     "psgd_last_error": (ctypes.c_char_p, []),
     "psgd_version": (_I32, []),

@@ -224,13 +224,12 @@ class PowerSGD(Compressor):
                 tree_mean_(ps, pm)
             else:
                 pm, div = ps[0], 1
-            _lib.check(lib.psgd_orthogonalize(h, ptr(pm), div, ptr(repl), None, ptr(status), sp),
-                       "psgd_orthogonalize")  # :338
+            phat = torch.zeros(pl.p_elems, **f32)
             qws, escratch = [], torch.empty(pl.flat_elems, **f32)
-            for w in works:               # :339 (and the EF locals, :376-378)
+            for w in works:               # :338-339 (GS, q_w) and the EF locals (:376-378)
                 qw = torch.zeros(pl.q_elems, **f32)
-                _lib.check(lib.psgd_q_ef(h, ptr(w), ptr(pm), ptr(qw), ptr(escratch), ptr(status), sp),
-                           "psgd_q_ef")
+                _lib.check(lib.psgd_q_ef(h, ptr(w), ptr(pm), div, ptr(repl), ptr(phat), ptr(qw),
+                                         ptr(escratch), None, ptr(status), sp), "psgd_q_ef")
                 qws.append(qw)
             if world == 1:
                 qbar = qws[0]
@@ -248,14 +247,14 @@ class PowerSGD(Compressor):
                     qdiv = 1
                 agg = torch.empty(pl.flat_elems, **f32)
                 qstore = torch.zeros(pl.q_elems, **f32)
-                _lib.check(lib.psgd_decompress(h, ptr(pm), ptr(qbar), qdiv, ptr(qstore), ptr(agg),
+                _lib.check(lib.psgd_decompress(h, ptr(phat), ptr(qbar), qdiv, ptr(qstore), ptr(agg),
                                                ptr(status), sp), "psgd_decompress")
                 if qdiv != 1:
                     qbar = qstore
                 locs = []
                 for qw in qws:
                     loc = torch.empty(pl.flat_elems, **f32)
-                    _lib.check(lib.psgd_decompress(h, ptr(pm), ptr(qw), 1, None, ptr(loc), ptr(status), sp),
+                    _lib.check(lib.psgd_decompress(h, ptr(phat), ptr(qw), 1, None, ptr(loc), ptr(status), sp),
                                "psgd_decompress")
                     locs.append(loc)
         st = int(status.item())
@@ -266,7 +265,7 @@ class PowerSGD(Compressor):
         q_new = pl.q_view(qbar, 0).clone()
         self.q_memory[ctx.param_index] = q_new           # :373
         comm.stats.decode_ops += 2 * n * m * r           # :374
-        payload = LowRank(_out(pl.p_view(pm, 0).clone(), as_np), _out(q_new, as_np))
+        payload = LowRank(_out(pl.p_view(phat, 0).clone(), as_np), _out(q_new, as_np))
         return RoundTrip(_out(pl.matrix_view(agg, 0).clone(), as_np),
                          [_out(pl.matrix_view(x, 0).clone(), as_np) for x in locs], payload)
 

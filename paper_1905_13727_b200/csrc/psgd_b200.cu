@@ -1,26 +1,32 @@
 // psgd_b200.cu — B200 (sm_100a) kernels + C ABI for the PowerSGD compression hot path.
 //
 // Reference semantics: /root/reference/pkg/src/gradcomp
-//   optimizer.py:98-129   EF add, per-matrix round trip, EF update, bias all-reduce
+//   optimizer.py:98-129    EF add, per-matrix round trip, EF update, bias all-reduce
 //   compressors.py:327-379 low_rank_iteration + PowerSGD.round_trip
-//   linalg.py:54-90       modified Gram-Schmidt with seeded degenerate replacement
-//   comm.py:51-98         tree-ordered all-reduce mean
+//   linalg.py:54-90        modified Gram-Schmidt with seeded degenerate replacement
+//   comm.py:51-98          tree-ordered all-reduce mean
 //
-// Design: every kernel is HBM-bound at small rank, so the work
-// is organised around streaming each gradient element through the SM the
-// minimum number of times:
-//   K1 k1_ef_p      warp-per-row items: delta = g + e (one read of g and e, one
-//                   write of delta), P = delta Q reduced in-warp (no atomics).
-//   K2 k2_gs        one CTA per matrix, float64 MGS over the tiny P.
-//   K3 k3_q_ef      one CTA per column slab holding ALL rows of the slab in
-//                   registers: q_w = delta^T P-hat reduced in smem, then
-//                   e = delta - P-hat q_w^T (and M-hat at W=1) written from the
-//                   same registers — delta is read exactly once.  Tall matrices
-//                   (n > 512) split rows into chunks, reduce chunk partials in
-//                   fixed order by the last-arriving CTA, and take K4.
-//   K4 k4_ef        row items: e = delta - P-hat q^T (+ M-hat at W=1), tall only.
-//   K5 k5_decomp    row items: M-hat = P-hat (q_sum / W)^T, Q store (W > 1).
-// All reductions are fixed-order, so results are bitwise run-to-run stable.
+// Every kernel is HBM-bound at small rank, so the design is
+// about streaming each gradient element through an SM the minimum number of
+// times with enough bytes in flight.  The two heavy kernels are persistent,
+// warp-specialised TMA pipelines (one CTA per SM, 8 consumer warps + 1
+// producer warp, mbarrier full/empty rings):
+//
+//   K1 k1_ef_p   producer: cp.async.bulk of row-aligned chunks of g and e into
+//                smem; consumers: delta = g + e (stored, L2 evict-last so K3
+//                finds it in L2), P = delta Q reduced in-warp / in-CTA.  Each
+//                CTA also publishes a non-finite flag into the P buffer so the
+//                P all-reduce carries it to every rank (all-or-nothing step).
+//   K3 k3_q_ef   producer: one cp.async.bulk per row segment of a column slab
+//                holding ALL n rows of the slab; consumers: Gram-Schmidt of the
+//                slab's matrix (float64, once per matrix per CTA, while the
+//                slab's bytes are in flight), q_w = delta^T P-hat, then
+//                e = delta - P-hat q_w^T (and M-hat at W=1) from the same smem
+//                copy — delta is read from memory once.
+//   Tall matrices (n > 512) take K2 (per-matrix GS) + a register-slab split-n
+//   q kernel + a row-streaming EF kernel (K4).  K5 writes M-hat after the
+//   q all-reduce when W > 1.
+// All reductions are fixed-order: results are bitwise run-to-run stable.
 
 #include "../../include/psgd_b200.h"
 
@@ -28,6 +34,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -35,9 +42,16 @@
 
 namespace {
 
-constexpr int kThreads = 256;            // every kernel: 8 warps
-constexpr int kRowItemElems = 4096;      // target elements per K1/K4/K5 warp item
+constexpr int kThreads = 256;      // consumer threads / plain CTA size (8 warps)
+constexpr int kTmaThreads = 288;   // + 1 producer warp
+constexpr int kRowItemElems = 4096;
 constexpr int kGsThreads = 512;
+constexpr int kFusedNMax = 512;    // K3 fused path holds all rows of a slab
+constexpr int K1_STAGES = 4;
+constexpr int K1_CHUNK = 4608;     // floats of g (and of e) per chunk
+constexpr int K1_STAGE_FLOATS = K1_CHUNK + 16;
+constexpr int K3_STAGES = 2;
+constexpr int K3_QMAX = 512;       // C * r per slab
 
 thread_local std::string g_last_error;
 
@@ -56,33 +70,96 @@ int fail(int code, const std::string& msg) {
 struct MatDev {
   long long flat_off, p_off, q_off, repl_off;
   int n, m, r, tall;
+  int lg1, pad0, pad1, pad2;  // lg1: log2 lanes per row in K1 (2..8)
 };
 
-// K1 / K4 / K5 work item: `nrows` rows of matrix `mat` starting at `row0`,
-// processed by one warp with 2^lg lanes per row.  mat < 0: bias chunk
-// [row0, row0 + nrows) of the bias vector (K1 only).
-struct RowItem {
+struct RowItem {   // K4 / K5 warp item: rows [row0, row0 + nrows) of `mat`, 2^lg lanes per row
   int mat, row0, nrows, lg;
 };
 
-// K3 work item: rows [chunk * rows_per_chunk, ...) x columns [c0, c0 + C) of `mat`,
-// C = vec << cq_log2.  nchunks > 1: tall matrix, partial written at ws_off.
-struct SlabItem {
+struct Chunk1 {    // K1 chunk: rows [row0, row0+nrows) x cols [c0, c0+ncols) of `mat`
+  long long off;   // flat element offset of the first element
+  int mat, row0, nrows, c0, ncols;
+  int split, part;  // split >= 0: a segment of an over-long row (partial P)
+  int pad;
+};
+
+struct SplitRow {  // an over-long row whose P is combined from `parts` partials
+  int mat, row, base, parts;
+};
+
+struct Slab3 {     // K3 fused slab: all n rows x cols [c0, c0 + ncols) of `mat`
+  int mat, c0, ncols, cql, vec, first, pad0, pad1;
+};
+
+struct SlabItem {  // tall-matrix split-n q item (register slab)
   long long ws_off;
   int mat, c0, chunk, nchunks, slab, vec, cq_log2, pad;
 };
 
-struct Group {       // a contiguous run of items sharing r_eff
-  int r, beg, end;
-  int smem;          // K3 only: dynamic shared memory bytes
+struct Group {
+  int r, beg, end, smem;
 };
 
 __host__ __device__ constexpr int k3_dcap(int r) { return r <= 4 ? 64 : 32; }
 
-// ----------------------------------------------------------------------------- helpers
+// ----------------------------------------------------------------------------- PTX helpers
 
-__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
-__device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t pol_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 1-D bulk copy global -> shared, completion counted on an mbarrier (TMA, SASS UBLKCP)
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_hint(float4* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
 
@@ -93,190 +170,321 @@ __device__ __forceinline__ bool finite4(float4 v) {
   return finite1(v.x) & finite1(v.y) & finite1(v.z) & finite1(v.w);
 }
 
-// Q rows j0..j0+3 (4*r consecutive floats starting at q) -> qv[4][R].
-template <int R, bool EXACT>
+// Q rows j0..j0+3 (4*r consecutive floats at q) -> qv[4][RM]; r <= RM.
+template <int RM>
 __device__ __forceinline__ void load_q4(const float* __restrict__ q, bool aligned, int r,
-                                        float (&qv)[4][R]) {
-  if (EXACT && aligned) {
+                                        float (&qv)[4][RM]) {
+  if (r == RM && aligned) {
 #pragma unroll
-    for (int t = 0; t < R; ++t) {
+    for (int t = 0; t < RM; ++t) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(q) + t);
       const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) qv[(4 * t + u) / R][(4 * t + u) % R] = vv[u];
+      for (int u = 0; u < 4; ++u) qv[(4 * t + u) / RM][(4 * t + u) % RM] = vv[u];
     }
   } else {
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
-      for (int k = 0; k < R; ++k)
-        qv[jj][k] = (EXACT || k < r) ? __ldg(q + jj * r + k) : 0.f;
+      for (int k = 0; k < RM; ++k) qv[jj][k] = k < r ? __ldg(q + jj * r + k) : 0.f;
+  }
+}
+
+// ----------------------------------------------------------------------------- Gram-Schmidt
+// linalg.py:61-90: in-order MODIFIED Gram-Schmidt on x (n x r row-major,
+// float64, smem or global); thread `tid` of `nth` owns rows tid + k*nth, so
+// only the reductions need barriers.  Degenerate columns (norm <
+// 1e-12 (before + 1), linalg.py:15,82) are replaced by the attempt-0 seeded
+// column from `repl` (column-major, n per column); a second degenerate draw
+// sets PSGD_STATUS_REPLACEMENT.
+
+struct BlockReducer {  // all threads of the CTA, __syncthreads
+  double* red;         // >= 32 doubles
+  __device__ double sum(double v) const {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += red[w];
+    __syncthreads();
+    return t;
+  }
+};
+
+struct ConsumerReducer {  // the 256 consumer threads of a TMA CTA, named barrier 1
+  double* red;            // 2 x 8 doubles (double-buffered by call parity)
+  int* parity;
+  __device__ double sum(double v) const {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* buf = red + 8 * (*parity & 1);
+    ++*parity;
+    if (lane == 0) buf[warp] = v;
+    bar_consumers();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += buf[w];
+    return t;
+  }
+};
+
+template <class Red>
+__device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ repl, int tid, int nth,
+                            const Red& red, int* status) {
+  for (int j = 0; j < r; ++j) {
+    double s = 0.0;
+    for (int i = tid; i < n; i += nth) s += x[i * r + j] * x[i * r + j];
+    double before = sqrt(red.sum(s));
+    double nrm = before;
+    if (j > 0) {
+      for (int i2 = 0; i2 < j; ++i2) {
+        s = 0.0;
+        for (int i = tid; i < n; i += nth) s += x[i * r + i2] * x[i * r + j];
+        const double c = red.sum(s);
+        for (int i = tid; i < n; i += nth) x[i * r + j] -= c * x[i * r + i2];
+      }
+      s = 0.0;
+      for (int i = tid; i < n; i += nth) s += x[i * r + j] * x[i * r + j];
+      nrm = sqrt(red.sum(s));
+    }
+    int attempt = 0;
+    while (nrm < 1e-12 * (before + 1.0)) {
+      if (attempt > 0) {
+        if (tid == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
+        break;
+      }
+      for (int i = tid; i < n; i += nth) x[i * r + j] = repl[(long long)j * n + i];
+      before = 1.0;
+      for (int i2 = 0; i2 < j; ++i2) {
+        s = 0.0;
+        for (int i = tid; i < n; i += nth) s += x[i * r + i2] * x[i * r + j];
+        const double c = red.sum(s);
+        for (int i = tid; i < n; i += nth) x[i * r + j] -= c * x[i * r + i2];
+      }
+      s = 0.0;
+      for (int i = tid; i < n; i += nth) s += x[i * r + j] * x[i * r + j];
+      nrm = sqrt(red.sum(s));
+      ++attempt;
+    }
+    for (int i = tid; i < n; i += nth) x[i * r + j] /= nrm;
   }
 }
 
 // ============================================================================= K1
 // delta = g + e ; P[i,:] = sum_j delta[i,j] Q[j,:]   (optimizer.py:120, compressors.py:336)
 
-template <int R, bool EXACT>
-__device__ __forceinline__ void k1_rows(const MatDev& md, const RowItem& it, int lane,
-                                        const float* __restrict__ g, const float* __restrict__ e,
-                                        float* __restrict__ work, const float* __restrict__ Qall,
-                                        float* __restrict__ Pall, bool& bad) {
-  const int r = EXACT ? R : md.r;
-  const int m = md.m;
-  const int lg = it.lg;
-  const int G = 1 << lg;
-  const int gl = lane & (G - 1);
-  const int sub = lane >> lg;
-  const int rpp = 32 >> lg;
-  const float* __restrict__ Q = Qall + md.q_off;
-  for (int rb = 0; rb < it.nrows; rb += rpp) {
-    const int li = rb + sub;
-    const bool active = li < it.nrows;
-    const int i = it.row0 + li;
-    float acc[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) acc[k] = 0.f;
-    if (active) {
-      const long long o = md.flat_off + (long long)i * m;
-      const int head = min((int)((4 - (o & 3)) & 3), m);
-      const int body4 = (m - head) >> 2;
-      const int tail = m - head - 4 * body4;
-      // scalar head / tail (rows whose start is not 16-B aligned, e.g. m = 27, 650)
-      for (int s = gl; s < head + tail; s += G) {
-        const int j = s < head ? s : head + 4 * body4 + (s - head);
-        const float gv = ld_stream(g + o + j);
-        const float d = e ? gv + ld_stream(e + o + j) : gv;
-        bad |= !finite1(gv);
-        work[o + j] = d;
-#pragma unroll
-        for (int k = 0; k < R; ++k)
-          if (EXACT || k < r) acc[k] = fmaf(d, __ldg(Q + (long long)j * r + k), acc[k]);
+struct K1Smem {
+  float g[K1_STAGES][K1_STAGE_FLOATS];
+  float e[K1_STAGES][K1_STAGE_FLOATS];
+  float red[2][8][PSGD_MAX_RANK];
+  uint64_t full[K1_STAGES];
+  uint64_t empty[K1_STAGES];
+  int flag;
+};
+
+template <int RM>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    k1_ef_p(const MatDev* __restrict__ mats, const Chunk1* __restrict__ chunks,
+            const int* __restrict__ cta_beg, const SplitRow* __restrict__ splits,
+            const float* __restrict__ g, const float* __restrict__ e, float* __restrict__ work,
+            const float* __restrict__ Q, float* __restrict__ P, float* __restrict__ psplit,
+            int* __restrict__ split_cnt, const float* __restrict__ bias_g, long long nbias,
+            long long bias_off, long long flag_off, int* status) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  K1Smem& S = *reinterpret_cast<K1Smem*>(smem_raw);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int cb = cta_beg[blockIdx.x], ce = cta_beg[blockIdx.x + 1];
+  if (t == 0) {
+    for (int s = 0; s < K1_STAGES; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], 8);
+    }
+    S.flag = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_trigger();  // let the next kernel's CTAs stage in as ours retire
+
+  if (warp == 8) {  // ---------------- producer
+    if (lane == 0) {
+      const uint64_t pol = pol_evict_first();
+      for (int k = cb; k < ce; ++k) {
+        const int s = (k - cb) % K1_STAGES;
+        const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
+        mbar_wait(&S.empty[s], ph ^ 1);
+        const Chunk1 ch = chunks[k];
+        const int m = mats[ch.mat].m;
+        const long long a4 = ch.off & ~3LL;
+        const long long span = (long long)(ch.nrows - 1) * m + ch.ncols;
+        const long long b4 = (ch.off + span + 3) & ~3LL;
+        const uint32_t bytes = (uint32_t)((b4 - a4) * 4);
+        mbar_expect_tx(&S.full[s], e ? 2 * bytes : bytes);
+        tma_load(S.g[s], g + a4, bytes, &S.full[s], pol);
+        if (e) tma_load(S.e[s], e + a4, bytes, &S.full[s], pol);
       }
-      const float4* __restrict__ g4 = reinterpret_cast<const float4*>(g + o + head);
-      const float4* __restrict__ e4 = e ? reinterpret_cast<const float4*>(e + o + head) : nullptr;
-      float4* __restrict__ w4 = reinterpret_cast<float4*>(work + o + head);
-      const float* __restrict__ qrow = Q + (long long)head * r;
-      const bool qal = ((head * r) & 3) == 0;
-      int c = gl;
-      // 4 independent 16-B loads of g and of e in flight per lane
-      for (; c + 3 * G < body4; c += 4 * G) {
-        float4 gv[4], ev[4];
+    }
+    return;
+  }
+
+  // ---------------- consumers (256 threads)
+  bool bad = false;
+  for (long long x = (long long)blockIdx.x * kThreads + t; x < nbias; x += (long long)gridDim.x * kThreads) {
+    const float v = bias_g[x];  // bias rides in the P all-reduce (optimizer.py:111-113)
+    bad |= !finite1(v);
+    P[bias_off + x] = v;
+  }
+  const uint64_t keep = pol_evict_last();
+  int rpar = 0;
+  for (int k = cb; k < ce; ++k) {
+    const int s = (k - cb) % K1_STAGES;
+    const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
+    const Chunk1 ch = chunks[k];
+    const MatDev md = mats[ch.mat];
+    const int r = md.r, m = md.m;
+    const float* __restrict__ Qm = Q + md.q_off;
+    const int lg = md.lg1;
+    const int G = 1 << lg;
+    const int gl = t & (G - 1);
+    const int gid = t >> lg;
+    const int rpp = kThreads >> lg;
+    const long long a4 = ch.off & ~3LL;
+    mbar_wait(&S.full[s], ph);
+    const float* __restrict__ sg = S.g[s];
+    const float* __restrict__ se = S.e[s];
+    for (int rb = 0; rb < ch.nrows; rb += rpp) {
+      const int li = rb + gid;
+      const bool active = li < ch.nrows;
+      float acc[RM];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) gv[u] = ld_stream(g4 + c + u * G);
+      for (int q = 0; q < RM; ++q) acc[q] = 0.f;
+      if (active) {
+        const long long og = ch.off + (long long)li * m;
+        const int sm = (int)(og - a4);
+        const int nc = ch.ncols;
+        const int head = min((int)((4 - (og & 3)) & 3), nc);
+        const int body4 = (nc - head) >> 2;
+        const int tail = nc - head - 4 * body4;
+        for (int x = gl; x < head + tail; x += G) {
+          const int j = x < head ? x : head + 4 * body4 + (x - head);
+          const float gv = sg[sm + j];
+          const float d = e ? gv + se[sm + j] : gv;
+          bad |= !finite1(gv);
+          st_hint(work + og + j, d, keep);
+          const float* qj = Qm + (long long)(ch.c0 + j) * r;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          ev[u] = e4 ? ld_stream(e4 + c + u * G) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int q = 0; q < RM; ++q)
+            if (q < r) acc[q] = fmaf(d, __ldg(qj + q), acc[q]);
+        }
+        const float4* __restrict__ g4 = reinterpret_cast<const float4*>(sg + sm + head);
+        const float4* __restrict__ e4 = reinterpret_cast<const float4*>(se + sm + head);
+        float4* __restrict__ w4 = reinterpret_cast<float4*>(work + og + head);
+        const float* __restrict__ qrow = Qm + (long long)(ch.c0 + head) * r;
+        const bool qal = (((ch.c0 + head) * r + (int)(md.q_off & 3)) & 3) == 0;
+#pragma unroll 2
+        for (int c = gl; c < body4; c += G) {
+          const float4 gv = g4[c];
+          const float4 ev = e ? e4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 d = make_float4(gv.x + ev.x, gv.y + ev.y, gv.z + ev.z, gv.w + ev.w);
+          bad |= !finite4(gv);
+          st_hint(w4 + c, d, keep);
+          float qv[4][RM];
+          load_q4<RM>(qrow + (long long)(4 * c) * r, qal, r, qv);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 d = make_float4(gv[u].x + ev[u].x, gv[u].y + ev[u].y, gv[u].z + ev[u].z,
-                                       gv[u].w + ev[u].w);
-          bad |= !finite4(gv[u]);
-          w4[c + u * G] = d;
-          float qv[4][R];
-          load_q4<R, EXACT>(qrow + (long long)(4 * (c + u * G)) * r, qal, r, qv);
-#pragma unroll
-          for (int k = 0; k < R; ++k) {
-            acc[k] = fmaf(d.x, qv[0][k], acc[k]);
-            acc[k] = fmaf(d.y, qv[1][k], acc[k]);
-            acc[k] = fmaf(d.z, qv[2][k], acc[k]);
-            acc[k] = fmaf(d.w, qv[3][k], acc[k]);
+          for (int q = 0; q < RM; ++q) {
+            acc[q] = fmaf(d.x, qv[0][q], acc[q]);
+            acc[q] = fmaf(d.y, qv[1][q], acc[q]);
+            acc[q] = fmaf(d.z, qv[2][q], acc[q]);
+            acc[q] = fmaf(d.w, qv[3][q], acc[q]);
           }
         }
       }
-      for (; c < body4; c += G) {
-        const float4 gv = ld_stream(g4 + c);
-        const float4 ev = e4 ? ld_stream(e4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 d = make_float4(gv.x + ev.x, gv.y + ev.y, gv.z + ev.z, gv.w + ev.w);
-        bad |= !finite4(gv);
-        w4[c] = d;
-        float qv[4][R];
-        load_q4<R, EXACT>(qrow + (long long)(4 * c) * r, qal, r, qv);
+      // fixed-order reduction across the row group
+      if (G <= 32) {
+        for (int off = G >> 1; off > 0; off >>= 1)
 #pragma unroll
-        for (int k = 0; k < R; ++k) {
-          acc[k] = fmaf(d.x, qv[0][k], acc[k]);
-          acc[k] = fmaf(d.y, qv[1][k], acc[k]);
-          acc[k] = fmaf(d.z, qv[2][k], acc[k]);
-          acc[k] = fmaf(d.w, qv[3][k], acc[k]);
+          for (int q = 0; q < RM; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+      } else {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+          for (int q = 0; q < RM; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+        float(*red)[PSGD_MAX_RANK] = S.red[rpar & 1];
+        ++rpar;
+        if (lane == 0) {
+#pragma unroll
+          for (int q = 0; q < RM; ++q) red[warp][q] = acc[q];
+        }
+        bar_consumers();
+        if (gl == 0) {
+          const int nw = G >> 5;
+#pragma unroll
+          for (int q = 0; q < RM; ++q) {
+            float sacc = 0.f;
+            for (int w = 0; w < nw; ++w) sacc += red[warp + w][q];
+            acc[q] = sacc;
+          }
+        }
+      }
+      if (active && gl == 0) {
+        if (ch.split < 0) {
+          float* dst = P + md.p_off + (long long)(ch.row0 + li) * r;
+#pragma unroll
+          for (int q = 0; q < RM; ++q)
+            if (q < r) dst[q] = acc[q];
+        } else {  // segment of an over-long row: the last-arriving segment combines in part order
+          const SplitRow sp = splits[ch.split];
+#pragma unroll
+          for (int q = 0; q < RM; ++q)
+            if (q < r) psplit[(long long)(sp.base + ch.part) * r + q] = acc[q];
+          __threadfence();
+          if (atomicAdd(split_cnt + ch.split, 1) == sp.parts - 1) {
+            __threadfence();
+            for (int q = 0; q < r; ++q) {
+              float sacc = 0.f;
+              for (int p = 0; p < sp.parts; ++p) sacc += __ldcg(psplit + (long long)(sp.base + p) * r + q);
+              P[md.p_off + (long long)sp.row * r + q] = sacc;
+            }
+            split_cnt[ch.split] = 0;
+          }
         }
       }
     }
-    // fixed-order butterfly inside the 2^lg-lane group
-    for (int off = G >> 1; off > 0; off >>= 1)
-#pragma unroll
-      for (int k = 0; k < R; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
-    if (active && gl == 0) {
-#pragma unroll
-      for (int k = 0; k < R; ++k)
-        if (EXACT || k < r) Pall[md.p_off + (long long)i * r + k] = acc[k];
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[s]);
   }
-}
-
-template <int R, bool EXACT>
-__global__ void __launch_bounds__(kThreads) k1_ef_p(const MatDev* __restrict__ mats,
-                                                    const RowItem* __restrict__ items, int beg,
-                                                    int end, const float* __restrict__ g,
-                                                    const float* __restrict__ e,
-                                                    float* __restrict__ work,
-                                                    const float* __restrict__ Q,
-                                                    float* __restrict__ P,
-                                                    const float* __restrict__ bias_g,
-                                                    long long bias_off, int* status) {
-  const int lane = threadIdx.x & 31;
-  const int wi = beg + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-  bool bad = false;
-  if (wi < end) {
-    const RowItem it = items[wi];
-    if (it.mat < 0) {  // bias chunk -> P tail (packed into the P all-reduce, optimizer.py:111-113)
-      for (int x = lane; x < it.nrows; x += 32) {
-        const float v = bias_g[it.row0 + x];
-        bad |= !finite1(v);
-        P[bias_off + it.row0 + x] = v;
-      }
-    } else {
-      const MatDev md = mats[it.mat];
-      k1_rows<R, EXACT>(md, it, lane, g, e, work, Q, P, bad);
-    }
+  if (bad) atomicOr(&S.flag, 1);
+  bar_consumers();
+  if (t == 0) {
+    P[flag_off + blockIdx.x] = S.flag ? 1.f : 0.f;  // carried to every rank by the P all-reduce
+    if (S.flag) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
   }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
 }
 
 // ============================================================================= K2
-// P-hat = MGS(P / W)   (comm.py:97-98, linalg.py:61-90), float64 inside.
+// standalone / tall-matrix Gram-Schmidt: P-hat = MGS(P / W)  (comm.py:97-98, linalg.py:61-90)
 
-__device__ double block_sum(double v, double* red) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (warp == 0) {
-    double t = lane < nw ? red[lane] : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-    if (lane == 0) red[32] = t;
+__global__ void __launch_bounds__(kGsThreads)
+    k2_gs(const MatDev* __restrict__ mats, const int* __restrict__ list, int nlist,
+          const float* __restrict__ P, float* __restrict__ Phat, int divisor,
+          const double* __restrict__ repl, double* __restrict__ ws, float* __restrict__ bias_out,
+          long long bias_off, long long nbias, long long flag_off, int nflags, int* status) {
+  __shared__ double red[40];
+  {
+    int bad = 0;  // a non-finite gradient anywhere (any rank) poisons the whole step
+    for (int x = threadIdx.x; x < nflags; x += blockDim.x) bad |= P[flag_off + x] != 0.f;
+    if (__syncthreads_or(bad) || (*status & PSGD_STATUS_NONFINITE_GRAD)) {
+      if (threadIdx.x == 0 && bad) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+      return;
+    }
   }
-  __syncthreads();
-  const double out = red[32];
-  __syncthreads();
-  return out;
-}
-
-__global__ void __launch_bounds__(kGsThreads) k2_gs(const MatDev* __restrict__ mats, int nmat,
-                                                    float* __restrict__ P, int divisor,
-                                                    const double* __restrict__ repl,
-                                                    double* __restrict__ ws,
-                                                    float* __restrict__ bias_out,
-                                                    long long bias_off, long long nbias,
-                                                    int* status) {
-  __shared__ double red[33];
-  if (*status & PSGD_STATUS_NONFINITE_GRAD) return;
   const double div = (double)divisor;
-  if ((int)blockIdx.x >= nmat) {  // bias mean: P tail / W
-    const long long nb = gridDim.x - nmat;
+  if ((int)blockIdx.x >= nlist) {  // bias mean: P tail / W
+    const long long nb = gridDim.x - nlist;
     bool bad = false;
-    for (long long x = (blockIdx.x - nmat) * (long long)blockDim.x + threadIdx.x; x < nbias;
+    for (long long x = (blockIdx.x - nlist) * (long long)blockDim.x + threadIdx.x; x < nbias;
          x += nb * blockDim.x) {
       const float v = P[bias_off + x];
       bad |= !finite1(v);
@@ -285,13 +493,12 @@ __global__ void __launch_bounds__(kGsThreads) k2_gs(const MatDev* __restrict__ m
     if (bad) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
     return;
   }
-  const MatDev md = mats[blockIdx.x];
+  const MatDev md = mats[list[blockIdx.x]];
   const int n = md.n, r = md.r;
-  double* __restrict__ x = ws + md.p_off;  // row-major n x r, same indexing as P
-  float* __restrict__ p = P + md.p_off;
+  double* __restrict__ x = ws + md.p_off;
   int bad = 0;
   for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
-    const float v = p[idx];
+    const float v = P[md.p_off + idx];
     bad |= !finite1(v);
     x[idx] = (double)v / div;
   }
@@ -299,61 +506,259 @@ __global__ void __launch_bounds__(kGsThreads) k2_gs(const MatDev* __restrict__ m
     if (threadIdx.x == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
     return;
   }
-  // Each thread owns rows i = tid + k * blockDim for the whole kernel, so the
-  // elementwise updates need no barrier beyond the ones inside block_sum.
-  for (int j = 0; j < r; ++j) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i * r + j] * x[i * r + j];
-    double before = sqrt(block_sum(s, red));
-    for (int i2 = 0; i2 < j; ++i2) {
-      s = 0.0;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i * r + i2] * x[i * r + j];
-      const double c = block_sum(s, red);
-      for (int i = threadIdx.x; i < n; i += blockDim.x) x[i * r + j] -= c * x[i * r + i2];
-    }
-    s = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i * r + j] * x[i * r + j];
-    double nrm = sqrt(block_sum(s, red));
-    int attempt = 0;
-    while (nrm < 1e-12 * (before + 1.0)) {  // DEGENERATE_EPS, linalg.py:15,82
-      if (attempt > 0) {                     // table holds attempt 0 only
-        if (threadIdx.x == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
-        break;
-      }
-      for (int i = threadIdx.x; i < n; i += blockDim.x)
-        x[i * r + j] = repl[md.repl_off + (long long)j * n + i];
-      before = 1.0;
-      for (int i2 = 0; i2 < j; ++i2) {
-        s = 0.0;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i * r + i2] * x[i * r + j];
-        const double c = block_sum(s, red);
-        for (int i = threadIdx.x; i < n; i += blockDim.x) x[i * r + j] -= c * x[i * r + i2];
-      }
-      s = 0.0;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i * r + j] * x[i * r + j];
-      nrm = sqrt(block_sum(s, red));
-      ++attempt;
-    }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i * r + j] /= nrm;
-  }
-  __syncthreads();  // rows were owned per-thread above; the copy-out mapping differs
-  for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) p[idx] = (float)x[idx];
+  BlockReducer br{red};
+  mgs_inplace(x, n, r, repl + md.repl_off, threadIdx.x, blockDim.x, br, status);
+  __syncthreads();  // rows were thread-owned above; the copy-out mapping differs
+  for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) Phat[md.p_off + idx] = (float)x[idx];
 }
 
-// ============================================================================= K3
-// q_w = delta^T P-hat over a column slab holding all (or a chunk of) rows;
-// fused e = delta - P-hat q_w^T (+ M-hat when W == 1)   (compressors.py:339,375-378)
+// ============================================================================= K3 (fused)
+// per slab (all n rows x C cols): [GS of the matrix if new to this CTA] ;
+// q_w = delta^T P-hat ; e = delta - P-hat q_w^T ; M-hat (W=1)   (compressors.py:338-339,375-378)
+
+struct K3Layout {  // byte offsets inside dynamic smem
+  int stage_floats;
+  int off_gs, off_ps, off_red, off_qs, off_dred, off_bar, total;
+};
+
+template <int RM>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    k3_q_ef(const MatDev* __restrict__ mats, const Slab3* __restrict__ slabs,
+            const int* __restrict__ cta_beg, K3Layout L, float* __restrict__ work,
+            const float* __restrict__ P, int divisor, const double* __restrict__ repl,
+            float* __restrict__ Phat, float* __restrict__ qout, float* __restrict__ e,
+            float* __restrict__ bias_out, long long nbias, long long bias_off, long long flag_off,
+            int nflags, int write_mhat, int* status) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage0 = reinterpret_cast<float*>(smem_raw);
+  double* gsd = reinterpret_cast<double*>(smem_raw + L.off_gs);
+  float* ps = reinterpret_cast<float*>(smem_raw + L.off_ps);
+  float* red = reinterpret_cast<float*>(smem_raw + L.off_red);
+  float* qs = reinterpret_cast<float*>(smem_raw + L.off_qs);
+  double* dred = reinterpret_cast<double*>(smem_raw + L.off_dred);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
+  uint64_t* empty = full + K3_STAGES;
+
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int cb = cta_beg[blockIdx.x], ce = cta_beg[blockIdx.x + 1];
+  if (t == 0) {
+    for (int s = 0; s < K3_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  pdl_wait();  // K1's delta / P (or the all-reduce) must be complete and visible
+  {
+    int bad = 0;
+    for (int x = t; x < nflags; x += kTmaThreads) bad |= P[flag_off + x] != 0.f;
+    if (__syncthreads_or(bad)) {  // optimizer.py:72-76: nothing is mutated
+      if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+      return;
+    }
+  }
+
+  if (warp == 8) {  // ---------------- producer: one bulk copy per row segment
+    const uint64_t pol = pol_evict_first();
+    for (int k = cb; k < ce; ++k) {
+      const int s = (k - cb) % K3_STAGES;
+      const uint32_t ph = ((k - cb) / K3_STAGES) & 1;
+      const Slab3 sl = slabs[k];
+      const MatDev md = mats[sl.mat];
+      const int C = sl.vec << sl.cql;
+      const int stride = C + 8;
+      if (lane == 0) mbar_wait(&empty[s], ph ^ 1);
+      __syncwarp();
+      uint32_t bytes = 0;
+      for (int i = lane; i < md.n; i += 32) {
+        const long long st = md.flat_off + (long long)i * md.m + sl.c0;
+        bytes += (uint32_t)((((st + sl.ncols + 3) & ~3LL) - (st & ~3LL)) * 4);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
+      if (lane == 0) mbar_expect_tx(&full[s], bytes);
+      __syncwarp();
+      float* stg = stage0 + (long long)s * L.stage_floats;
+      for (int i = lane; i < md.n; i += 32) {
+        const long long st = md.flat_off + (long long)i * md.m + sl.c0;
+        const long long a4 = st & ~3LL;
+        const uint32_t b = (uint32_t)((((st + sl.ncols + 3) & ~3LL) - a4) * 4);
+        tma_load(stg + i * stride, work + a4, b, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  {
+    bool bad = false;
+    for (long long x = (long long)blockIdx.x * kThreads + t; x < nbias; x += (long long)gridDim.x * kThreads) {
+      const float v = P[bias_off + x];
+      bad |= !finite1(v);
+      bias_out[x] = divisor == 1 ? v : v / (float)divisor;
+    }
+    if (bad) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+  }
+  int rpar = 0;
+  ConsumerReducer cr{dred, &rpar};
+  int cur = -1;
+  bool skip = false;
+  const double div = (double)divisor;
+  for (int k = cb; k < ce; ++k) {
+    const int s = (k - cb) % K3_STAGES;
+    const uint32_t ph = ((k - cb) / K3_STAGES) & 1;
+    const Slab3 sl = slabs[k];
+    const MatDev md = mats[sl.mat];
+    const int n = md.n, m = md.m, r = md.r;
+    if (sl.mat != cur) {  // ---- Gram-Schmidt of this matrix (overlaps the slab's TMA)
+      cur = sl.mat;
+      bar_consumers();  // previous slab's readers of ps are done
+      int bad = 0;
+      for (int idx = t; idx < n * r; idx += kThreads) {
+        const float v = P[md.p_off + idx];
+        bad |= !finite1(v);
+        gsd[idx] = (double)v / div;
+      }
+      skip = cr.sum(bad ? 1.0 : 0.0) != 0.0;
+      if (skip) {
+        if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
+      } else {
+        mgs_inplace(gsd, n, r, repl + md.repl_off, t, kThreads, cr, status);
+        bar_consumers();
+        for (int idx = t; idx < n * r; idx += kThreads) {
+          const float v = (float)gsd[idx];
+          ps[idx] = v;
+          if (sl.first) Phat[md.p_off + idx] = v;
+        }
+        bar_consumers();
+      }
+    }
+    mbar_wait(&full[s], ph);
+    const float* stg = stage0 + (long long)s * L.stage_floats;
+    if (!skip) {
+      const int vec = sl.vec, cql = sl.cql;
+      const int CQ = 1 << cql, C = vec << cql, RG = kThreads >> cql, stride = C + 8;
+      const int cq = t & (CQ - 1), rg = t >> cql;
+      const int col = cq * vec;
+      const bool colok = col < sl.ncols;
+      float qp[4][RM];
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int q = 0; q < RM; ++q) qp[v][q] = 0.f;
+      if (colok) {
+        if (vec == 4) {
+          for (int i = rg; i < n; i += RG) {
+            const float4 d = *reinterpret_cast<const float4*>(stg + i * stride + col);
+            const float dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+            for (int q = 0; q < RM; ++q) {
+              if (q < r) {
+                const float pk = ps[i * r + q];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) qp[v][q] = fmaf(dv[v], pk, qp[v][q]);
+              }
+            }
+          }
+        } else {
+          for (int i = rg; i < n; i += RG) {
+            const int dl = (int)((md.flat_off + (long long)i * m + sl.c0) & 3);
+            const float d = stg[i * stride + dl + col];
+#pragma unroll
+            for (int q = 0; q < RM; ++q)
+              if (q < r) qp[0][q] = fmaf(d, ps[i * r + q], qp[0][q]);
+          }
+        }
+      }
+      // fixed-order reduction: in-warp over row groups sharing cq, then over warps
+      if (CQ < 32) {
+        for (int off = CQ; off < 32; off <<= 1)
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+#pragma unroll
+            for (int q = 0; q < RM; ++q) qp[v][q] += __shfl_xor_sync(0xffffffffu, qp[v][q], off);
+      }
+      if (CQ >= 32 || lane < CQ) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+          for (int q = 0; q < RM; ++q)
+            if (v < vec && q < r) red[warp * K3_QMAX + (col + v) * r + q] = qp[v][q];
+      }
+      bar_consumers();
+      for (int o = t; o < C * r; o += kThreads) {
+        const int cqo = (o / r) / vec;
+        float sacc = 0.f;
+        if (CQ <= 32) {
+#pragma unroll
+          for (int w = 0; w < 8; ++w) sacc += red[w * K3_QMAX + o];
+        } else {
+          const int per = CQ >> 5;  // warps per row group
+          for (int w = (cqo >> 5); w < 8; w += per) sacc += red[w * K3_QMAX + o];
+        }
+        qs[o] = sacc;
+      }
+      bar_consumers();
+      {
+        float* qd = qout + md.q_off + (long long)sl.c0 * r;
+        for (int o = t; o < sl.ncols * r; o += kThreads) qd[o] = qs[o];
+      }
+      // error feedback (and M-hat at W=1) from the same smem copy of delta
+      if (colok) {
+        float qv[4][RM];
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+          for (int q = 0; q < RM; ++q) qv[v][q] = (v < vec && q < r) ? qs[(col + v) * r + q] : 0.f;
+        if (vec == 4) {
+          for (int i = rg; i < n; i += RG) {
+            const float4 d = *reinterpret_cast<const float4*>(stg + i * stride + col);
+            float mh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int q = 0; q < RM; ++q) {
+              if (q < r) {
+                const float pk = ps[i * r + q];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) mh[v] = fmaf(pk, qv[v][q], mh[v]);
+              }
+            }
+            const long long a = md.flat_off + (long long)i * m + sl.c0 + col;
+            st_stream(reinterpret_cast<float4*>(e + a),
+                      make_float4(d.x - mh[0], d.y - mh[1], d.z - mh[2], d.w - mh[3]));
+            if (write_mhat)
+              st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
+          }
+        } else {
+          for (int i = rg; i < n; i += RG) {
+            const long long a0 = md.flat_off + (long long)i * m + sl.c0;
+            const float d = stg[i * stride + (int)(a0 & 3) + col];
+            float mh = 0.f;
+#pragma unroll
+            for (int q = 0; q < RM; ++q)
+              if (q < r) mh = fmaf(ps[i * r + q], qv[0][q], mh);
+            st_stream(e + a0 + col, d - mh);
+            if (write_mhat) st_stream(work + a0 + col, mh);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+// ============================================================================= tall path
+// split-n q partials for matrices with n > kFusedNMax (register slab, last CTA reduces)
 
 template <int R, bool EXACT>
 __global__ void __launch_bounds__(kThreads, 2)
-    k3_q_ef(const MatDev* __restrict__ mats, const SlabItem* __restrict__ items, int beg,
-            float* __restrict__ work, const float* __restrict__ Phat, float* __restrict__ qout,
-            float* __restrict__ e, float* __restrict__ wsq, int* __restrict__ counters,
-            int write_mhat, const int* __restrict__ status) {
+    k3_tall(const MatDev* __restrict__ mats, const SlabItem* __restrict__ items,
+            const float* __restrict__ work, const float* __restrict__ Phat, float* __restrict__ qout,
+            float* __restrict__ wsq, int* __restrict__ counters, const int* __restrict__ status) {
   constexpr int DCAP = k3_dcap(R);
   extern __shared__ float smem[];
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
-  const SlabItem it = items[beg + blockIdx.x];
+  const SlabItem it = items[blockIdx.x];
   const MatDev md = mats[it.mat];
   const int r = EXACT ? R : md.r;
   const int n = md.n, m = md.m;
@@ -372,12 +777,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int rbeg = it.chunk * rows_chunk;
   const int nrows = min(n - rbeg, rows_chunk);
   const int ncols = min(C, m - it.c0);
+  float* ps = smem;
+  float* red = ps + rows_chunk * r;
+  float* qs = red + RG * C * r;
 
-  float* ps = smem;                           // nrows x r   (P-hat rows of this chunk)
-  float* red = ps + rows_chunk * r;           // RG x C x r  (per-row-group partial q)
-  float* qs = red + RG * C * r;               // C x r       (q of this slab)
-
-  // 1. all loads of the slab in flight at once
   float d[DCAP];
   const long long base = md.flat_off + (long long)rbeg * m + col;
   if (vec == 4) {
@@ -385,23 +788,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int s = 0; s < DCAP / 4; ++s) {
       const int li = rg + RG * s;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (colok && li < nrows) v = __ldcs(reinterpret_cast<const float4*>(work + base + (long long)li * m));
+      if (colok && li < nrows) v = __ldcg(reinterpret_cast<const float4*>(work + base + (long long)li * m));
       d[4 * s + 0] = v.x; d[4 * s + 1] = v.y; d[4 * s + 2] = v.z; d[4 * s + 3] = v.w;
     }
   } else {
 #pragma unroll
     for (int s = 0; s < DCAP; ++s) {
       const int li = rg + RG * s;
-      d[s] = (colok && li < nrows) ? __ldcs(work + base + (long long)li * m) : 0.f;
+      d[s] = (colok && li < nrows) ? __ldcg(work + base + (long long)li * m) : 0.f;
     }
   }
-  // 2. P-hat rows of the chunk to smem (overlaps the loads above)
   {
     const float* src = Phat + md.p_off + (long long)rbeg * r;
     for (int x = t; x < nrows * r; x += kThreads) ps[x] = src[x];
   }
   __syncthreads();
-  // 3. per-thread partial q over its rows
   float qp[4][R];
 #pragma unroll
   for (int v = 0; v < 4; ++v)
@@ -433,7 +834,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
   }
-  // 4. fixed-order reduction over the row groups
 #pragma unroll
   for (int v = 0; v < 4; ++v)
 #pragma unroll
@@ -446,82 +846,28 @@ __global__ void __launch_bounds__(kThreads, 2)
     qs[o] = s;
   }
   __syncthreads();
-
   float* __restrict__ qdst = qout + md.q_off + (long long)it.c0 * r;
-  if (it.nchunks > 1) {
-    // tall matrix: publish the chunk partial; the last CTA of the slab reduces
-    // all partials in chunk order (deterministic) and writes q.
-    float* part = wsq + it.ws_off;
-    for (int o = t; o < ncols * r; o += kThreads) part[(long long)it.chunk * C * r + o] = qs[o];
+  float* part = wsq + it.ws_off;
+  for (int o = t; o < ncols * r; o += kThreads) part[(long long)it.chunk * C * r + o] = qs[o];
+  __threadfence();
+  __syncthreads();
+  __shared__ int is_last;
+  if (t == 0) is_last = atomicAdd(counters + it.slab, 1) == it.nchunks - 1;
+  __syncthreads();
+  if (is_last) {
     __threadfence();
-    __syncthreads();
-    __shared__ int is_last;
-    if (t == 0) is_last = atomicAdd(counters + it.slab, 1) == it.nchunks - 1;
-    __syncthreads();
-    if (is_last) {
-      __threadfence();
-      for (int o = t; o < ncols * r; o += kThreads) {
-        float s = 0.f;
-        for (int ch = 0; ch < it.nchunks; ++ch) s += __ldcg(part + (long long)ch * C * r + o);
-        qdst[o] = s;
-      }
-      if (t == 0) counters[it.slab] = 0;  // self-resetting for the next launch
+    for (int o = t; o < ncols * r; o += kThreads) {
+      float s = 0.f;
+      for (int ch = 0; ch < it.nchunks; ++ch) s += __ldcg(part + (long long)ch * C * r + o);
+      qdst[o] = s;
     }
-    return;
-  }
-  for (int o = t; o < ncols * r; o += kThreads) qdst[o] = qs[o];
-
-  // 5. error feedback (and M-hat at W=1) from the registers
-  float qv[4][R];
-#pragma unroll
-  for (int v = 0; v < 4; ++v)
-#pragma unroll
-    for (int k = 0; k < R; ++k)
-      qv[v][k] = (v < vec && (EXACT || k < r)) ? qs[(cq * vec + v) * r + k] : 0.f;
-  if (!colok) return;
-  if (vec == 4) {
-#pragma unroll
-    for (int s = 0; s < DCAP / 4; ++s) {
-      const int li = rg + RG * s;
-      if (li < nrows) {
-        float mh[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          if (EXACT || k < r) {
-            const float pk = ps[li * r + k];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) mh[v] = fmaf(pk, qv[v][k], mh[v]);
-          }
-        }
-        const long long a = base + (long long)li * m;
-        st_stream(reinterpret_cast<float4*>(e + a),
-                  make_float4(d[4 * s] - mh[0], d[4 * s + 1] - mh[1], d[4 * s + 2] - mh[2],
-                              d[4 * s + 3] - mh[3]));
-        if (write_mhat)
-          st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
-      }
-    }
-  } else {
-#pragma unroll
-    for (int s = 0; s < DCAP; ++s) {
-      const int li = rg + RG * s;
-      if (li < nrows) {
-        float mh = 0.f;
-#pragma unroll
-        for (int k = 0; k < R; ++k)
-          if (EXACT || k < r) mh = fmaf(ps[li * r + k], qv[0][k], mh);
-        const long long a = base + (long long)li * m;
-        st_stream(e + a, d[s] - mh);
-        if (write_mhat) st_stream(work + a, mh);
-      }
-    }
+    if (t == 0) counters[it.slab] = 0;
   }
 }
 
-// ============================================================================= K4 / K5
-// Row-streaming outer products.  mode 0 (K4): e = delta - P-hat q^T, and M-hat
-// in place of delta when write_mhat.  mode 1 (K5): M-hat = P-hat (q / div)^T,
-// items with row0 == 0 also store Q-bar = q / div.
+// K4 / K5 row streaming.  MODE 0 (K4): e = delta - P-hat q^T (+ M-hat in place
+// when write_mhat).  MODE 1 (K5): M-hat = P-hat (q / div)^T; items with
+// row0 == 0 store Q-bar = q / div.
 
 template <int R, bool EXACT, int MODE>
 __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ mats,
@@ -540,7 +886,6 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
   const MatDev md = mats[it.mat];
   const int r = EXACT ? R : md.r;
   const int m = md.m;
-  const float inv = 1.0f / (float)divisor;
   const float* __restrict__ Q = qsrc + md.q_off;
   if (MODE == 1 && it.row0 == 0 && qstore != nullptr && qstore != qsrc) {
     for (int x = lane; x < m * r; x += 32) {
@@ -559,7 +904,8 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
     const int i = it.row0 + li;
     float ph[R];
 #pragma unroll
-    for (int k = 0; k < R; ++k) ph[k] = (EXACT || k < r) ? __ldg(Phat + md.p_off + (long long)i * r + k) : 0.f;
+    for (int k = 0; k < R; ++k)
+      ph[k] = (EXACT || k < r) ? __ldg(Phat + md.p_off + (long long)i * r + k) : 0.f;
     const long long o = md.flat_off + (long long)i * m;
     const int head = min((int)((4 - (o & 3)) & 3), m);
     const int body4 = (m - head) >> 2;
@@ -584,12 +930,19 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
       }
     }
     const float* __restrict__ qrow = Q + (long long)head * r;
-    const bool qal = ((head * r) & 3) == 0;
+    const bool qal = ((head * r + (int)(md.q_off & 3)) & 3) == 0;
     float4* __restrict__ w4 = reinterpret_cast<float4*>(work + o + head);
     float4* __restrict__ e4 = reinterpret_cast<float4*>(e + o + head);
     for (int c = gl; c < body4; c += G) {
       float qv[4][R];
-      load_q4<R, EXACT>(qrow + (long long)(4 * c) * r, qal, r, qv);
+      if (EXACT) {
+        load_q4<R>(qrow + (long long)(4 * c) * r, qal, R, qv);
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int k = 0; k < R; ++k) qv[jj][k] = k < r ? __ldg(qrow + (long long)(4 * c + jj) * r + k) : 0.f;
+      }
       float mh[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int k = 0; k < R; ++k) {
@@ -609,7 +962,6 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
       }
     }
   }
-  (void)inv;
 }
 
 // ============================================================================= tree mean
@@ -650,24 +1002,49 @@ int dispatch_r(int r, A... args) {
   }
 }
 
+int rmax_of(int r) { return r <= 1 ? 1 : r <= 2 ? 2 : r <= 4 ? 4 : r <= 8 ? 8 : 16; }
+
 }  // namespace
 
 // ============================================================================= plan
 
 struct psgd_plan {
-  int nmat = 0, rank = 0, world = 1, device = 0;
-  long long nbias = 0, flat_elems = 0, p_elems = 0, p_bias_off = 0, q_elems = 0, repl_elems = 0;
+  int nmat = 0, rank = 0, world = 1, device = 0, nsm = 148;
+  long long nbias = 0, flat_elems = 0, p_elems = 0, p_bias_off = 0, flag_off = 0, q_elems = 0,
+            repl_elems = 0;
+  int nflags = 0;
+  int rmax = 1;
   std::vector<MatDev> mats;
-  std::vector<RowItem> k1, k4, k5;
-  std::vector<SlabItem> k3;
-  std::vector<Group> g1, g3, g4, g5;
+  // K1
+  std::vector<Chunk1> k1;
+  std::vector<int> k1_beg;
+  std::vector<SplitRow> splits;
+  long long psplit_elems = 0;
+  // K3 fused
+  std::vector<Slab3> k3;
+  std::vector<int> k3_beg;
+  K3Layout k3l{};
+  // tall path
+  std::vector<int> tall_list, all_list;
+  std::vector<SlabItem> k3t;
+  std::vector<Group> g3t;
+  std::vector<RowItem> k4, k5;
+  std::vector<Group> g4, g5;
   int n_tall = 0, n_tall_slabs = 0;
   long long wsq_elems = 0;
   // device
   void* dev_block = nullptr;
   MatDev* d_mats = nullptr;
-  RowItem *d_k1 = nullptr, *d_k4 = nullptr, *d_k5 = nullptr;
-  SlabItem* d_k3 = nullptr;
+  Chunk1* d_k1 = nullptr;
+  int* d_k1_beg = nullptr;
+  SplitRow* d_splits = nullptr;
+  float* d_psplit = nullptr;
+  int* d_split_cnt = nullptr;
+  Slab3* d_k3 = nullptr;
+  int* d_k3_beg = nullptr;
+  int *d_tall_list = nullptr, *d_all_list = nullptr;
+  SlabItem* d_k3t = nullptr;
+  RowItem *d_k4 = nullptr, *d_k5 = nullptr;
   double* d_gsws = nullptr;
   float* d_wsq = nullptr;
   int* d_counters = nullptr;
@@ -677,41 +1054,15 @@ namespace {
 
 long long align4(long long x) { return (x + 3) & ~3LL; }
 
-int lanes_log2_for(int m) {
-  // lanes per row: enough that each lane streams ~4 float4 per row, 4..32
-  const long long per = (m + 15) / 16;
+int lanes_log2_for(int m, int max_lg) {
+  const long long per = (m + 15) / 16;  // ~4 float4 per lane per row
   int lg = 2;
-  while ((1 << lg) < per && lg < 5) ++lg;
+  while ((1LL << lg) < per && lg < max_lg) ++lg;
   return lg;
-}
-
-struct K3Cfg {
-  int vec, cql, rows_chunk, nchunks;
-};
-
-// K3 geometry of one matrix: as many columns per CTA as possible while the CTA
-// still holds all n rows (RG * smax >= n); at least 32 columns per row segment
-// (one 128-B line); never wider than needed to cover m.
-K3Cfg k3_config(int n, int m, int r) {
-  const int vec = (m % 4 == 0) ? 4 : 1;
-  const int smax = k3_dcap(r) / vec;
-  int cql = vec == 4 ? 3 : 5;
-  while (cql < 8) {
-    const int cq2 = 1 << (cql + 1);
-    const int rg2 = kThreads / cq2;
-    if ((long long)rg2 * smax < n) break;
-    if ((long long)(cq2 / 2) * vec >= m) break;
-    if (r > 8 && cq2 * vec > 256) break;  // smem budget at high rank
-    ++cql;
-  }
-  const int RG = kThreads >> cql;
-  const int rows_chunk = RG * smax;
-  return {vec, cql, rows_chunk, (n + rows_chunk - 1) / rows_chunk};
 }
 
 void build_row_items(const std::vector<MatDev>& mats, bool tall_only, std::vector<RowItem>& items,
                      std::vector<Group>& groups) {
-  // group by r so each launch is one template instantiation
   std::vector<int> rs;
   for (auto& md : mats)
     if (!tall_only || md.tall)
@@ -721,7 +1072,7 @@ void build_row_items(const std::vector<MatDev>& mats, bool tall_only, std::vecto
     for (int mi = 0; mi < (int)mats.size(); ++mi) {
       const MatDev& md = mats[mi];
       if (md.r != r || (tall_only && !md.tall)) continue;
-      const int lg = lanes_log2_for(md.m);
+      const int lg = lanes_log2_for(md.m, 5);
       const int rpp = 32 >> lg;
       int rows = std::max(1, kRowItemElems / md.m);
       rows = ((rows + rpp - 1) / rpp) * rpp;
@@ -732,11 +1083,57 @@ void build_row_items(const std::vector<MatDev>& mats, bool tall_only, std::vecto
   }
 }
 
+// contiguous ranges of items with ~equal weight, one per CTA
+std::vector<int> balance(const std::vector<double>& w, int ctas) {
+  const int n = (int)w.size();
+  std::vector<int> beg(1, 0);
+  if (n == 0) {
+    beg.push_back(0);
+    return beg;
+  }
+  ctas = std::max(1, std::min(ctas, n));
+  double total = 0;
+  for (double x : w) total += x;
+  double acc = 0;
+  int b = 1;
+  for (int i = 0; i < n && b < ctas; ++i) {
+    acc += w[i];
+    if (acc >= total * b / ctas && i + 1 < n) {
+      beg.push_back(i + 1);
+      ++b;
+    }
+  }
+  beg.push_back(n);
+  return beg;
+}
+
+struct K3Cfg {
+  int vec, cql, rows_chunk, nchunks;
+};
+
+// tall-path geometry (register slab): RG * smax rows per chunk
+K3Cfg k3_tall_config(int n, int m, int r) {
+  const int vec = (m % 4 == 0) ? 4 : 1;
+  const int smax = k3_dcap(r) / vec;
+  int cql = vec == 4 ? 3 : 5;
+  while (cql < 8) {
+    const int cq2 = 1 << (cql + 1);
+    const int rg2 = kThreads / cq2;
+    if ((long long)rg2 * smax < n) break;
+    if ((long long)(cq2 / 2) * vec >= m) break;
+    if (r > 8 && cq2 * vec > 256) break;
+    ++cql;
+  }
+  const int RG = kThreads >> cql;
+  const int rows_chunk = RG * smax;
+  return {vec, cql, rows_chunk, (n + rows_chunk - 1) / rows_chunk};
+}
+
 }  // namespace
 
 extern "C" {
 
-int32_t psgd_version(void) { return 1; }
+int32_t psgd_version(void) { return 2; }
 
 const char* psgd_last_error(void) { return g_last_error.c_str(); }
 
@@ -754,6 +1151,9 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->world = world;
   pl->nbias = nbias;
   cudaGetDevice(&pl->device);
+  if (cudaDeviceGetAttribute(&pl->nsm, cudaDevAttrMultiProcessorCount, pl->device) != cudaSuccess || pl->nsm <= 0)
+    pl->nsm = 148;
+  cudaGetLastError();
   long long fo = 0, po = 0, qo = 0, ro = 0;
   for (int i = 0; i < nmat; ++i) {
     if (n[i] < 1 || m[i] < 1 || n[i] > (1LL << 26) || m[i] > (1LL << 26)) {
@@ -768,7 +1168,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       delete pl;
       return fail(PSGD_EINVAL, "effective rank " + std::to_string(md.r) + " exceeds PSGD_MAX_RANK");
     }
-    md.tall = k3_config(md.n, md.m, md.r).nchunks > 1;
+    md.tall = md.n > kFusedNMax;
+    md.lg1 = lanes_log2_for(md.m, 8);
     md.flat_off = fo;
     md.p_off = po;
     md.q_off = qo;
@@ -778,72 +1179,141 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     qo = align4(qo + (long long)md.m * md.r);
     ro += (long long)md.n * md.r;
     pl->n_tall += md.tall;
+    pl->rmax = std::max(pl->rmax, rmax_of(md.r));
+    pl->all_list.push_back(i);
+    if (md.tall) pl->tall_list.push_back(i);
     pl->mats.push_back(md);
   }
-  pl->flat_elems = fo;
+  pl->flat_elems = std::max(4LL, fo);
+
+  // ---- K1 chunks: row-aligned, <= K1_CHUNK floats; over-long rows split into segments
+  const int seg = K1_CHUNK - 8;
+  for (int mi = 0; mi < nmat; ++mi) {
+    const MatDev& md = pl->mats[mi];
+    if (md.m <= seg) {
+      const int rows = std::max(1, seg / md.m);
+      for (int r0 = 0; r0 < md.n; r0 += rows) {
+        const int nr = std::min(rows, md.n - r0);
+        pl->k1.push_back({md.flat_off + (long long)r0 * md.m, mi, r0, nr, 0, md.m, -1, 0, 0});
+      }
+    } else {
+      const int parts = (md.m + seg - 1) / seg;
+      for (int row = 0; row < md.n; ++row) {
+        const int sid = (int)pl->splits.size();
+        pl->splits.push_back({mi, row, (int)(pl->psplit_elems / md.r), parts});
+        pl->psplit_elems += (long long)parts * md.r;
+        for (int p = 0; p < parts; ++p) {
+          const int c0 = p * seg;
+          const int nc = std::min(seg, md.m - c0);
+          pl->k1.push_back({md.flat_off + (long long)row * md.m + c0, mi, row, 1, c0, nc, sid, p, 0});
+        }
+      }
+    }
+  }
+  {
+    std::vector<double> w;
+    for (auto& c : pl->k1) w.push_back((double)c.nrows * c.ncols + 64.0);
+    pl->k1_beg = balance(w, pl->nsm);
+  }
+  pl->nflags = std::max(1, (int)pl->k1_beg.size() - 1);
   pl->p_bias_off = po;
-  pl->p_elems = std::max(1LL, po + nbias);
-  pl->q_elems = std::max(1LL, qo);
+  pl->flag_off = align4(po + nbias);
+  pl->p_elems = pl->flag_off + align4(pl->nflags);
+  pl->q_elems = std::max(4LL, qo);
   pl->repl_elems = std::max(1LL, ro);
 
-  // K1 items (+ bias chunks in the first group)
-  build_row_items(pl->mats, false, pl->k1, pl->g1);
-  if (nbias > 0) {
-    if (pl->g1.empty()) pl->g1.push_back({1, 0, 0, 0});
-    Group& g0 = pl->g1.front();
-    std::vector<RowItem> bias;
-    for (long long b = 0; b < nbias; b += kRowItemElems)
-      bias.push_back({-1, (int)b, (int)std::min<long long>(kRowItemElems, nbias - b), 0});
-    pl->k1.insert(pl->k1.begin() + g0.end, bias.begin(), bias.end());
-    const int add = (int)bias.size();
-    g0.end += add;
-    for (size_t gi = 1; gi < pl->g1.size(); ++gi) { pl->g1[gi].beg += add; pl->g1[gi].end += add; }
+  // ---- K3 fused slabs (n <= kFusedNMax)
+  {
+    const int cmax512 = pl->rmax <= 8 ? 32 : 16;  // C at n = 512
+    const int stage_floats = kFusedNMax * (cmax512 + 8);
+    std::vector<double> w;
+    for (int mi = 0; mi < nmat; ++mi) {
+      const MatDev& md = pl->mats[mi];
+      if (md.tall) continue;
+      const int vec = (md.m % 4 == 0) ? 4 : 1;
+      // widest power-of-two C that fits the stage, keeps C * r <= K3_QMAX,
+      // is not wider than needed for m, and maps onto 256 threads (CQ <= 256)
+      int cql = vec == 4 ? 2 : 4;
+      while (cql < 8) {
+        const int C2 = vec << (cql + 1);
+        if ((long long)md.n * (C2 + 8) > stage_floats) break;
+        if ((long long)C2 * md.r > K3_QMAX) break;
+        if ((vec << cql) >= md.m) break;
+        ++cql;
+      }
+      const int C = vec << cql;
+      for (int c0 = 0; c0 < md.m; c0 += C) {
+        pl->k3.push_back({mi, c0, std::min(C, md.m - c0), cql, vec, c0 == 0 ? 1 : 0, 0, 0});
+        w.push_back((double)md.n * std::min(C, md.m - c0) + 256.0);
+      }
+    }
+    pl->k3_beg = balance(w, pl->nsm);
+    K3Layout& L = pl->k3l;
+    L.stage_floats = stage_floats;
+    int off = K3_STAGES * stage_floats * 4;
+    L.off_gs = off;   off += kFusedNMax * pl->rmax * 8;
+    L.off_ps = off;   off += kFusedNMax * pl->rmax * 4;
+    L.off_red = off;  off += 8 * K3_QMAX * 4;
+    L.off_qs = off;   off += K3_QMAX * 4;
+    L.off_dred = off; off += 16 * 8;
+    L.off_bar = off;  off += 2 * K3_STAGES * 8 + 16;
+    L.total = off;
+  }
+
+  // ---- tall path: split-n q items, K4 rows; K5 rows for every matrix
+  {
+    std::vector<int> rs;
+    for (auto& md : pl->mats)
+      if (md.tall && std::find(rs.begin(), rs.end(), md.r) == rs.end()) rs.push_back(md.r);
+    for (int r : rs) {
+      Group gp{r, (int)pl->k3t.size(), 0, 0};
+      for (int mi = 0; mi < nmat; ++mi) {
+        const MatDev& md = pl->mats[mi];
+        if (!md.tall || md.r != r) continue;
+        const K3Cfg cf = k3_tall_config(md.n, md.m, r);
+        const int CQ = 1 << cf.cql, C = CQ * cf.vec, RG = kThreads / CQ;
+        const int nslab = (md.m + C - 1) / C;
+        for (int s = 0; s < nslab; ++s) {
+          const int slab_id = pl->n_tall_slabs++;
+          const long long wo = pl->wsq_elems;
+          pl->wsq_elems += (long long)cf.nchunks * C * r;
+          for (int ch = 0; ch < cf.nchunks; ++ch)
+            pl->k3t.push_back({wo, mi, s * C, ch, cf.nchunks, slab_id, cf.vec, cf.cql, 0});
+        }
+        const int smem = (cf.rows_chunk * r + RG * C * r + C * r) * (int)sizeof(float);
+        gp.smem = std::max(gp.smem, smem);
+      }
+      gp.end = (int)pl->k3t.size();
+      pl->g3t.push_back(gp);
+    }
   }
   build_row_items(pl->mats, true, pl->k4, pl->g4);
   build_row_items(pl->mats, false, pl->k5, pl->g5);
 
-  // K3 slab items
-  {
-    std::vector<int> rs;
-    for (auto& md : pl->mats)
-      if (std::find(rs.begin(), rs.end(), md.r) == rs.end()) rs.push_back(md.r);
-    for (int r : rs) {
-      Group gp{r, (int)pl->k3.size(), 0, 0};
-      for (int mi = 0; mi < nmat; ++mi) {
-        const MatDev& md = pl->mats[mi];
-        if (md.r != r) continue;
-        const K3Cfg cf = k3_config(md.n, md.m, r);
-        const int vec = cf.vec, cql = cf.cql;
-        const int CQ = 1 << cql, C = CQ * vec, RG = kThreads / CQ;
-        const int rows_chunk = cf.rows_chunk;
-        const int nchunks = cf.nchunks;
-        const int nslab = (md.m + C - 1) / C;
-        for (int s = 0; s < nslab; ++s) {
-          const int slab_id = nchunks > 1 ? pl->n_tall_slabs++ : -1;
-          const long long wo = nchunks > 1 ? pl->wsq_elems : 0;
-          if (nchunks > 1) pl->wsq_elems += (long long)nchunks * C * r;
-          for (int ch = 0; ch < nchunks; ++ch)
-            pl->k3.push_back({wo, mi, s * C, ch, nchunks, slab_id, vec, cql, 0});
-        }
-        const int smem = (rows_chunk * r + RG * C * r + C * r) * (int)sizeof(float);
-        gp.smem = std::max(gp.smem, smem);
-      }
-      gp.end = (int)pl->k3.size();
-      pl->g3.push_back(gp);
-    }
-  }
-
-  // device block: mats | k1 | k3 | k4 | k5 | gs ws (doubles) | wsq | counters
+  // ---- device block
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t off = 0;
-  const size_t o_mats = off; off = al(off + pl->mats.size() * sizeof(MatDev));
-  const size_t o_k1 = off; off = al(off + pl->k1.size() * sizeof(RowItem));
-  const size_t o_k3 = off; off = al(off + pl->k3.size() * sizeof(SlabItem));
-  const size_t o_k4 = off; off = al(off + pl->k4.size() * sizeof(RowItem));
-  const size_t o_k5 = off; off = al(off + pl->k5.size() * sizeof(RowItem));
-  const size_t o_gs = off; off = al(off + (size_t)pl->p_elems * sizeof(double));
-  const size_t o_wsq = off; off = al(off + (size_t)std::max(1LL, pl->wsq_elems) * sizeof(float));
-  const size_t o_cnt = off; off = al(off + (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = al(off + std::max<size_t>(bytes, 16));
+    return o;
+  };
+  const size_t o_mats = take(pl->mats.size() * sizeof(MatDev));
+  const size_t o_k1 = take(pl->k1.size() * sizeof(Chunk1));
+  const size_t o_k1b = take(pl->k1_beg.size() * sizeof(int));
+  const size_t o_spl = take(pl->splits.size() * sizeof(SplitRow));
+  const size_t o_psp = take((size_t)pl->psplit_elems * sizeof(float));
+  const size_t o_spc = take(pl->splits.size() * sizeof(int));
+  const size_t o_k3 = take(pl->k3.size() * sizeof(Slab3));
+  const size_t o_k3b = take(pl->k3_beg.size() * sizeof(int));
+  const size_t o_tl = take(pl->tall_list.size() * sizeof(int));
+  const size_t o_al = take(pl->all_list.size() * sizeof(int));
+  const size_t o_k3t = take(pl->k3t.size() * sizeof(SlabItem));
+  const size_t o_k4 = take(pl->k4.size() * sizeof(RowItem));
+  const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
+  const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
+  const size_t o_wsq = take((size_t)std::max(1LL, pl->wsq_elems) * sizeof(float));
+  const size_t o_cnt = take((size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
   cudaError_t ce = cudaMalloc(&pl->dev_block, off);
   if (ce != cudaSuccess) {
     delete pl;
@@ -851,8 +1321,16 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   }
   char* b = static_cast<char*>(pl->dev_block);
   pl->d_mats = reinterpret_cast<MatDev*>(b + o_mats);
-  pl->d_k1 = reinterpret_cast<RowItem*>(b + o_k1);
-  pl->d_k3 = reinterpret_cast<SlabItem*>(b + o_k3);
+  pl->d_k1 = reinterpret_cast<Chunk1*>(b + o_k1);
+  pl->d_k1_beg = reinterpret_cast<int*>(b + o_k1b);
+  pl->d_splits = reinterpret_cast<SplitRow*>(b + o_spl);
+  pl->d_psplit = reinterpret_cast<float*>(b + o_psp);
+  pl->d_split_cnt = reinterpret_cast<int*>(b + o_spc);
+  pl->d_k3 = reinterpret_cast<Slab3*>(b + o_k3);
+  pl->d_k3_beg = reinterpret_cast<int*>(b + o_k3b);
+  pl->d_tall_list = reinterpret_cast<int*>(b + o_tl);
+  pl->d_all_list = reinterpret_cast<int*>(b + o_al);
+  pl->d_k3t = reinterpret_cast<SlabItem*>(b + o_k3t);
   pl->d_k4 = reinterpret_cast<RowItem*>(b + o_k4);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
@@ -861,13 +1339,20 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   auto up = [&](void* dst, const void* src, size_t bytes) {
     return bytes ? cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
   };
-  if ((ce = up(pl->d_mats, pl->mats.data(), pl->mats.size() * sizeof(MatDev))) != cudaSuccess ||
-      (ce = up(pl->d_k1, pl->k1.data(), pl->k1.size() * sizeof(RowItem))) != cudaSuccess ||
-      (ce = up(pl->d_k3, pl->k3.data(), pl->k3.size() * sizeof(SlabItem))) != cudaSuccess ||
-      (ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem))) != cudaSuccess ||
-      (ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem))) != cudaSuccess ||
-      (ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int))) !=
-          cudaSuccess) {
+  ce = up(pl->d_mats, pl->mats.data(), pl->mats.size() * sizeof(MatDev));
+  if (ce == cudaSuccess) ce = up(pl->d_k1, pl->k1.data(), pl->k1.size() * sizeof(Chunk1));
+  if (ce == cudaSuccess) ce = up(pl->d_k1_beg, pl->k1_beg.data(), pl->k1_beg.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_splits, pl->splits.data(), pl->splits.size() * sizeof(SplitRow));
+  if (ce == cudaSuccess) ce = up(pl->d_k3, pl->k3.data(), pl->k3.size() * sizeof(Slab3));
+  if (ce == cudaSuccess) ce = up(pl->d_k3_beg, pl->k3_beg.data(), pl->k3_beg.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_tall_list, pl->tall_list.data(), pl->tall_list.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_all_list, pl->all_list.data(), pl->all_list.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_k3t, pl->k3t.data(), pl->k3t.size() * sizeof(SlabItem));
+  if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
+  if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
+  if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
+  if (ce == cudaSuccess) ce = cudaMemset(pl->d_split_cnt, 0, std::max<size_t>(16, pl->splits.size() * sizeof(int)));
+  if (ce != cudaSuccess) {
     cudaFree(pl->dev_block);
     delete pl;
     return fail(PSGD_ECUDA, std::string("plan upload: ") + cudaGetErrorString(ce));
@@ -896,15 +1381,17 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->world = pl->world;
   o->n_tall = pl->n_tall;
   o->items_k1 = (int64_t)pl->k1.size();
-  o->items_k3 = (int64_t)pl->k3.size();
+  o->items_k3 = (int64_t)(pl->k3.size() + pl->k3t.size());
   auto nonempty = [](const std::vector<Group>& gs) {
     int c = 0;
     for (const Group& g : gs) c += g.end > g.beg;
     return c;
   };
-  o->launches_ef_p = nonempty(pl->g1);
+  const bool fused = !pl->k3.empty();
+  o->launches_ef_p = (pl->k1.empty() && pl->nbias == 0) ? 0 : 1;
   o->launches_orthogonalize = (pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0;
-  o->launches_q_ef = nonempty(pl->g3) + nonempty(pl->g4);
+  o->launches_q_ef = (fused ? 1 : 0) + ((pl->n_tall > 0 || (!fused && pl->nbias > 0)) ? 1 : 0) +
+                     nonempty(pl->g3t) + nonempty(pl->g4);
   o->launches_decompress = nonempty(pl->g5);
   return PSGD_OK;
 }
@@ -930,32 +1417,65 @@ int psgd_plan_matrix(const psgd_plan* pl, int32_t i, psgd_matrix_info* o) {
 
 namespace {
 
-template <int R, bool EXACT>
-struct RunK1 {
-  static int run(const psgd_plan* pl, const Group& gp, const float* g, const float* e, float* work,
-                 const float* q, float* p, const float* bias_g, int* status, cudaStream_t st) {
-    const int nitems = gp.end - gp.beg;
-    if (nitems <= 0) return PSGD_OK;
-    const int blocks = (nitems + 7) / 8;
-    k1_ef_p<R, EXACT><<<blocks, kThreads, 0, st>>>(pl->d_mats, pl->d_k1, gp.beg, gp.end, g, e,
-                                                   work, q, p, bias_g, pl->p_bias_off, status);
-    PSGD_CUDA_CHECK(cudaGetLastError());
-    return PSGD_OK;
-  }
-};
+template <class Kern, class... Args>
+cudaError_t launch_ex(Kern kern, int grid, int block, size_t smem, cudaStream_t st, bool pdl,
+                      Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <int RM>
+int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, const float* q, float* p,
+           const float* bias_g, int* status, cudaStream_t st) {
+  const int grid = (int)pl->k1_beg.size() - 1;
+  if (pl->k1.empty() && pl->nbias == 0) return PSGD_OK;
+  auto kern = k1_ef_p<RM>;
+  const size_t smem = sizeof(K1Smem);
+  PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PSGD_CUDA_CHECK(launch_ex(kern, std::max(1, grid), kTmaThreads, smem, st, false,
+                            (const MatDev*)pl->d_mats, (const Chunk1*)pl->d_k1, (const int*)pl->d_k1_beg,
+                            (const SplitRow*)pl->d_splits, g, e, work, q, p, pl->d_psplit,
+                            pl->d_split_cnt, bias_g, (long long)pl->nbias, (long long)pl->p_bias_off,
+                            (long long)pl->flag_off, status));
+  return PSGD_OK;
+}
+
+template <int RM>
+int run_k3(const psgd_plan* pl, float* work, const float* p, int divisor, const double* repl,
+           float* phat, float* qout, float* e, float* bias_out, int* status, cudaStream_t st) {
+  const int grid = (int)pl->k3_beg.size() - 1;
+  if (grid <= 0 || pl->k3.empty()) return PSGD_OK;
+  auto kern = k3_q_ef<RM>;
+  const size_t smem = pl->k3l.total;
+  PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PSGD_CUDA_CHECK(launch_ex(kern, grid, kTmaThreads, smem, st, true, (const MatDev*)pl->d_mats,
+                            (const Slab3*)pl->d_k3, (const int*)pl->d_k3_beg, pl->k3l, work, p, divisor,
+                            repl, phat, qout, e, bias_out, (long long)pl->nbias,
+                            (long long)pl->p_bias_off, (long long)pl->flag_off, pl->nflags,
+                            pl->world == 1 ? 1 : 0, status));
+  return PSGD_OK;
+}
 
 template <int R, bool EXACT>
-struct RunK3 {
-  static int run(const psgd_plan* pl, const Group& gp, float* work, const float* phat, float* qout,
-                 float* e, const int* status, cudaStream_t st) {
+struct RunK3Tall {
+  static int run(const psgd_plan* pl, const Group& gp, const float* work, const float* phat, float* qout,
+                 const int* status, cudaStream_t st) {
     const int nitems = gp.end - gp.beg;
     if (nitems <= 0) return PSGD_OK;
-    auto kern = k3_q_ef<R, EXACT>;
+    auto kern = k3_tall<R, EXACT>;
     if (gp.smem > 48 * 1024)
       PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gp.smem));
-    kern<<<nitems, kThreads, gp.smem, st>>>(pl->d_mats, pl->d_k3, gp.beg, work, phat, qout, e,
-                                            pl->d_wsq, pl->d_counters, pl->world == 1 ? 1 : 0,
-                                            status);
+    kern<<<nitems, kThreads, gp.smem, st>>>(pl->d_mats, pl->d_k3t + gp.beg, work, phat, qout, pl->d_wsq,
+                                            pl->d_counters, status);
     PSGD_CUDA_CHECK(cudaGetLastError());
     return PSGD_OK;
   }
@@ -991,51 +1511,77 @@ bool check_dev(const psgd_plan* pl) {
   return dev == pl->device;
 }
 
+int launch_k2(const psgd_plan* pl, bool tall_only, bool with_bias, const float* p, float* phat,
+              int divisor, const double* repl, float* bias_out, int* status, cudaStream_t st) {
+  const int nlist = tall_only ? (int)pl->tall_list.size() : pl->nmat;
+  const int bias_blocks =
+      (with_bias && pl->nbias > 0) ? (int)std::min<long long>(64, (pl->nbias + kGsThreads * 4 - 1) / (kGsThreads * 4)) : 0;
+  const int grid = nlist + bias_blocks;
+  if (grid == 0) return PSGD_OK;
+  k2_gs<<<grid, kGsThreads, 0, st>>>(pl->d_mats, tall_only ? pl->d_tall_list : pl->d_all_list, nlist, p,
+                                     phat, divisor, repl, pl->d_gsws, bias_out, pl->p_bias_off, pl->nbias,
+                                     pl->flag_off, pl->nflags, status);
+  PSGD_CUDA_CHECK(cudaGetLastError());
+  return PSGD_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 int psgd_ef_p(const psgd_plan* pl, const float* g, const float* e, float* work, const float* q,
               float* p, const float* bias_g, int32_t* status, void* stream) {
-  if (!pl || !status || !p || (pl->flat_elems > 0 && (!g || !work || !q)) ||
-      (pl->nbias > 0 && !bias_g))
+  if (!pl || !status || !p || (pl->nmat > 0 && (!g || !work || !q)) || (pl->nbias > 0 && !bias_g))
     return fail(PSGD_EINVAL, "psgd_ef_p: NULL argument");
   if (!check_dev(pl)) return fail(PSGD_EINVAL, "psgd_ef_p: plan belongs to another device");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  for (const Group& gp : pl->g1) {
-    int rc = dispatch_r<RunK1>(gp.r, pl, gp, g, e, work, q, p, bias_g, (int*)status, st);
+  switch (pl->rmax) {
+    case 1: return run_k1<1>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+    case 2: return run_k1<2>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+    case 4: return run_k1<4>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+    case 8: return run_k1<8>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+    default: return run_k1<16>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+  }
+}
+
+int psgd_orthogonalize(const psgd_plan* pl, const float* p, int32_t divisor, const double* repl,
+                       float* p_hat, float* bias_out, int32_t* status, void* stream) {
+  if (!pl || !p || !p_hat || !status || divisor < 1 || (pl->nmat > 0 && !repl) ||
+      (pl->nbias > 0 && !bias_out))
+    return fail(PSGD_EINVAL, "psgd_orthogonalize: bad argument");
+  return launch_k2(pl, false, true, p, p_hat, divisor, repl, bias_out, (int*)status,
+                   static_cast<cudaStream_t>(stream));
+}
+
+int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor, const double* repl,
+              float* p_hat, float* q_out, float* e, float* bias_out, int32_t* status, void* stream) {
+  if (!pl || !status || divisor < 1 ||
+      (pl->nmat > 0 && (!work || !p || !repl || !p_hat || !q_out || !e)) || (pl->nbias > 0 && !bias_out))
+    return fail(PSGD_EINVAL, "psgd_q_ef: bad argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = PSGD_OK;
+  const bool fused = !pl->k3.empty();
+  switch (pl->rmax) {
+    case 1: rc = run_k3<1>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
+    case 2: rc = run_k3<2>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
+    case 4: rc = run_k3<4>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
+    case 8: rc = run_k3<8>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
+    default: rc = run_k3<16>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
+  }
+  if (rc) return rc;
+  if (pl->n_tall > 0 || (!fused && pl->nbias > 0)) {
+    rc = launch_k2(pl, true, !fused, p, p_hat, divisor, repl, bias_out, (int*)status, st);
     if (rc) return rc;
   }
-  return PSGD_OK;
-}
-
-int psgd_orthogonalize(const psgd_plan* pl, float* p, int32_t divisor, const double* repl,
-                       float* bias_out, int32_t* status, void* stream) {
-  if (!pl || !p || !status || divisor < 1 || (pl->nmat > 0 && !repl) || (pl->nbias > 0 && !bias_out))
-    return fail(PSGD_EINVAL, "psgd_orthogonalize: bad argument");
-  const int bias_blocks = pl->nbias > 0 ? (int)std::min<long long>(64, (pl->nbias + kGsThreads * 4 - 1) / (kGsThreads * 4)) : 0;
-  const int grid = pl->nmat + bias_blocks;
-  if (grid == 0) return PSGD_OK;
-  k2_gs<<<grid, kGsThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      pl->d_mats, pl->nmat, p, divisor, repl, pl->d_gsws, bias_out, pl->p_bias_off, pl->nbias,
-      (int*)status);
-  PSGD_CUDA_CHECK(cudaGetLastError());
-  return PSGD_OK;
-}
-
-int psgd_q_ef(const psgd_plan* pl, float* work, const float* p_hat, float* q_out, float* e,
-              const int32_t* status, void* stream) {
-  if (!pl || !status || (pl->nmat > 0 && (!work || !p_hat || !q_out || !e)))
-    return fail(PSGD_EINVAL, "psgd_q_ef: NULL argument");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  for (const Group& gp : pl->g3) {
-    int rc = dispatch_r<RunK3>(gp.r, pl, gp, work, p_hat, q_out, e, (const int*)status, st);
+  for (const Group& gp : pl->g3t) {
+    rc = dispatch_r<RunK3Tall>(gp.r, pl, gp, (const float*)work, (const float*)p_hat, q_out,
+                               (const int*)status, st);
     if (rc) return rc;
   }
   for (const Group& gp : pl->g4) {
-    int rc = dispatch_r<RunK4>(gp.r, pl, (const RowItem*)pl->d_k4, gp, work, e, p_hat,
-                               (const float*)q_out, 1, (float*)nullptr, pl->world == 1 ? 1 : 0,
-                               (const int*)status, st);
+    rc = dispatch_r<RunK4>(gp.r, pl, (const RowItem*)pl->d_k4, gp, work, e, (const float*)p_hat,
+                           (const float*)q_out, 1, (float*)nullptr, pl->world == 1 ? 1 : 0,
+                           (const int*)status, st);
     if (rc) return rc;
   }
   return PSGD_OK;
@@ -1055,15 +1601,14 @@ int psgd_decompress(const psgd_plan* pl, const float* p_hat, const float* q_sum,
 }
 
 int psgd_step_single(const psgd_plan* pl, const float* g, float* e, float* work, float* q, float* p,
-                     const float* bias_g, const double* repl, float* bias_out, int32_t* status,
-                     void* stream) {
+                     float* p_hat, const float* bias_g, const double* repl, float* bias_out,
+                     int32_t* status, void* stream) {
   if (!pl) return fail(PSGD_EINVAL, "NULL plan");
   if (pl->world != 1) return fail(PSGD_EINVAL, "psgd_step_single needs a world-1 plan");
   if (!status) return fail(PSGD_EINVAL, "NULL status");
   PSGD_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
   int rc = psgd_ef_p(pl, g, e, work, q, p, bias_g, status, stream);
-  if (!rc) rc = psgd_orthogonalize(pl, p, 1, repl, bias_out, status, stream);
-  if (!rc) rc = psgd_q_ef(pl, work, p, q, e, status, stream);
+  if (!rc) rc = psgd_q_ef(pl, work, p, 1, repl, p_hat, q, e, bias_out, status, stream);
   return rc;
 }
 

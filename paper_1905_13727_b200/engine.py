@@ -7,16 +7,17 @@ on one device, the packed fp32 buffers of a parameter catalog:
     g[w]      flat gradients of local worker w       (caller fills; `grad_view`)
     e[w]      error-feedback memory                  (WorkerState.error, optimizer.py:63)
     work[w]   delta, then M-hat                      (RoundTrip.aggregated)
-    P[w]      packed P + uncompressed bias tail      (AR1 payload)
+    P[w]      packed P + bias tail + non-finite flags (AR1 payload)
+    Phat      P-hat of every matrix                  (RoundTrip.payload.p)
     Q         warm-start Q of every matrix           (PowerSGD.q_memory, compressors.py:357)
     qbuf[w]   local q_w                              (AR2 payload, W > 1)
     bias_out  mean of the bias gradients             (optimizer.py:111-113)
 
 and runs, per step,
 
-    W == 1 (one GPU)        psgd_step_single                       -- 3 kernels
-    W > 1, distributed      K1 | all_reduce(P) | K2 | K3 | all_reduce(q) | K5
-    W > 1, simulated        K1 x W | tree_mean | K2 | K3 x W | tree_mean | K5
+    W == 1 (one GPU)        psgd_step_single                       -- 2 kernels
+    W > 1, distributed      K1 | all_reduce(P) | K3 | all_reduce(q) | K5
+    W > 1, simulated        K1 x W | tree_mean | K3 x W | tree_mean | K5
 
 Q is seeded exactly as the reference (derive_rng(seed, "warm_start_init",
 param_index), compressors.py:362-367) and CommStats are charged exactly as the
@@ -91,6 +92,7 @@ class PowerSGDEngine:
         self.bias_g = [torch.zeros(max(1, self.nbias), **z) for _ in range(L)]
         self.P = [torch.zeros(pl.p_elems, **z) for _ in range(L)]
         self.Pm = torch.zeros(pl.p_elems, **z) if L > 1 else self.P[0]
+        self.Phat = torch.zeros(pl.p_elems, **z)
         self.Q = torch.zeros(pl.q_elems, **z)
         self.qbuf = [torch.zeros(pl.q_elems, **z) for _ in range(L)] if self.world > 1 else None
         self.bias_out = torch.zeros(max(1, self.nbias), **z)
@@ -139,7 +141,7 @@ class PowerSGDEngine:
 
     def p_view(self, param_index):
         """P-hat of `param_index` after a step (RoundTrip.payload.p)."""
-        return self.plan.p_view(self.Pm, self.slot[param_index])
+        return self.plan.p_view(self.Phat, self.slot[param_index])
 
     def q_view(self, param_index):
         """Warm-start Q of `param_index` (= Q-bar of the last step, payload.q)."""
@@ -156,47 +158,39 @@ class PowerSGDEngine:
         pl = self.plan
         sp = stream_ptr(stream)
         h = pl.handle
-        e = self.e if self.error_feedback else [None] * self.nlocal
+        e = self.e if self.error_feedback else [self._e_scratch] * self.nlocal
+        ein = self.e if self.error_feedback else [None] * self.nlocal
         if self.world == 1 and self.error_feedback:
             _lib.check(lib.psgd_step_single(h, ptr(self.g[0]), ptr(e[0]), ptr(self.work[0]), ptr(self.Q),
-                                            ptr(self.P[0]), ptr(self.bias_g[0]), ptr(self.repl),
+                                            ptr(self.P[0]), ptr(self.Phat), ptr(self.bias_g[0]), ptr(self.repl),
                                             ptr(self.bias_out), ptr(self.status), sp), "psgd_step_single")
             return
-        if self.world == 1:
-            # error feedback off (optimizer.py:118-119): delta = g, EF output discarded
-            self.status.zero_()
-            _lib.check(lib.psgd_ef_p(h, ptr(self.g[0]), None, ptr(self.work[0]), ptr(self.Q),
-                                     ptr(self.P[0]), ptr(self.bias_g[0]), ptr(self.status), sp), "psgd_ef_p")
-            _lib.check(lib.psgd_orthogonalize(h, ptr(self.P[0]), 1, ptr(self.repl), ptr(self.bias_out),
-                                              ptr(self.status), sp), "psgd_orthogonalize")
-            _lib.check(lib.psgd_q_ef(h, ptr(self.work[0]), ptr(self.P[0]), ptr(self.Q),
-                                     ptr(self._scratch_e()), ptr(self.status), sp), "psgd_q_ef")
-            return
         self.status.zero_()
-        for w in range(self.nlocal):
-            _lib.check(lib.psgd_ef_p(h, ptr(self.g[w]), ptr(e[w]), ptr(self.work[w]), ptr(self.Q),
-                                     ptr(self.P[w]), ptr(self.bias_g[w]), ptr(self.status), sp),
-                       "psgd_ef_p")
-        if self.distributed:
+        for w in range(self.nlocal):      # K1: delta = g + e, P = delta Q  (e NULL: EF off)
+            _lib.check(lib.psgd_ef_p(h, ptr(self.g[w]), ptr(ein[w]), ptr(self.work[w]), ptr(self.Q),
+                                     ptr(self.P[w]), ptr(self.bias_g[w]), ptr(self.status), sp), "psgd_ef_p")
+        if self.distributed:              # AR1 (P + bias + flags), / W fused into K3
             self.comm.all_reduce_sum_(self.P[0])
             div = self.world
-        else:
+        elif self.nlocal > 1:
             tree_mean_(self.P, self.Pm, stream)
             div = 1
-        _lib.check(lib.psgd_orthogonalize(h, ptr(self.Pm), div, ptr(self.repl), ptr(self.bias_out),
-                                          ptr(self.status), sp), "psgd_orthogonalize")
-        # with error feedback off the EF output goes to a scratch buffer (never read)
-        for w in range(self.nlocal):
-            ew = e[w] if e[w] is not None else self._scratch_e()
-            _lib.check(lib.psgd_q_ef(h, ptr(self.work[w]), ptr(self.Pm), ptr(self.qbuf[w]), ptr(ew),
-                                     ptr(self.status), sp), "psgd_q_ef")
-        if self.distributed:
+        else:
+            div = 1
+        qout = self.Q if self.world == 1 else None
+        for w in range(self.nlocal):      # K3: GS, q_w, e (+ M-hat and Q at W=1)
+            q_w = qout if qout is not None else self.qbuf[w]
+            _lib.check(lib.psgd_q_ef(h, ptr(self.work[w]), ptr(self.Pm), div, ptr(self.repl), ptr(self.Phat),
+                                     ptr(q_w), ptr(e[w]), ptr(self.bias_out), ptr(self.status), sp), "psgd_q_ef")
+        if self.world == 1:
+            return
+        if self.distributed:              # AR2 (q), then Q-bar = q / W and M-hat
             self.comm.all_reduce_sum_(self.qbuf[0])
-            _lib.check(lib.psgd_decompress(h, ptr(self.Pm), ptr(self.qbuf[0]), self.world, ptr(self.Q),
+            _lib.check(lib.psgd_decompress(h, ptr(self.Phat), ptr(self.qbuf[0]), self.world, ptr(self.Q),
                                            ptr(self.work[0]), ptr(self.status), sp), "psgd_decompress")
         else:
             tree_mean_(self.qbuf, self.Q, stream)
-            _lib.check(lib.psgd_decompress(h, ptr(self.Pm), ptr(self.Q), 1, None, ptr(self.work[0]),
+            _lib.check(lib.psgd_decompress(h, ptr(self.Phat), ptr(self.Q), 1, None, ptr(self.work[0]),
                                            ptr(self.status), sp), "psgd_decompress")
 
     def _scratch_e(self):

@@ -34,12 +34,12 @@ def orthogonalize(p, device=None):
     if r > n:
         raise ContractViolation(f"cannot orthonormalize {r} columns in R^{n}")
     plan = _plan_for(n, r, t.device)
-    buf = torch.empty(plan.p_elems, dtype=torch.float32, device=t.device)
+    buf = torch.zeros(plan.p_elems, dtype=torch.float32, device=t.device)
     plan.p_view(buf, 0).copy_(t)
     status = torch.zeros(1, dtype=torch.int32, device=t.device)
     with torch.cuda.device(t.device):
         _lib.check(_lib.lib().psgd_orthogonalize(plan.handle, ptr(buf), 1, ptr(plan.repl_table()),
-                                                 None, ptr(status), stream_ptr()), "psgd_orthogonalize")
+                                                 ptr(buf), None, ptr(status), stream_ptr()), "psgd_orthogonalize")
     st = int(status.item())
     if st & _lib.STATUS_NONFINITE_P:
         raise ContractViolation("orthogonalize input contains non-finite entries")
