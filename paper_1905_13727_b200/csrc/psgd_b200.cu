@@ -30,9 +30,12 @@
 
 #include "../../include/psgd_b200.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -47,8 +50,10 @@ constexpr int kTmaThreads = 288;   // + 1 producer warp
 constexpr int kRowItemElems = 4096;
 constexpr int kGsThreads = 512;
 constexpr int kFusedNMax = 512;    // K3 fused path holds all rows of a slab
-constexpr int K1_STAGES = 4;
+constexpr int K1_STAGES = 3;
 constexpr int K1_CHUNK = 4608;     // floats of g (and of e) per chunk
+constexpr int K1_QSLOT_CAP = 12288;  // floats of Q per smem slot (2 slots)
+constexpr int K1_RED_ROWS = 16;
 constexpr int K1_STAGE_FLOATS = K1_CHUNK + 16;
 constexpr int K3_STAGES = 2;
 constexpr int K3_QMAX = 512;       // C * r per slab
@@ -70,7 +75,7 @@ int fail(int code, const std::string& msg) {
 struct MatDev {
   long long flat_off, p_off, q_off, repl_off;
   int n, m, r, tall;
-  int lg1, pad0, pad1, pad2;  // lg1: log2 lanes per row in K1 (2..8)
+  int lg1, qs, pad1, pad2;  // lg1: log2 lanes per row in K1 (2..8); qs: Q staged in smem by K1
 };
 
 struct RowItem {   // K4 / K5 warp item: rows [row0, row0 + nrows) of `mat`, 2^lg lanes per row
@@ -89,7 +94,15 @@ struct SplitRow {  // an over-long row whose P is combined from `parts` partials
 };
 
 struct Slab3 {     // K3 fused slab: all n rows x cols [c0, c0 + ncols) of `mat`
-  int mat, c0, ncols, cql, vec, first, pad0, pad1;
+  int mat, c0, ncols, cql, vec, first;
+  int map;         // >= 0: 2-D TMA tensor map index (box C x brows); -1: one bulk copy per row
+  int stride;      // smem floats per slab row
+  int brows, pad0, pad1, pad2;
+};
+
+constexpr int K3_MAXMAPS = 64;
+struct K3Maps {    // __grid_constant__ kernel parameter (8 KB)
+  CUtensorMap map[K3_MAXMAPS];
 };
 
 struct SlabItem {  // tall-matrix split-n q item (register slab)
@@ -146,6 +159,15 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           su32(dst)),
       "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
+      : "memory");
+}
+// 2-D tiled tensor copy global -> shared (TMA, SASS UTMALDG)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar)), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void st_hint(float4* p, float4 v, uint64_t pol) {
@@ -276,33 +298,181 @@ __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ 
 // ============================================================================= K1
 // delta = g + e ; P[i,:] = sum_j delta[i,j] Q[j,:]   (optimizer.py:120, compressors.py:336)
 
-struct K1Smem {
-  float g[K1_STAGES][K1_STAGE_FLOATS];
-  float e[K1_STAGES][K1_STAGE_FLOATS];
-  float red[2][8][PSGD_MAX_RANK];
-  uint64_t full[K1_STAGES];
-  uint64_t empty[K1_STAGES];
-  int flag;
+struct K1Layout {  // dynamic smem: g stages | e stages | Q slots | red | barriers
+  int qslot_floats;
+  int off_q, off_red, off_bar, total;
 };
+
+template <int RM, bool QS>
+__device__ __forceinline__ void k1_q4(const float* __restrict__ q, bool aligned, int r, float (&qv)[4][RM]) {
+  if (QS) {  // Q staged in shared memory
+    if (r == RM && aligned) {
+#pragma unroll
+      for (int t = 0; t < RM; ++t) {
+        const float4 v = reinterpret_cast<const float4*>(q)[t];
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) qv[(4 * t + u) / RM][(4 * t + u) % RM] = vv[u];
+      }
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int k = 0; k < RM; ++k) qv[jj][k] = k < r ? q[jj * r + k] : 0.f;
+    }
+  } else {
+    load_q4<RM>(q, aligned, r, qv);
+  }
+}
+
+// One chunk: rows of the chunk to row groups of G = 2^lg consumer threads.
+template <int RM, bool QS>
+__device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, const float* __restrict__ Qm,
+                                         const float* __restrict__ sg, const float* __restrict__ se,
+                                         bool has_e, float* __restrict__ work, float* __restrict__ P,
+                                         const SplitRow* __restrict__ splits, float* __restrict__ psplit,
+                                         int* __restrict__ split_cnt, float* __restrict__ red, uint64_t keep,
+                                         bool& bad) {
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int r = md.r, m = md.m;
+  const int lg = md.lg1;
+  const int G = 1 << lg;
+  const int gl = t & (G - 1);
+  const int gid = t >> lg;
+  const int rpp = kThreads >> lg;
+  const long long a4 = ch.off & ~3LL;
+  for (int rb = 0; rb < ch.nrows; rb += rpp) {
+    const int li = rb + gid;
+    const bool active = li < ch.nrows;
+    float acc[RM];
+#pragma unroll
+    for (int q = 0; q < RM; ++q) acc[q] = 0.f;
+    if (active) {
+      const long long og = ch.off + (long long)li * m;
+      const int sm = (int)(og - a4);
+      const int nc = ch.ncols;
+      const int head = min((int)((4 - (og & 3)) & 3), nc);
+      const int body4 = (nc - head) >> 2;
+      const int tail = nc - head - 4 * body4;
+      for (int x = gl; x < head + tail; x += G) {
+        const int j = x < head ? x : head + 4 * body4 + (x - head);
+        const float gv = sg[sm + j];
+        const float d = has_e ? gv + se[sm + j] : gv;
+        bad |= !finite1(gv);
+        st_hint(work + og + j, d, keep);
+        const float* qj = Qm + (long long)(ch.c0 + j) * r;
+#pragma unroll
+        for (int q = 0; q < RM; ++q)
+          if (q < r) acc[q] = fmaf(d, QS ? qj[q] : __ldg(qj + q), acc[q]);
+      }
+      const float4* __restrict__ g4 = reinterpret_cast<const float4*>(sg + sm + head);
+      const float4* __restrict__ e4 = reinterpret_cast<const float4*>(se + sm + head);
+      float4* __restrict__ w4 = reinterpret_cast<float4*>(work + og + head);
+      const float* __restrict__ qrow = Qm + (long long)(ch.c0 + head) * r;
+      const bool qal = (((ch.c0 + head) * r) & 3) == 0;
+#pragma unroll 2
+      for (int c = gl; c < body4; c += G) {
+        const float4 gv = g4[c];
+        const float4 ev = has_e ? e4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 d = make_float4(gv.x + ev.x, gv.y + ev.y, gv.z + ev.z, gv.w + ev.w);
+        bad |= !finite4(gv);
+        st_hint(w4 + c, d, keep);
+        float qv[4][RM];
+        k1_q4<RM, QS>(qrow + (long long)(4 * c) * r, qal, r, qv);
+#pragma unroll
+        for (int q = 0; q < RM; ++q) {
+          acc[q] = fmaf(d.x, qv[0][q], acc[q]);
+          acc[q] = fmaf(d.y, qv[1][q], acc[q]);
+          acc[q] = fmaf(d.z, qv[2][q], acc[q]);
+          acc[q] = fmaf(d.w, qv[3][q], acc[q]);
+        }
+      }
+    }
+    if (G <= 32) {  // fixed-order butterfly inside the row group; no barrier
+      for (int off = G >> 1; off > 0; off >>= 1)
+#pragma unroll
+        for (int q = 0; q < RM; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+      if (active && gl == 0) {
+        float* dst = P + md.p_off + (long long)(ch.row0 + li) * r;
+#pragma unroll
+        for (int q = 0; q < RM; ++q)
+          if (q < r) dst[q] = acc[q];
+      }
+    } else {  // multi-warp rows: per-warp partials, combined once per chunk below
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int q = 0; q < RM; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+      if (active && lane == 0) {
+#pragma unroll
+        for (int q = 0; q < RM; ++q) red[(li * 8 + warp) * RM + q] = acc[q];
+      }
+    }
+  }
+  if (G > 32) {
+    bar_consumers();
+    const int nw = G >> 5;
+    for (int o = t; o < ch.nrows * r; o += kThreads) {
+      const int li = o / r, q = o - li * r;
+      const int w0 = (li % rpp) * nw;
+      float s = 0.f;
+      for (int w = 0; w < nw; ++w) s += red[(li * 8 + w0 + w) * RM + q];
+      if (ch.split < 0) {
+        P[md.p_off + (long long)(ch.row0 + li) * r + q] = s;
+      } else {
+        red[(K1_RED_ROWS * 8) * RM + q] = s;  // staged for the split combine below
+      }
+    }
+    if (ch.split >= 0) {
+      bar_consumers();
+      if (t == 0) {  // segment of an over-long row: the last-arriving segment combines in part order
+        const SplitRow sp = splits[ch.split];
+        for (int q = 0; q < r; ++q) psplit[(long long)(sp.base + ch.part) * r + q] = red[(K1_RED_ROWS * 8) * RM + q];
+        __threadfence();
+        if (atomicAdd(split_cnt + ch.split, 1) == sp.parts - 1) {
+          __threadfence();
+          for (int q = 0; q < r; ++q) {
+            float s = 0.f;
+            for (int p = 0; p < sp.parts; ++p) s += __ldcg(psplit + (long long)(sp.base + p) * r + q);
+            P[md.p_off + (long long)sp.row * r + q] = s;
+          }
+          split_cnt[ch.split] = 0;
+        }
+      }
+    }
+  }
+}
 
 template <int RM>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     k1_ef_p(const MatDev* __restrict__ mats, const Chunk1* __restrict__ chunks,
-            const int* __restrict__ cta_beg, const SplitRow* __restrict__ splits,
+            const int* __restrict__ cta_beg, const SplitRow* __restrict__ splits, K1Layout L,
             const float* __restrict__ g, const float* __restrict__ e, float* __restrict__ work,
             const float* __restrict__ Q, float* __restrict__ P, float* __restrict__ psplit,
             int* __restrict__ split_cnt, const float* __restrict__ bias_g, long long nbias,
             long long bias_off, long long flag_off, int* status) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  K1Smem& S = *reinterpret_cast<K1Smem*>(smem_raw);
+  float* sgb = reinterpret_cast<float*>(smem_raw);
+  float* seb = sgb + K1_STAGES * K1_STAGE_FLOATS;
+  float* qsl = reinterpret_cast<float*>(smem_raw + L.off_q);
+  float* red = reinterpret_cast<float*>(smem_raw + L.off_red);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
+  uint64_t* empty = full + K1_STAGES;
+  uint64_t* qfull = empty + K1_STAGES;
+  uint64_t* qempty = qfull + 2;
+  int* sflag = reinterpret_cast<int*>(qempty + 2);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int cb = cta_beg[blockIdx.x], ce = cta_beg[blockIdx.x + 1];
   if (t == 0) {
     for (int s = 0; s < K1_STAGES; ++s) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], 8);
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
     }
-    S.flag = 0;
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qfull[s], 1);
+      mbar_init(&qempty[s], 8);
+    }
+    *sflag = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -311,19 +481,32 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if (warp == 8) {  // ---------------- producer
     if (lane == 0) {
       const uint64_t pol = pol_evict_first();
+      const uint64_t polq = pol_evict_last();
+      int cur = -1, mseq = -1;
       for (int k = cb; k < ce; ++k) {
         const int s = (k - cb) % K1_STAGES;
         const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
-        mbar_wait(&S.empty[s], ph ^ 1);
         const Chunk1 ch = chunks[k];
-        const int m = mats[ch.mat].m;
+        const MatDev md = mats[ch.mat];
+        if (ch.mat != cur) {  // Q of the next matrix into a smem slot (double-buffered)
+          cur = ch.mat;
+          ++mseq;
+          if (md.qs) {
+            const int qs = mseq & 1;
+            mbar_wait(&qempty[qs], ((mseq >> 1) & 1) ^ 1);
+            const uint32_t qb = (uint32_t)((((long long)md.m * md.r + 3) & ~3LL) * 4);
+            mbar_expect_tx(&qfull[qs], qb);
+            tma_load(qsl + qs * L.qslot_floats, Q + md.q_off, qb, &qfull[qs], polq);
+          }
+        }
+        mbar_wait(&empty[s], ph ^ 1);
         const long long a4 = ch.off & ~3LL;
-        const long long span = (long long)(ch.nrows - 1) * m + ch.ncols;
+        const long long span = (long long)(ch.nrows - 1) * md.m + ch.ncols;
         const long long b4 = (ch.off + span + 3) & ~3LL;
         const uint32_t bytes = (uint32_t)((b4 - a4) * 4);
-        mbar_expect_tx(&S.full[s], e ? 2 * bytes : bytes);
-        tma_load(S.g[s], g + a4, bytes, &S.full[s], pol);
-        if (e) tma_load(S.e[s], e + a4, bytes, &S.full[s], pol);
+        mbar_expect_tx(&full[s], e ? 2 * bytes : bytes);
+        tma_load(sgb + s * K1_STAGE_FLOATS, g + a4, bytes, &full[s], pol);
+        if (e) tma_load(seb + s * K1_STAGE_FLOATS, e + a4, bytes, &full[s], pol);
       }
     }
     return;
@@ -337,129 +520,42 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     P[bias_off + x] = v;
   }
   const uint64_t keep = pol_evict_last();
-  int rpar = 0;
+  int cur = -1, mseq = -1, rpar = 0;
+  bool cur_qs = false;
   for (int k = cb; k < ce; ++k) {
     const int s = (k - cb) % K1_STAGES;
     const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
     const Chunk1 ch = chunks[k];
     const MatDev md = mats[ch.mat];
-    const int r = md.r, m = md.m;
-    const float* __restrict__ Qm = Q + md.q_off;
-    const int lg = md.lg1;
-    const int G = 1 << lg;
-    const int gl = t & (G - 1);
-    const int gid = t >> lg;
-    const int rpp = kThreads >> lg;
-    const long long a4 = ch.off & ~3LL;
-    mbar_wait(&S.full[s], ph);
-    const float* __restrict__ sg = S.g[s];
-    const float* __restrict__ se = S.e[s];
-    for (int rb = 0; rb < ch.nrows; rb += rpp) {
-      const int li = rb + gid;
-      const bool active = li < ch.nrows;
-      float acc[RM];
-#pragma unroll
-      for (int q = 0; q < RM; ++q) acc[q] = 0.f;
-      if (active) {
-        const long long og = ch.off + (long long)li * m;
-        const int sm = (int)(og - a4);
-        const int nc = ch.ncols;
-        const int head = min((int)((4 - (og & 3)) & 3), nc);
-        const int body4 = (nc - head) >> 2;
-        const int tail = nc - head - 4 * body4;
-        for (int x = gl; x < head + tail; x += G) {
-          const int j = x < head ? x : head + 4 * body4 + (x - head);
-          const float gv = sg[sm + j];
-          const float d = e ? gv + se[sm + j] : gv;
-          bad |= !finite1(gv);
-          st_hint(work + og + j, d, keep);
-          const float* qj = Qm + (long long)(ch.c0 + j) * r;
-#pragma unroll
-          for (int q = 0; q < RM; ++q)
-            if (q < r) acc[q] = fmaf(d, __ldg(qj + q), acc[q]);
-        }
-        const float4* __restrict__ g4 = reinterpret_cast<const float4*>(sg + sm + head);
-        const float4* __restrict__ e4 = reinterpret_cast<const float4*>(se + sm + head);
-        float4* __restrict__ w4 = reinterpret_cast<float4*>(work + og + head);
-        const float* __restrict__ qrow = Qm + (long long)(ch.c0 + head) * r;
-        const bool qal = (((ch.c0 + head) * r + (int)(md.q_off & 3)) & 3) == 0;
-#pragma unroll 2
-        for (int c = gl; c < body4; c += G) {
-          const float4 gv = g4[c];
-          const float4 ev = e ? e4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-          const float4 d = make_float4(gv.x + ev.x, gv.y + ev.y, gv.z + ev.z, gv.w + ev.w);
-          bad |= !finite4(gv);
-          st_hint(w4 + c, d, keep);
-          float qv[4][RM];
-          load_q4<RM>(qrow + (long long)(4 * c) * r, qal, r, qv);
-#pragma unroll
-          for (int q = 0; q < RM; ++q) {
-            acc[q] = fmaf(d.x, qv[0][q], acc[q]);
-            acc[q] = fmaf(d.y, qv[1][q], acc[q]);
-            acc[q] = fmaf(d.z, qv[2][q], acc[q]);
-            acc[q] = fmaf(d.w, qv[3][q], acc[q]);
-          }
-        }
+    if (ch.mat != cur) {
+      if (cur >= 0 && cur_qs) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&qempty[mseq & 1]);
       }
-      // fixed-order reduction across the row group
-      if (G <= 32) {
-        for (int off = G >> 1; off > 0; off >>= 1)
-#pragma unroll
-          for (int q = 0; q < RM; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
-      } else {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-          for (int q = 0; q < RM; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
-        float(*red)[PSGD_MAX_RANK] = S.red[rpar & 1];
-        ++rpar;
-        if (lane == 0) {
-#pragma unroll
-          for (int q = 0; q < RM; ++q) red[warp][q] = acc[q];
-        }
-        bar_consumers();
-        if (gl == 0) {
-          const int nw = G >> 5;
-#pragma unroll
-          for (int q = 0; q < RM; ++q) {
-            float sacc = 0.f;
-            for (int w = 0; w < nw; ++w) sacc += red[warp + w][q];
-            acc[q] = sacc;
-          }
-        }
-      }
-      if (active && gl == 0) {
-        if (ch.split < 0) {
-          float* dst = P + md.p_off + (long long)(ch.row0 + li) * r;
-#pragma unroll
-          for (int q = 0; q < RM; ++q)
-            if (q < r) dst[q] = acc[q];
-        } else {  // segment of an over-long row: the last-arriving segment combines in part order
-          const SplitRow sp = splits[ch.split];
-#pragma unroll
-          for (int q = 0; q < RM; ++q)
-            if (q < r) psplit[(long long)(sp.base + ch.part) * r + q] = acc[q];
-          __threadfence();
-          if (atomicAdd(split_cnt + ch.split, 1) == sp.parts - 1) {
-            __threadfence();
-            for (int q = 0; q < r; ++q) {
-              float sacc = 0.f;
-              for (int p = 0; p < sp.parts; ++p) sacc += __ldcg(psplit + (long long)(sp.base + p) * r + q);
-              P[md.p_off + (long long)sp.row * r + q] = sacc;
-            }
-            split_cnt[ch.split] = 0;
-          }
-        }
-      }
+      cur = ch.mat;
+      ++mseq;
+      cur_qs = md.qs != 0;
+      if (cur_qs) mbar_wait(&qfull[mseq & 1], (mseq >> 1) & 1);
     }
+    mbar_wait(&full[s], ph);
+    const float* sg = sgb + s * K1_STAGE_FLOATS;
+    const float* se = seb + s * K1_STAGE_FLOATS;
+    float* rb = red + (rpar & 1) * (K1_RED_ROWS * 8 * RM + RM);
+    if ((1 << md.lg1) > 32) ++rpar;
+    if (cur_qs)
+      k1_chunk<RM, true>(ch, md, qsl + (mseq & 1) * L.qslot_floats, sg, se, e != nullptr, work, P, splits,
+                         psplit, split_cnt, rb, keep, bad);
+    else
+      k1_chunk<RM, false>(ch, md, Q + md.q_off, sg, se, e != nullptr, work, P, splits, psplit, split_cnt,
+                          rb, keep, bad);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&S.empty[s]);
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
-  if (bad) atomicOr(&S.flag, 1);
+  if (bad) atomicOr(sflag, 1);
   bar_consumers();
   if (t == 0) {
-    P[flag_off + blockIdx.x] = S.flag ? 1.f : 0.f;  // carried to every rank by the P all-reduce
-    if (S.flag) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+    P[flag_off + blockIdx.x] = *sflag ? 1.f : 0.f;  // carried to every rank by the P all-reduce
+    if (*sflag) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
   }
 }
 
@@ -524,7 +620,8 @@ struct K3Layout {  // byte offsets inside dynamic smem
 template <int RM>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     k3_q_ef(const MatDev* __restrict__ mats, const Slab3* __restrict__ slabs,
-            const int* __restrict__ cta_beg, K3Layout L, float* __restrict__ work,
+            const int* __restrict__ cta_beg, K3Layout L, const __grid_constant__ K3Maps maps,
+            float* __restrict__ work,
             const float* __restrict__ P, int divisor, const double* __restrict__ repl,
             float* __restrict__ Phat, float* __restrict__ qout, float* __restrict__ e,
             float* __restrict__ bias_out, long long nbias, long long bias_off, long long flag_off,
@@ -558,7 +655,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
   }
 
-  if (warp == 8) {  // ---------------- producer: one bulk copy per row segment
+  if (warp == 8) {  // ---------------- producer: 2-D tensor tiles, or one bulk copy per row
     const uint64_t pol = pol_evict_first();
     for (int k = cb; k < ce; ++k) {
       const int s = (k - cb) % K3_STAGES;
@@ -566,9 +663,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       const Slab3 sl = slabs[k];
       const MatDev md = mats[sl.mat];
       const int C = sl.vec << sl.cql;
-      const int stride = C + 8;
+      float* stg = stage0 + (long long)s * L.stage_floats;
       if (lane == 0) mbar_wait(&empty[s], ph ^ 1);
       __syncwarp();
+      if (sl.map >= 0) {
+        if (lane == 0) {
+          const int nbox = (md.n + sl.brows - 1) / sl.brows;
+          mbar_expect_tx(&full[s], (uint32_t)(nbox * sl.brows * C * 4));
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(stg + (long long)b * sl.brows * C, &maps.map[sl.map], sl.c0, b * sl.brows, &full[s], pol);
+        }
+        continue;
+      }
       uint32_t bytes = 0;
       for (int i = lane; i < md.n; i += 32) {
         const long long st = md.flat_off + (long long)i * md.m + sl.c0;
@@ -578,12 +684,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       for (int off = 16; off > 0; off >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
       if (lane == 0) mbar_expect_tx(&full[s], bytes);
       __syncwarp();
-      float* stg = stage0 + (long long)s * L.stage_floats;
       for (int i = lane; i < md.n; i += 32) {
         const long long st = md.flat_off + (long long)i * md.m + sl.c0;
         const long long a4 = st & ~3LL;
         const uint32_t b = (uint32_t)((((st + sl.ncols + 3) & ~3LL) - a4) * 4);
-        tma_load(stg + i * stride, work + a4, b, &full[s], pol);
+        tma_load(stg + i * sl.stride, work + a4, b, &full[s], pol);
       }
     }
     return;
@@ -637,7 +742,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const float* stg = stage0 + (long long)s * L.stage_floats;
     if (!skip) {
       const int vec = sl.vec, cql = sl.cql;
-      const int CQ = 1 << cql, C = vec << cql, RG = kThreads >> cql, stride = C + 8;
+      const int CQ = 1 << cql, C = vec << cql, RG = kThreads >> cql, stride = sl.stride;
       const int cq = t & (CQ - 1), rg = t >> cql;
       const int col = cq * vec;
       const bool colok = col < sl.ncols;
@@ -1018,12 +1123,18 @@ struct psgd_plan {
   // K1
   std::vector<Chunk1> k1;
   std::vector<int> k1_beg;
+  K1Layout k1l{};
   std::vector<SplitRow> splits;
   long long psplit_elems = 0;
   // K3 fused
   std::vector<Slab3> k3;
   std::vector<int> k3_beg;
   K3Layout k3l{};
+  std::vector<int> map_mat;          // tensor-map index -> matrix
+  std::vector<int> map_cols, map_rows;
+  // tensor maps bind the work buffer's address: encoded on first use per buffer
+  mutable std::mutex map_mu;
+  mutable std::vector<std::pair<const void*, K3Maps*>> map_cache;
   // tall path
   std::vector<int> tall_list, all_list;
   std::vector<SlabItem> k3t;
@@ -1170,6 +1281,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     }
     md.tall = md.n > kFusedNMax;
     md.lg1 = lanes_log2_for(md.m, 8);
+    md.qs = align4((long long)md.m * md.r) <= K1_QSLOT_CAP ? 1 : 0;
     md.flat_off = fo;
     md.p_off = po;
     md.q_off = qo;
@@ -1216,6 +1328,19 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     pl->k1_beg = balance(w, pl->nsm);
   }
   pl->nflags = std::max(1, (int)pl->k1_beg.size() - 1);
+  {
+    K1Layout& L = pl->k1l;
+    long long qslot = 4;
+    for (auto& md : pl->mats)
+      if (md.qs) qslot = std::max(qslot, align4((long long)md.m * md.r));
+    L.qslot_floats = (int)qslot;
+    int off = 2 * K1_STAGES * K1_STAGE_FLOATS * 4;
+    L.off_q = off;   off += 2 * L.qslot_floats * 4;
+    L.off_red = off; off += 2 * (K1_RED_ROWS * 8 * pl->rmax + pl->rmax) * 4;
+    off = (off + 15) & ~15;
+    L.off_bar = off; off += (2 * K1_STAGES + 4) * 8 + 16;
+    L.total = off;
+  }
   pl->p_bias_off = po;
   pl->flag_off = align4(po + nbias);
   pl->p_elems = pl->flag_off + align4(pl->nflags);
@@ -1231,19 +1356,35 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       const MatDev& md = pl->mats[mi];
       if (md.tall) continue;
       const int vec = (md.m % 4 == 0) ? 4 : 1;
-      // widest power-of-two C that fits the stage, keeps C * r <= K3_QMAX,
-      // is not wider than needed for m, and maps onto 256 threads (CQ <= 256)
+      const bool use_map = vec == 4 && (int)pl->map_mat.size() < K3_MAXMAPS;
+      const int brows = md.n <= 256 ? md.n : 256;
+      const int nbox = (md.n + brows - 1) / brows;
+      // widest power-of-two C that fits the stage (row copies: n x (C+8); tiles:
+      // nbox * brows x C), keeps C * r <= K3_QMAX, is not wider than needed for
+      // m, and maps onto 256 threads (CQ <= 256)
+      auto fits = [&](int C) {
+        if ((long long)C * md.r > K3_QMAX) return false;
+        if (use_map) return (long long)nbox * brows * C <= stage_floats && C <= 256;
+        return (long long)md.n * (C + 8) <= stage_floats;
+      };
       int cql = vec == 4 ? 2 : 4;
       while (cql < 8) {
         const int C2 = vec << (cql + 1);
-        if ((long long)md.n * (C2 + 8) > stage_floats) break;
-        if ((long long)C2 * md.r > K3_QMAX) break;
+        if (!fits(C2)) break;
         if ((vec << cql) >= md.m) break;
         ++cql;
       }
       const int C = vec << cql;
+      int map = -1;
+      if (use_map) {
+        map = (int)pl->map_mat.size();
+        pl->map_mat.push_back(mi);
+        pl->map_cols.push_back(C);
+        pl->map_rows.push_back(brows);
+      }
       for (int c0 = 0; c0 < md.m; c0 += C) {
-        pl->k3.push_back({mi, c0, std::min(C, md.m - c0), cql, vec, c0 == 0 ? 1 : 0, 0, 0});
+        pl->k3.push_back({mi, c0, std::min(C, md.m - c0), cql, vec, c0 == 0 ? 1 : 0, map,
+                          use_map ? C : C + 8, brows, 0, 0, 0});
         w.push_back((double)md.n * std::min(C, md.m - c0) + 256.0);
       }
     }
@@ -1363,6 +1504,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
 
 int psgd_plan_destroy(psgd_plan* plan) {
   if (!plan) return PSGD_OK;
+  for (auto& kv : plan->map_cache) delete kv.second;
   if (plan->dev_block) cudaFree(plan->dev_block);
   delete plan;
   return PSGD_OK;
@@ -1439,13 +1581,55 @@ int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, con
   const int grid = (int)pl->k1_beg.size() - 1;
   if (pl->k1.empty() && pl->nbias == 0) return PSGD_OK;
   auto kern = k1_ef_p<RM>;
-  const size_t smem = sizeof(K1Smem);
+  const size_t smem = pl->k1l.total;
   PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   PSGD_CUDA_CHECK(launch_ex(kern, std::max(1, grid), kTmaThreads, smem, st, false,
                             (const MatDev*)pl->d_mats, (const Chunk1*)pl->d_k1, (const int*)pl->d_k1_beg,
-                            (const SplitRow*)pl->d_splits, g, e, work, q, p, pl->d_psplit,
+                            (const SplitRow*)pl->d_splits, pl->k1l, g, e, work, q, p, pl->d_psplit,
                             pl->d_split_cnt, bias_g, (long long)pl->nbias, (long long)pl->p_bias_off,
                             (long long)pl->flag_off, status));
+  return PSGD_OK;
+}
+
+// 2-D tensor maps of the fused vec-4 matrices inside `work` (cached per buffer)
+int k3_maps_for(const psgd_plan* pl, const float* work, const K3Maps** out) {
+  std::lock_guard<std::mutex> lk(pl->map_mu);
+  for (auto& kv : pl->map_cache)
+    if (kv.first == work) {
+      *out = kv.second;
+      return PSGD_OK;
+    }
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode && !pl->map_mat.empty()) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    PSGD_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+    if (!fn || qr != cudaDriverEntryPointSuccess) return fail(PSGD_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  K3Maps* maps = new K3Maps();
+  std::memset(maps, 0, sizeof(K3Maps));
+  for (size_t i = 0; i < pl->map_mat.size(); ++i) {
+    const MatDev& md = pl->mats[pl->map_mat[i]];
+    const cuuint64_t dims[2] = {(cuuint64_t)md.m, (cuuint64_t)md.n};
+    const cuuint64_t strides[1] = {(cuuint64_t)md.m * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)pl->map_cols[i], (cuuint32_t)pl->map_rows[i]};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult cr = encode(&maps->map[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                         const_cast<float*>(work + md.flat_off), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+      delete maps;
+      return fail(PSGD_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)cr) + ")");
+    }
+  }
+  if (pl->map_cache.size() >= 16) {  // bounded: callers use a handful of persistent buffers
+    delete pl->map_cache.front().second;
+    pl->map_cache.erase(pl->map_cache.begin());
+  }
+  pl->map_cache.emplace_back(work, maps);
+  *out = maps;
   return PSGD_OK;
 }
 
@@ -1454,12 +1638,15 @@ int run_k3(const psgd_plan* pl, float* work, const float* p, int divisor, const 
            float* phat, float* qout, float* e, float* bias_out, int* status, cudaStream_t st) {
   const int grid = (int)pl->k3_beg.size() - 1;
   if (grid <= 0 || pl->k3.empty()) return PSGD_OK;
+  const K3Maps* maps = nullptr;
+  int rc = k3_maps_for(pl, work, &maps);
+  if (rc) return rc;
   auto kern = k3_q_ef<RM>;
   const size_t smem = pl->k3l.total;
   PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   PSGD_CUDA_CHECK(launch_ex(kern, grid, kTmaThreads, smem, st, true, (const MatDev*)pl->d_mats,
-                            (const Slab3*)pl->d_k3, (const int*)pl->d_k3_beg, pl->k3l, work, p, divisor,
-                            repl, phat, qout, e, bias_out, (long long)pl->nbias,
+                            (const Slab3*)pl->d_k3, (const int*)pl->d_k3_beg, pl->k3l, *maps, work, p,
+                            divisor, repl, phat, qout, e, bias_out, (long long)pl->nbias,
                             (long long)pl->p_bias_off, (long long)pl->flag_off, pl->nflags,
                             pl->world == 1 ? 1 : 0, status));
   return PSGD_OK;
