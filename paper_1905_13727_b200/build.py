@@ -35,21 +35,23 @@ def stale():
     return any(os.path.getmtime(d) > mt for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
-    """Compile csrc/psgd_b200.cu -> libpsgd_b200.so (sm_100a).  Returns the path."""
-    if not force and not stale():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile csrc/psgd_b200.cu -> libpsgd_b200.so (sm_100a).  Returns the path.
+    `out` / `defines` build experiment variants (e.g. PSGD_PDL=0) beside it."""
+    lib = out or LIB
+    if not force and out is None and not stale():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-I", INCLUDE, "-o", tmp, SRC]
+    tmp = lib + ".tmp"
+    cmd = [nvcc_path(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-o", tmp, SRC]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
         print(res.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

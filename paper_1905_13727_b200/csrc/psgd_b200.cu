@@ -45,8 +45,10 @@
 
 namespace {
 
-constexpr int kThreads = 256;      // consumer threads / plain CTA size (8 warps)
-constexpr int kTmaThreads = 288;   // + 1 producer warp
+constexpr int kThreads = 256;      // plain CTA size (8 warps)
+constexpr int kCons = 512;         // consumer threads of the TMA kernels (16 warps)
+constexpr int kConsWarps = kCons / 32;
+constexpr int kTmaThreads = kCons + 32;  // + 1 producer warp
 constexpr int kRowItemElems = 4096;
 constexpr int kGsThreads = 512;
 constexpr int kFusedNMax = 512;    // K3 fused path holds all rows of a slab
@@ -54,7 +56,7 @@ constexpr int K1_STAGES = 3;
 constexpr int K1_CHUNK = 4608;     // floats of g (and of e) per chunk
 constexpr int K1_QSLOT_CAP = 12288;  // floats of Q per smem slot (2 slots)
 constexpr int K1_RED_ROWS = 16;
-constexpr int K1_STAGE_FLOATS = K1_CHUNK + 16;
+constexpr int K1_STAGE_FLOATS = K1_CHUNK + 8;  // + misalignment slack of a chunk
 constexpr int K3_STAGES = 2;
 constexpr int K3_QMAX = 512;       // C * r per slab
 
@@ -93,19 +95,7 @@ struct SplitRow {  // an over-long row whose P is combined from `parts` partials
   int mat, row, base, parts;
 };
 
-struct Slab3 {     // K3 fused slab: all n rows x cols [c0, c0 + ncols) of `mat`
-  int mat, c0, ncols, cql, vec, first;
-  int map;         // >= 0: 2-D TMA tensor map index (box C x brows); -1: one bulk copy per row
-  int stride;      // smem floats per slab row
-  int brows, pad0, pad1, pad2;
-};
-
-constexpr int K3_MAXMAPS = 64;
-struct K3Maps {    // __grid_constant__ kernel parameter (8 KB)
-  CUtensorMap map[K3_MAXMAPS];
-};
-
-struct SlabItem {  // tall-matrix split-n q item (register slab)
+struct SlabItem {  // K3 item: column slab [c0, c0 + C) x row chunk `chunk` of `mat` (nchunks == 1: fused)
   long long ws_off;
   int mat, c0, chunk, nchunks, slab, vec, cq_log2, pad;
 };
@@ -170,15 +160,29 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar)), "l"(pol)
       : "memory");
 }
+#ifndef PSGD_STORE_HINT
+#define PSGD_STORE_HINT 1
+#endif
+#ifndef PSGD_PDL
+#define PSGD_PDL 1
+#endif
 __device__ __forceinline__ void st_hint(float4* p, float4 v, uint64_t pol) {
+#if !PSGD_STORE_HINT
+  *p = v;
+  return;
+#endif
   asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
                "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
                : "memory");
 }
 __device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
+#if !PSGD_STORE_HINT
+  *p = v;
+  return;
+#endif
   asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
 }
-__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -235,20 +239,20 @@ struct BlockReducer {  // all threads of the CTA, __syncthreads
   }
 };
 
-struct ConsumerReducer {  // the 256 consumer threads of a TMA CTA, named barrier 1
-  double* red;            // 2 x 8 doubles (double-buffered by call parity)
+struct ConsumerReducer {  // the consumer threads of a TMA CTA, named barrier 1
+  double* red;            // 2 x kConsWarps doubles (double-buffered by call parity)
   int* parity;
   __device__ double sum(double v) const {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* buf = red + 8 * (*parity & 1);
+    double* buf = red + kConsWarps * (*parity & 1);
     ++*parity;
     if (lane == 0) buf[warp] = v;
     bar_consumers();
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) t += buf[w];
+    for (int w = 0; w < kConsWarps; ++w) t += buf[w];
     return t;
   }
 };
@@ -291,7 +295,8 @@ __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ 
       nrm = sqrt(red.sum(s));
       ++attempt;
     }
-    for (int i = tid; i < n; i += nth) x[i * r + j] /= nrm;
+    const double inv = 1.0 / nrm;  // one fp64 divide; the column scales by the reciprocal
+    for (int i = tid; i < n; i += nth) x[i * r + j] *= inv;
   }
 }
 
@@ -339,7 +344,7 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
   const int G = 1 << lg;
   const int gl = t & (G - 1);
   const int gid = t >> lg;
-  const int rpp = kThreads >> lg;
+  const int rpp = kCons >> lg;
   const long long a4 = ch.off & ~3LL;
   for (int rb = 0; rb < ch.nrows; rb += rpp) {
     const int li = rb + gid;
@@ -358,7 +363,6 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
         const int j = x < head ? x : head + 4 * body4 + (x - head);
         const float gv = sg[sm + j];
         const float d = has_e ? gv + se[sm + j] : gv;
-        bad |= !finite1(gv);
         st_hint(work + og + j, d, keep);
         const float* qj = Qm + (long long)(ch.c0 + j) * r;
 #pragma unroll
@@ -375,7 +379,6 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
         const float4 gv = g4[c];
         const float4 ev = has_e ? e4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 d = make_float4(gv.x + ev.x, gv.y + ev.y, gv.z + ev.z, gv.w + ev.w);
-        bad |= !finite4(gv);
         st_hint(w4 + c, d, keep);
         float qv[4][RM];
         k1_q4<RM, QS>(qrow + (long long)(4 * c) * r, qal, r, qv);
@@ -396,7 +399,10 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
         float* dst = P + md.p_off + (long long)(ch.row0 + li) * r;
 #pragma unroll
         for (int q = 0; q < RM; ++q)
-          if (q < r) dst[q] = acc[q];
+          if (q < r) {
+            dst[q] = acc[q];
+            bad |= !finite1(acc[q]);  // a non-finite delta poisons its P row (inf*0 = NaN too)
+          }
       }
     } else {  // multi-warp rows: per-warp partials, combined once per chunk below
 #pragma unroll
@@ -405,29 +411,30 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
         for (int q = 0; q < RM; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
       if (active && lane == 0) {
 #pragma unroll
-        for (int q = 0; q < RM; ++q) red[(li * 8 + warp) * RM + q] = acc[q];
+        for (int q = 0; q < RM; ++q) red[(li * kConsWarps + warp) * RM + q] = acc[q];
       }
     }
   }
   if (G > 32) {
     bar_consumers();
     const int nw = G >> 5;
-    for (int o = t; o < ch.nrows * r; o += kThreads) {
+    for (int o = t; o < ch.nrows * r; o += kCons) {
       const int li = o / r, q = o - li * r;
       const int w0 = (li % rpp) * nw;
       float s = 0.f;
-      for (int w = 0; w < nw; ++w) s += red[(li * 8 + w0 + w) * RM + q];
+      for (int w = 0; w < nw; ++w) s += red[(li * kConsWarps + w0 + w) * RM + q];
+      bad |= !finite1(s);
       if (ch.split < 0) {
         P[md.p_off + (long long)(ch.row0 + li) * r + q] = s;
       } else {
-        red[(K1_RED_ROWS * 8) * RM + q] = s;  // staged for the split combine below
+        red[(K1_RED_ROWS * kConsWarps) * RM + q] = s;  // staged for the split combine below
       }
     }
     if (ch.split >= 0) {
       bar_consumers();
       if (t == 0) {  // segment of an over-long row: the last-arriving segment combines in part order
         const SplitRow sp = splits[ch.split];
-        for (int q = 0; q < r; ++q) psplit[(long long)(sp.base + ch.part) * r + q] = red[(K1_RED_ROWS * 8) * RM + q];
+        for (int q = 0; q < r; ++q) psplit[(long long)(sp.base + ch.part) * r + q] = red[(K1_RED_ROWS * kConsWarps) * RM + q];
         __threadfence();
         if (atomicAdd(split_cnt + ch.split, 1) == sp.parts - 1) {
           __threadfence();
@@ -466,29 +473,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if (t == 0) {
     for (int s = 0; s < K1_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
+      mbar_init(&empty[s], kConsWarps);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qfull[s], 1);
-      mbar_init(&qempty[s], 8);
+      mbar_init(&qempty[s], kConsWarps);
     }
     *sflag = 0;
     fence_mbar_init();
   }
   __syncthreads();
+#if PSGD_PDL
   pdl_trigger();  // let the next kernel's CTAs stage in as ours retire
+#endif
 
-  if (warp == 8) {  // ---------------- producer
+  if (warp == kConsWarps) {  // ---------------- producer
     if (lane == 0) {
       const uint64_t pol = pol_evict_first();
       const uint64_t polq = pol_evict_last();
       int cur = -1, mseq = -1;
+      Chunk1 nx = chunks[cb < ce ? cb : 0];
+      MatDev md{};
       for (int k = cb; k < ce; ++k) {
         const int s = (k - cb) % K1_STAGES;
         const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
-        const Chunk1 ch = chunks[k];
-        const MatDev md = mats[ch.mat];
+        const Chunk1 ch = nx;
+        if (k + 1 < ce) nx = chunks[k + 1];  // next descriptor in flight
         if (ch.mat != cur) {  // Q of the next matrix into a smem slot (double-buffered)
+          md = mats[ch.mat];
           cur = ch.mat;
           ++mseq;
           if (md.qs) {
@@ -512,9 +524,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     return;
   }
 
-  // ---------------- consumers (256 threads)
+  // ---------------- consumers
   bool bad = false;
-  for (long long x = (long long)blockIdx.x * kThreads + t; x < nbias; x += (long long)gridDim.x * kThreads) {
+  for (long long x = (long long)blockIdx.x * kCons + t; x < nbias; x += (long long)gridDim.x * kCons) {
     const float v = bias_g[x];  // bias rides in the P all-reduce (optimizer.py:111-113)
     bad |= !finite1(v);
     P[bias_off + x] = v;
@@ -522,16 +534,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   const uint64_t keep = pol_evict_last();
   int cur = -1, mseq = -1, rpar = 0;
   bool cur_qs = false;
+  Chunk1 nx = chunks[cb < ce ? cb : 0];
+  MatDev md{};
   for (int k = cb; k < ce; ++k) {
     const int s = (k - cb) % K1_STAGES;
     const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
-    const Chunk1 ch = chunks[k];
-    const MatDev md = mats[ch.mat];
+    const Chunk1 ch = nx;
+    if (k + 1 < ce) nx = chunks[k + 1];  // next descriptor in flight
     if (ch.mat != cur) {
       if (cur >= 0 && cur_qs) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&qempty[mseq & 1]);
       }
+      md = mats[ch.mat];
       cur = ch.mat;
       ++mseq;
       cur_qs = md.qs != 0;
@@ -540,12 +555,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     mbar_wait(&full[s], ph);
     const float* sg = sgb + s * K1_STAGE_FLOATS;
     const float* se = seb + s * K1_STAGE_FLOATS;
-    float* rb = red + (rpar & 1) * (K1_RED_ROWS * 8 * RM + RM);
+    float* rb = red + (rpar & 1) * (K1_RED_ROWS * kConsWarps * RM + RM);
     if ((1 << md.lg1) > 32) ++rpar;
+#ifdef PSGD_K1_NOCOMPUTE
+    if (false)
+#else
     if (cur_qs)
+#endif
       k1_chunk<RM, true>(ch, md, qsl + (mseq & 1) * L.qslot_floats, sg, se, e != nullptr, work, P, splits,
                          psplit, split_cnt, rb, keep, bad);
+#ifndef PSGD_K1_NOCOMPUTE
     else
+#else
+    else if (false)
+#endif
       k1_chunk<RM, false>(ch, md, Q + md.q_off, sg, se, e != nullptr, work, P, splits, psplit, split_cnt,
                           rb, keep, bad);
     __syncwarp();
@@ -560,23 +583,48 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 }
 
 // ============================================================================= K2
-// standalone / tall-matrix Gram-Schmidt: P-hat = MGS(P / W)  (comm.py:97-98, linalg.py:61-90)
+// P-hat = MGS(P / W) for every listed matrix, one CTA each (comm.py:97-98,
+// linalg.py:61-90), float64 in smem when it fits; plus the bias mean
+// (optimizer.py:111-113) in the trailing CTAs.  Launched with programmatic
+// dependent launch: it waits for K1 (or the all-reduce), then immediately lets
+// K3 launch, so K3's CTAs stream their delta slabs in while this runs.
+
+struct SyncReducer {  // all threads of the CTA, one __syncthreads per reduction
+  double* red;        // 2 x 32 doubles, double-buffered by call parity
+  int* parity;
+  __device__ double sum(double v) const {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* buf = red + 32 * (*parity & 1);
+    ++*parity;
+    if (lane == 0) buf[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += buf[w];
+    return t;
+  }
+};
+
+constexpr int K2_SMEM_DOUBLES = 12288;  // 96 KB: n * r up to this stays in smem
 
 __global__ void __launch_bounds__(kGsThreads)
     k2_gs(const MatDev* __restrict__ mats, const int* __restrict__ list, int nlist,
           const float* __restrict__ P, float* __restrict__ Phat, int divisor,
           const double* __restrict__ repl, double* __restrict__ ws, float* __restrict__ bias_out,
           long long bias_off, long long nbias, long long flag_off, int nflags, int* status) {
-  __shared__ double red[40];
+  extern __shared__ __align__(16) double k2smem[];
+  __shared__ double red[64];
+  pdl_wait();     // P (K1 output or the all-reduce result) is complete
+  pdl_trigger();  // K3 may launch now: it only touches P-hat after its own wait
   {
     int bad = 0;  // a non-finite gradient anywhere (any rank) poisons the whole step
     for (int x = threadIdx.x; x < nflags; x += blockDim.x) bad |= P[flag_off + x] != 0.f;
-    if (__syncthreads_or(bad) || (*status & PSGD_STATUS_NONFINITE_GRAD)) {
-      if (threadIdx.x == 0 && bad) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+    if (__syncthreads_or(bad)) {
+      if (threadIdx.x == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
       return;
     }
   }
-  const double div = (double)divisor;
   if ((int)blockIdx.x >= nlist) {  // bias mean: P tail / W
     const long long nb = gridDim.x - nlist;
     bool bad = false;
@@ -591,279 +639,47 @@ __global__ void __launch_bounds__(kGsThreads)
   }
   const MatDev md = mats[list[blockIdx.x]];
   const int n = md.n, r = md.r;
-  double* __restrict__ x = ws + md.p_off;
+  double* __restrict__ x = (n * r <= K2_SMEM_DOUBLES) ? k2smem : ws + md.p_off;
+  const double inv_div = 1.0 / (double)divisor;
   int bad = 0;
   for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
     const float v = P[md.p_off + idx];
     bad |= !finite1(v);
-    x[idx] = (double)v / div;
+    x[idx] = (double)v * inv_div;
   }
   if (__syncthreads_or(bad)) {  // linalg.py:35-36 (ContractViolation)
     if (threadIdx.x == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
     return;
   }
-  BlockReducer br{red};
-  mgs_inplace(x, n, r, repl + md.repl_off, threadIdx.x, blockDim.x, br, status);
+  int par = 0;
+  SyncReducer sr{red, &par};
+  mgs_inplace(x, n, r, repl + md.repl_off, threadIdx.x, blockDim.x, sr, status);
   __syncthreads();  // rows were thread-owned above; the copy-out mapping differs
   for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) Phat[md.p_off + idx] = (float)x[idx];
 }
 
-// ============================================================================= K3 (fused)
-// per slab (all n rows x C cols): [GS of the matrix if new to this CTA] ;
-// q_w = delta^T P-hat ; e = delta - P-hat q_w^T ; M-hat (W=1)   (compressors.py:338-339,375-378)
-
-struct K3Layout {  // byte offsets inside dynamic smem
-  int stage_floats;
-  int off_gs, off_ps, off_red, off_qs, off_dred, off_bar, total;
-};
-
-template <int RM>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-    k3_q_ef(const MatDev* __restrict__ mats, const Slab3* __restrict__ slabs,
-            const int* __restrict__ cta_beg, K3Layout L, const __grid_constant__ K3Maps maps,
-            float* __restrict__ work,
-            const float* __restrict__ P, int divisor, const double* __restrict__ repl,
-            float* __restrict__ Phat, float* __restrict__ qout, float* __restrict__ e,
-            float* __restrict__ bias_out, long long nbias, long long bias_off, long long flag_off,
-            int nflags, int write_mhat, int* status) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* stage0 = reinterpret_cast<float*>(smem_raw);
-  double* gsd = reinterpret_cast<double*>(smem_raw + L.off_gs);
-  float* ps = reinterpret_cast<float*>(smem_raw + L.off_ps);
-  float* red = reinterpret_cast<float*>(smem_raw + L.off_red);
-  float* qs = reinterpret_cast<float*>(smem_raw + L.off_qs);
-  double* dred = reinterpret_cast<double*>(smem_raw + L.off_dred);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
-  uint64_t* empty = full + K3_STAGES;
-
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int cb = cta_beg[blockIdx.x], ce = cta_beg[blockIdx.x + 1];
-  if (t == 0) {
-    for (int s = 0; s < K3_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
-    }
-    fence_mbar_init();
-  }
-  pdl_wait();  // K1's delta / P (or the all-reduce) must be complete and visible
-  {
-    int bad = 0;
-    for (int x = t; x < nflags; x += kTmaThreads) bad |= P[flag_off + x] != 0.f;
-    if (__syncthreads_or(bad)) {  // optimizer.py:72-76: nothing is mutated
-      if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
-      return;
-    }
-  }
-
-  if (warp == 8) {  // ---------------- producer: 2-D tensor tiles, or one bulk copy per row
-    const uint64_t pol = pol_evict_first();
-    for (int k = cb; k < ce; ++k) {
-      const int s = (k - cb) % K3_STAGES;
-      const uint32_t ph = ((k - cb) / K3_STAGES) & 1;
-      const Slab3 sl = slabs[k];
-      const MatDev md = mats[sl.mat];
-      const int C = sl.vec << sl.cql;
-      float* stg = stage0 + (long long)s * L.stage_floats;
-      if (lane == 0) mbar_wait(&empty[s], ph ^ 1);
-      __syncwarp();
-      if (sl.map >= 0) {
-        if (lane == 0) {
-          const int nbox = (md.n + sl.brows - 1) / sl.brows;
-          mbar_expect_tx(&full[s], (uint32_t)(nbox * sl.brows * C * 4));
-          for (int b = 0; b < nbox; ++b)
-            tma_load_2d(stg + (long long)b * sl.brows * C, &maps.map[sl.map], sl.c0, b * sl.brows, &full[s], pol);
-        }
-        continue;
-      }
-      uint32_t bytes = 0;
-      for (int i = lane; i < md.n; i += 32) {
-        const long long st = md.flat_off + (long long)i * md.m + sl.c0;
-        bytes += (uint32_t)((((st + sl.ncols + 3) & ~3LL) - (st & ~3LL)) * 4);
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
-      if (lane == 0) mbar_expect_tx(&full[s], bytes);
-      __syncwarp();
-      for (int i = lane; i < md.n; i += 32) {
-        const long long st = md.flat_off + (long long)i * md.m + sl.c0;
-        const long long a4 = st & ~3LL;
-        const uint32_t b = (uint32_t)((((st + sl.ncols + 3) & ~3LL) - a4) * 4);
-        tma_load(stg + i * sl.stride, work + a4, b, &full[s], pol);
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumers
-  {
-    bool bad = false;
-    for (long long x = (long long)blockIdx.x * kThreads + t; x < nbias; x += (long long)gridDim.x * kThreads) {
-      const float v = P[bias_off + x];
-      bad |= !finite1(v);
-      bias_out[x] = divisor == 1 ? v : v / (float)divisor;
-    }
-    if (bad) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
-  }
-  int rpar = 0;
-  ConsumerReducer cr{dred, &rpar};
-  int cur = -1;
-  bool skip = false;
-  const double div = (double)divisor;
-  for (int k = cb; k < ce; ++k) {
-    const int s = (k - cb) % K3_STAGES;
-    const uint32_t ph = ((k - cb) / K3_STAGES) & 1;
-    const Slab3 sl = slabs[k];
-    const MatDev md = mats[sl.mat];
-    const int n = md.n, m = md.m, r = md.r;
-    if (sl.mat != cur) {  // ---- Gram-Schmidt of this matrix (overlaps the slab's TMA)
-      cur = sl.mat;
-      bar_consumers();  // previous slab's readers of ps are done
-      int bad = 0;
-      for (int idx = t; idx < n * r; idx += kThreads) {
-        const float v = P[md.p_off + idx];
-        bad |= !finite1(v);
-        gsd[idx] = (double)v / div;
-      }
-      skip = cr.sum(bad ? 1.0 : 0.0) != 0.0;
-      if (skip) {
-        if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
-      } else {
-        mgs_inplace(gsd, n, r, repl + md.repl_off, t, kThreads, cr, status);
-        bar_consumers();
-        for (int idx = t; idx < n * r; idx += kThreads) {
-          const float v = (float)gsd[idx];
-          ps[idx] = v;
-          if (sl.first) Phat[md.p_off + idx] = v;
-        }
-        bar_consumers();
-      }
-    }
-    mbar_wait(&full[s], ph);
-    const float* stg = stage0 + (long long)s * L.stage_floats;
-    if (!skip) {
-      const int vec = sl.vec, cql = sl.cql;
-      const int CQ = 1 << cql, C = vec << cql, RG = kThreads >> cql, stride = sl.stride;
-      const int cq = t & (CQ - 1), rg = t >> cql;
-      const int col = cq * vec;
-      const bool colok = col < sl.ncols;
-      float qp[4][RM];
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-#pragma unroll
-        for (int q = 0; q < RM; ++q) qp[v][q] = 0.f;
-      if (colok) {
-        if (vec == 4) {
-          for (int i = rg; i < n; i += RG) {
-            const float4 d = *reinterpret_cast<const float4*>(stg + i * stride + col);
-            const float dv[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-            for (int q = 0; q < RM; ++q) {
-              if (q < r) {
-                const float pk = ps[i * r + q];
-#pragma unroll
-                for (int v = 0; v < 4; ++v) qp[v][q] = fmaf(dv[v], pk, qp[v][q]);
-              }
-            }
-          }
-        } else {
-          for (int i = rg; i < n; i += RG) {
-            const int dl = (int)((md.flat_off + (long long)i * m + sl.c0) & 3);
-            const float d = stg[i * stride + dl + col];
-#pragma unroll
-            for (int q = 0; q < RM; ++q)
-              if (q < r) qp[0][q] = fmaf(d, ps[i * r + q], qp[0][q]);
-          }
-        }
-      }
-      // fixed-order reduction: in-warp over row groups sharing cq, then over warps
-      if (CQ < 32) {
-        for (int off = CQ; off < 32; off <<= 1)
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-#pragma unroll
-            for (int q = 0; q < RM; ++q) qp[v][q] += __shfl_xor_sync(0xffffffffu, qp[v][q], off);
-      }
-      if (CQ >= 32 || lane < CQ) {
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-#pragma unroll
-          for (int q = 0; q < RM; ++q)
-            if (v < vec && q < r) red[warp * K3_QMAX + (col + v) * r + q] = qp[v][q];
-      }
-      bar_consumers();
-      for (int o = t; o < C * r; o += kThreads) {
-        const int cqo = (o / r) / vec;
-        float sacc = 0.f;
-        if (CQ <= 32) {
-#pragma unroll
-          for (int w = 0; w < 8; ++w) sacc += red[w * K3_QMAX + o];
-        } else {
-          const int per = CQ >> 5;  // warps per row group
-          for (int w = (cqo >> 5); w < 8; w += per) sacc += red[w * K3_QMAX + o];
-        }
-        qs[o] = sacc;
-      }
-      bar_consumers();
-      {
-        float* qd = qout + md.q_off + (long long)sl.c0 * r;
-        for (int o = t; o < sl.ncols * r; o += kThreads) qd[o] = qs[o];
-      }
-      // error feedback (and M-hat at W=1) from the same smem copy of delta
-      if (colok) {
-        float qv[4][RM];
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-#pragma unroll
-          for (int q = 0; q < RM; ++q) qv[v][q] = (v < vec && q < r) ? qs[(col + v) * r + q] : 0.f;
-        if (vec == 4) {
-          for (int i = rg; i < n; i += RG) {
-            const float4 d = *reinterpret_cast<const float4*>(stg + i * stride + col);
-            float mh[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int q = 0; q < RM; ++q) {
-              if (q < r) {
-                const float pk = ps[i * r + q];
-#pragma unroll
-                for (int v = 0; v < 4; ++v) mh[v] = fmaf(pk, qv[v][q], mh[v]);
-              }
-            }
-            const long long a = md.flat_off + (long long)i * m + sl.c0 + col;
-            st_stream(reinterpret_cast<float4*>(e + a),
-                      make_float4(d.x - mh[0], d.y - mh[1], d.z - mh[2], d.w - mh[3]));
-            if (write_mhat)
-              st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
-          }
-        } else {
-          for (int i = rg; i < n; i += RG) {
-            const long long a0 = md.flat_off + (long long)i * m + sl.c0;
-            const float d = stg[i * stride + (int)(a0 & 3) + col];
-            float mh = 0.f;
-#pragma unroll
-            for (int q = 0; q < RM; ++q)
-              if (q < r) mh = fmaf(ps[i * r + q], qv[0][q], mh);
-            st_stream(e + a0 + col, d - mh);
-            if (write_mhat) st_stream(work + a0 + col, mh);
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-}
-
-// ============================================================================= tall path
-// split-n q partials for matrices with n > kFusedNMax (register slab, last CTA reduces)
+// ============================================================================= K3
+// One CTA per column slab (all n rows x C cols of one matrix, or a chunk of
+// rows for tall matrices), the slab held in registers: every load is issued
+// up front (64 KB in flight per CTA), then the CTA waits (PDL) for K2's P-hat.
+//   fused (n <= rows per CTA): q_w = delta^T P-hat, e = delta - P-hat q_w^T and
+//     M-hat at W = 1 from the same registers: delta is read once
+//     (compressors.py:339,375-378, optimizer.py:124-127).
+//   tall (n > rows per CTA): a chunk of rows contributes a partial q; the
+//     last-arriving chunk of the slab sums the partials in chunk order; the EF
+//     pass is K4.
 
 template <int R, bool EXACT>
 __global__ void __launch_bounds__(kThreads, 2)
-    k3_tall(const MatDev* __restrict__ mats, const SlabItem* __restrict__ items,
-            const float* __restrict__ work, const float* __restrict__ Phat, float* __restrict__ qout,
-            float* __restrict__ wsq, int* __restrict__ counters, const int* __restrict__ status) {
+    k3_slab(const MatDev* __restrict__ mats, const SlabItem* __restrict__ items, float* __restrict__ work,
+            const float* __restrict__ Phat, float* __restrict__ qout, float* __restrict__ e,
+            float* __restrict__ wsq, int* __restrict__ counters, int write_mhat, const int* status) {
   constexpr int DCAP = k3_dcap(R);
-  extern __shared__ float smem[];
-  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
+  extern __shared__ __align__(16) unsigned char k3smem[];
+  __shared__ int s_flag;
   const SlabItem it = items[blockIdx.x];
+  const int t = threadIdx.x;
+  const bool fused = it.nchunks == 1;
   const MatDev md = mats[it.mat];
   const int r = EXACT ? R : md.r;
   const int n = md.n, m = md.m;
@@ -874,7 +690,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int RG = kThreads >> cql;
   const int smax = DCAP / vec;
   const int rows_chunk = RG * smax;
-  const int t = threadIdx.x;
   const int cq = t & (CQ - 1);
   const int rg = t >> cql;
   const int col = it.c0 + cq * vec;
@@ -882,10 +697,12 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int rbeg = it.chunk * rows_chunk;
   const int nrows = min(n - rbeg, rows_chunk);
   const int ncols = min(C, m - it.c0);
-  float* ps = smem;
-  float* red = ps + rows_chunk * r;
-  float* qs = red + RG * C * r;
+  float* ps = reinterpret_cast<float*>(k3smem);  // nrows x r
+  float* red = ps + rows_chunk * r;              // RG x C x r
+  float* qs = red + RG * C * r;                  // C x r
 
+  // 1. every load of the slab in flight at once (delta is final: K2 started
+  //    after K1 completed, and this grid starts after K2's trigger)
   float d[DCAP];
   const long long base = md.flat_off + (long long)rbeg * m + col;
   if (vec == 4) {
@@ -893,21 +710,25 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int s = 0; s < DCAP / 4; ++s) {
       const int li = rg + RG * s;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (colok && li < nrows) v = __ldcg(reinterpret_cast<const float4*>(work + base + (long long)li * m));
+      if (colok && li < nrows) v = __ldcs(reinterpret_cast<const float4*>(work + base + (long long)li * m));
       d[4 * s + 0] = v.x; d[4 * s + 1] = v.y; d[4 * s + 2] = v.z; d[4 * s + 3] = v.w;
     }
   } else {
 #pragma unroll
     for (int s = 0; s < DCAP; ++s) {
       const int li = rg + RG * s;
-      d[s] = (colok && li < nrows) ? __ldcg(work + base + (long long)li * m) : 0.f;
+      d[s] = (colok && li < nrows) ? __ldcs(work + base + (long long)li * m) : 0.f;
     }
   }
+  // 2. P-hat of the rows, from K2 (wait for it; nothing is mutated on failure)
+  pdl_wait();
+  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
   {
     const float* src = Phat + md.p_off + (long long)rbeg * r;
     for (int x = t; x < nrows * r; x += kThreads) ps[x] = src[x];
   }
   __syncthreads();
+  // 3. per-thread partial q over its rows
   float qp[4][R];
 #pragma unroll
   for (int v = 0; v < 4; ++v)
@@ -939,6 +760,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
   }
+  // 4. fixed-order reduction over the row groups
 #pragma unroll
   for (int v = 0; v < 4; ++v)
 #pragma unroll
@@ -952,21 +774,67 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   __syncthreads();
   float* __restrict__ qdst = qout + md.q_off + (long long)it.c0 * r;
-  float* part = wsq + it.ws_off;
-  for (int o = t; o < ncols * r; o += kThreads) part[(long long)it.chunk * C * r + o] = qs[o];
-  __threadfence();
-  __syncthreads();
-  __shared__ int is_last;
-  if (t == 0) is_last = atomicAdd(counters + it.slab, 1) == it.nchunks - 1;
-  __syncthreads();
-  if (is_last) {
+  if (!fused) {  // partial of a tall slab; the last chunk combines in chunk order
+    float* part = wsq + it.ws_off;
+    for (int o = t; o < ncols * r; o += kThreads) part[(long long)it.chunk * C * r + o] = qs[o];
     __threadfence();
-    for (int o = t; o < ncols * r; o += kThreads) {
-      float s = 0.f;
-      for (int ch = 0; ch < it.nchunks; ++ch) s += __ldcg(part + (long long)ch * C * r + o);
-      qdst[o] = s;
+    __syncthreads();
+    if (t == 0) s_flag = atomicAdd(counters + it.slab, 1) == it.nchunks - 1;
+    __syncthreads();
+    if (s_flag) {
+      __threadfence();
+      for (int o = t; o < ncols * r; o += kThreads) {
+        float s = 0.f;
+        for (int ch = 0; ch < it.nchunks; ++ch) s += __ldcg(part + (long long)ch * C * r + o);
+        qdst[o] = s;
+      }
+      if (t == 0) counters[it.slab] = 0;
     }
-    if (t == 0) counters[it.slab] = 0;
+    return;
+  }
+  for (int o = t; o < ncols * r; o += kThreads) qdst[o] = qs[o];
+  // 5. error feedback (and M-hat at W=1) from the registers
+  float qv[4][R];
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      qv[v][k] = (v < vec && (EXACT || k < r)) ? qs[(cq * vec + v) * r + k] : 0.f;
+  if (!colok) return;
+  if (vec == 4) {
+#pragma unroll
+    for (int s = 0; s < DCAP / 4; ++s) {
+      const int li = rg + RG * s;
+      if (li < nrows) {
+        float mh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          if (EXACT || k < r) {
+            const float pk = ps[li * r + k];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) mh[v] = fmaf(pk, qv[v][k], mh[v]);
+          }
+        }
+        const long long a = base + (long long)li * m;
+        st_stream(reinterpret_cast<float4*>(e + a),
+                  make_float4(d[4 * s] - mh[0], d[4 * s + 1] - mh[1], d[4 * s + 2] - mh[2], d[4 * s + 3] - mh[3]));
+        if (write_mhat) st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < DCAP; ++s) {
+      const int li = rg + RG * s;
+      if (li < nrows) {
+        float mh = 0.f;
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (EXACT || k < r) mh = fmaf(ps[li * r + k], qv[0][k], mh);
+        const long long a = base + (long long)li * m;
+        st_stream(e + a, d[s] - mh);
+        if (write_mhat) st_stream(work + a, mh);
+      }
+    }
   }
 }
 
@@ -1127,18 +995,12 @@ struct psgd_plan {
   std::vector<SplitRow> splits;
   long long psplit_elems = 0;
   // K3 fused
-  std::vector<Slab3> k3;
-  std::vector<int> k3_beg;
-  K3Layout k3l{};
-  std::vector<int> map_mat;          // tensor-map index -> matrix
-  std::vector<int> map_cols, map_rows;
-  // tensor maps bind the work buffer's address: encoded on first use per buffer
-  mutable std::mutex map_mu;
-  mutable std::vector<std::pair<const void*, K3Maps*>> map_cache;
+  int k2_smem = 0;
+  std::vector<SlabItem> k3;          // fused and tall slabs, grouped by r
+  std::vector<Group> g3;
+
   // tall path
   std::vector<int> tall_list, all_list;
-  std::vector<SlabItem> k3t;
-  std::vector<Group> g3t;
   std::vector<RowItem> k4, k5;
   std::vector<Group> g4, g5;
   int n_tall = 0, n_tall_slabs = 0;
@@ -1151,10 +1013,8 @@ struct psgd_plan {
   SplitRow* d_splits = nullptr;
   float* d_psplit = nullptr;
   int* d_split_cnt = nullptr;
-  Slab3* d_k3 = nullptr;
-  int* d_k3_beg = nullptr;
+  SlabItem* d_k3 = nullptr;
   int *d_tall_list = nullptr, *d_all_list = nullptr;
-  SlabItem* d_k3t = nullptr;
   RowItem *d_k4 = nullptr, *d_k5 = nullptr;
   double* d_gsws = nullptr;
   float* d_wsq = nullptr;
@@ -1279,9 +1139,9 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       delete pl;
       return fail(PSGD_EINVAL, "effective rank " + std::to_string(md.r) + " exceeds PSGD_MAX_RANK");
     }
-    md.tall = md.n > kFusedNMax;
-    md.lg1 = lanes_log2_for(md.m, 8);
-    md.qs = align4((long long)md.m * md.r) <= K1_QSLOT_CAP ? 1 : 0;
+    md.tall = k3_tall_config(md.n, md.m, md.r).nchunks > 1;
+    md.lg1 = lanes_log2_for(md.m, 9);
+    md.qs = 0;  // decided below, once the K1 smem budget is known
     md.flat_off = fo;
     md.p_off = po;
     md.q_off = qo;
@@ -1299,7 +1159,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->flat_elems = std::max(4LL, fo);
 
   // ---- K1 chunks: row-aligned, <= K1_CHUNK floats; over-long rows split into segments
-  const int seg = K1_CHUNK - 8;
+  const int seg = K1_CHUNK;
   for (int mi = 0; mi < nmat; ++mi) {
     const MatDev& md = pl->mats[mi];
     if (md.m <= seg) {
@@ -1310,13 +1170,14 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       }
     } else {
       const int parts = (md.m + seg - 1) / seg;
+      const int slen = (int)align4((md.m + parts - 1) / parts);  // equal segments
       for (int row = 0; row < md.n; ++row) {
         const int sid = (int)pl->splits.size();
         pl->splits.push_back({mi, row, (int)(pl->psplit_elems / md.r), parts});
         pl->psplit_elems += (long long)parts * md.r;
         for (int p = 0; p < parts; ++p) {
-          const int c0 = p * seg;
-          const int nc = std::min(seg, md.m - c0);
+          const int c0 = p * slen;
+          const int nc = std::min(slen, md.m - c0);
           pl->k1.push_back({md.flat_off + (long long)row * md.m + c0, mi, row, 1, c0, nc, sid, p, 0});
         }
       }
@@ -1330,13 +1191,19 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->nflags = std::max(1, (int)pl->k1_beg.size() - 1);
   {
     K1Layout& L = pl->k1l;
+    // Q slots get what the stages and reduction buffers leave of 227 KB
+    const long long fixed = 2LL * K1_STAGES * K1_STAGE_FLOATS * 4 +
+                            2LL * (K1_RED_ROWS * kConsWarps * pl->rmax + pl->rmax) * 4 + 512;
+    const long long cap = std::min<long long>(K1_QSLOT_CAP, ((227LL * 1024 - fixed) / 8) & ~3LL);
     long long qslot = 4;
-    for (auto& md : pl->mats)
+    for (auto& md : pl->mats) {
+      md.qs = align4((long long)md.m * md.r) <= cap ? 1 : 0;
       if (md.qs) qslot = std::max(qslot, align4((long long)md.m * md.r));
+    }
     L.qslot_floats = (int)qslot;
     int off = 2 * K1_STAGES * K1_STAGE_FLOATS * 4;
     L.off_q = off;   off += 2 * L.qslot_floats * 4;
-    L.off_red = off; off += 2 * (K1_RED_ROWS * 8 * pl->rmax + pl->rmax) * 4;
+    L.off_red = off; off += 2 * (K1_RED_ROWS * kConsWarps * pl->rmax + pl->rmax) * 4;
     off = (off + 15) & ~15;
     L.off_bar = off; off += (2 * K1_STAGES + 4) * 8 + 16;
     L.total = off;
@@ -1347,85 +1214,37 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->q_elems = std::max(4LL, qo);
   pl->repl_elems = std::max(1LL, ro);
 
-  // ---- K3 fused slabs (n <= kFusedNMax)
-  {
-    const int cmax512 = pl->rmax <= 8 ? 32 : 16;  // C at n = 512
-    const int stage_floats = kFusedNMax * (cmax512 + 8);
-    std::vector<double> w;
-    for (int mi = 0; mi < nmat; ++mi) {
-      const MatDev& md = pl->mats[mi];
-      if (md.tall) continue;
-      const int vec = (md.m % 4 == 0) ? 4 : 1;
-      const bool use_map = vec == 4 && (int)pl->map_mat.size() < K3_MAXMAPS;
-      const int brows = md.n <= 256 ? md.n : 256;
-      const int nbox = (md.n + brows - 1) / brows;
-      // widest power-of-two C that fits the stage (row copies: n x (C+8); tiles:
-      // nbox * brows x C), keeps C * r <= K3_QMAX, is not wider than needed for
-      // m, and maps onto 256 threads (CQ <= 256)
-      auto fits = [&](int C) {
-        if ((long long)C * md.r > K3_QMAX) return false;
-        if (use_map) return (long long)nbox * brows * C <= stage_floats && C <= 256;
-        return (long long)md.n * (C + 8) <= stage_floats;
-      };
-      int cql = vec == 4 ? 2 : 4;
-      while (cql < 8) {
-        const int C2 = vec << (cql + 1);
-        if (!fits(C2)) break;
-        if ((vec << cql) >= md.m) break;
-        ++cql;
-      }
-      const int C = vec << cql;
-      int map = -1;
-      if (use_map) {
-        map = (int)pl->map_mat.size();
-        pl->map_mat.push_back(mi);
-        pl->map_cols.push_back(C);
-        pl->map_rows.push_back(brows);
-      }
-      for (int c0 = 0; c0 < md.m; c0 += C) {
-        pl->k3.push_back({mi, c0, std::min(C, md.m - c0), cql, vec, c0 == 0 ? 1 : 0, map,
-                          use_map ? C : C + 8, brows, 0, 0, 0});
-        w.push_back((double)md.n * std::min(C, md.m - c0) + 256.0);
-      }
-    }
-    pl->k3_beg = balance(w, pl->nsm);
-    K3Layout& L = pl->k3l;
-    L.stage_floats = stage_floats;
-    int off = K3_STAGES * stage_floats * 4;
-    L.off_gs = off;   off += kFusedNMax * pl->rmax * 8;
-    L.off_ps = off;   off += kFusedNMax * pl->rmax * 4;
-    L.off_red = off;  off += 8 * K3_QMAX * 4;
-    L.off_qs = off;   off += K3_QMAX * 4;
-    L.off_dred = off; off += 16 * 8;
-    L.off_bar = off;  off += 2 * K3_STAGES * 8 + 16;
-    L.total = off;
-  }
-
-  // ---- tall path: split-n q items, K4 rows; K5 rows for every matrix
+  for (auto& md : pl->mats)
+    if ((long long)md.n * md.r <= K2_SMEM_DOUBLES) pl->k2_smem = std::max(pl->k2_smem, md.n * md.r * 8);
+  // ---- K3 slabs, grouped by r (one launch per group): fused slabs hold all rows
   {
     std::vector<int> rs;
     for (auto& md : pl->mats)
-      if (md.tall && std::find(rs.begin(), rs.end(), md.r) == rs.end()) rs.push_back(md.r);
+      if (std::find(rs.begin(), rs.end(), md.r) == rs.end()) rs.push_back(md.r);
     for (int r : rs) {
-      Group gp{r, (int)pl->k3t.size(), 0, 0};
+      Group gp{r, (int)pl->k3.size(), 0, 0};
       for (int mi = 0; mi < nmat; ++mi) {
         const MatDev& md = pl->mats[mi];
-        if (!md.tall || md.r != r) continue;
+        if (md.r != r) continue;
         const K3Cfg cf = k3_tall_config(md.n, md.m, r);
         const int CQ = 1 << cf.cql, C = CQ * cf.vec, RG = kThreads / CQ;
         const int nslab = (md.m + C - 1) / C;
         for (int s = 0; s < nslab; ++s) {
-          const int slab_id = pl->n_tall_slabs++;
-          const long long wo = pl->wsq_elems;
-          pl->wsq_elems += (long long)cf.nchunks * C * r;
+          int slab_id = -1;
+          long long wo = 0;
+          if (cf.nchunks > 1) {
+            slab_id = pl->n_tall_slabs++;
+            wo = pl->wsq_elems;
+            pl->wsq_elems += (long long)cf.nchunks * C * r;
+          }
           for (int ch = 0; ch < cf.nchunks; ++ch)
-            pl->k3t.push_back({wo, mi, s * C, ch, cf.nchunks, slab_id, cf.vec, cf.cql, 0});
+            pl->k3.push_back({wo, mi, s * C, ch, cf.nchunks, slab_id, cf.vec, cf.cql, 0});
         }
         const int smem = (cf.rows_chunk * r + RG * C * r + C * r) * (int)sizeof(float);
         gp.smem = std::max(gp.smem, smem);
       }
-      gp.end = (int)pl->k3t.size();
-      pl->g3t.push_back(gp);
+      gp.end = (int)pl->k3.size();
+      pl->g3.push_back(gp);
     }
   }
   build_row_items(pl->mats, true, pl->k4, pl->g4);
@@ -1445,11 +1264,9 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_spl = take(pl->splits.size() * sizeof(SplitRow));
   const size_t o_psp = take((size_t)pl->psplit_elems * sizeof(float));
   const size_t o_spc = take(pl->splits.size() * sizeof(int));
-  const size_t o_k3 = take(pl->k3.size() * sizeof(Slab3));
-  const size_t o_k3b = take(pl->k3_beg.size() * sizeof(int));
+  const size_t o_k3 = take(pl->k3.size() * sizeof(SlabItem));
   const size_t o_tl = take(pl->tall_list.size() * sizeof(int));
   const size_t o_al = take(pl->all_list.size() * sizeof(int));
-  const size_t o_k3t = take(pl->k3t.size() * sizeof(SlabItem));
   const size_t o_k4 = take(pl->k4.size() * sizeof(RowItem));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
@@ -1467,11 +1284,9 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_splits = reinterpret_cast<SplitRow*>(b + o_spl);
   pl->d_psplit = reinterpret_cast<float*>(b + o_psp);
   pl->d_split_cnt = reinterpret_cast<int*>(b + o_spc);
-  pl->d_k3 = reinterpret_cast<Slab3*>(b + o_k3);
-  pl->d_k3_beg = reinterpret_cast<int*>(b + o_k3b);
+  pl->d_k3 = reinterpret_cast<SlabItem*>(b + o_k3);
   pl->d_tall_list = reinterpret_cast<int*>(b + o_tl);
   pl->d_all_list = reinterpret_cast<int*>(b + o_al);
-  pl->d_k3t = reinterpret_cast<SlabItem*>(b + o_k3t);
   pl->d_k4 = reinterpret_cast<RowItem*>(b + o_k4);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
@@ -1484,11 +1299,9 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_k1, pl->k1.data(), pl->k1.size() * sizeof(Chunk1));
   if (ce == cudaSuccess) ce = up(pl->d_k1_beg, pl->k1_beg.data(), pl->k1_beg.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_splits, pl->splits.data(), pl->splits.size() * sizeof(SplitRow));
-  if (ce == cudaSuccess) ce = up(pl->d_k3, pl->k3.data(), pl->k3.size() * sizeof(Slab3));
-  if (ce == cudaSuccess) ce = up(pl->d_k3_beg, pl->k3_beg.data(), pl->k3_beg.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_k3, pl->k3.data(), pl->k3.size() * sizeof(SlabItem));
   if (ce == cudaSuccess) ce = up(pl->d_tall_list, pl->tall_list.data(), pl->tall_list.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_all_list, pl->all_list.data(), pl->all_list.size() * sizeof(int));
-  if (ce == cudaSuccess) ce = up(pl->d_k3t, pl->k3t.data(), pl->k3t.size() * sizeof(SlabItem));
   if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
@@ -1504,7 +1317,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
 
 int psgd_plan_destroy(psgd_plan* plan) {
   if (!plan) return PSGD_OK;
-  for (auto& kv : plan->map_cache) delete kv.second;
   if (plan->dev_block) cudaFree(plan->dev_block);
   delete plan;
   return PSGD_OK;
@@ -1523,17 +1335,17 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->world = pl->world;
   o->n_tall = pl->n_tall;
   o->items_k1 = (int64_t)pl->k1.size();
-  o->items_k3 = (int64_t)(pl->k3.size() + pl->k3t.size());
+  o->items_k3 = (int64_t)pl->k3.size();
   auto nonempty = [](const std::vector<Group>& gs) {
     int c = 0;
     for (const Group& g : gs) c += g.end > g.beg;
     return c;
   };
-  const bool fused = !pl->k3.empty();
+  const bool any_fused = pl->n_tall < pl->nmat;
   o->launches_ef_p = (pl->k1.empty() && pl->nbias == 0) ? 0 : 1;
   o->launches_orthogonalize = (pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0;
-  o->launches_q_ef = (fused ? 1 : 0) + ((pl->n_tall > 0 || (!fused && pl->nbias > 0)) ? 1 : 0) +
-                     nonempty(pl->g3t) + nonempty(pl->g4);
+  o->launches_q_ef = ((pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0) + nonempty(pl->g3) + nonempty(pl->g4);
+  (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
   return PSGD_OK;
 }
@@ -1591,79 +1403,18 @@ int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, con
   return PSGD_OK;
 }
 
-// 2-D tensor maps of the fused vec-4 matrices inside `work` (cached per buffer)
-int k3_maps_for(const psgd_plan* pl, const float* work, const K3Maps** out) {
-  std::lock_guard<std::mutex> lk(pl->map_mu);
-  for (auto& kv : pl->map_cache)
-    if (kv.first == work) {
-      *out = kv.second;
-      return PSGD_OK;
-    }
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode && !pl->map_mat.empty()) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    PSGD_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
-    if (!fn || qr != cudaDriverEntryPointSuccess) return fail(PSGD_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
-  K3Maps* maps = new K3Maps();
-  std::memset(maps, 0, sizeof(K3Maps));
-  for (size_t i = 0; i < pl->map_mat.size(); ++i) {
-    const MatDev& md = pl->mats[pl->map_mat[i]];
-    const cuuint64_t dims[2] = {(cuuint64_t)md.m, (cuuint64_t)md.n};
-    const cuuint64_t strides[1] = {(cuuint64_t)md.m * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)pl->map_cols[i], (cuuint32_t)pl->map_rows[i]};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult cr = encode(&maps->map[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                         const_cast<float*>(work + md.flat_off), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) {
-      delete maps;
-      return fail(PSGD_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)cr) + ")");
-    }
-  }
-  if (pl->map_cache.size() >= 16) {  // bounded: callers use a handful of persistent buffers
-    delete pl->map_cache.front().second;
-    pl->map_cache.erase(pl->map_cache.begin());
-  }
-  pl->map_cache.emplace_back(work, maps);
-  *out = maps;
-  return PSGD_OK;
-}
-
-template <int RM>
-int run_k3(const psgd_plan* pl, float* work, const float* p, int divisor, const double* repl,
-           float* phat, float* qout, float* e, float* bias_out, int* status, cudaStream_t st) {
-  const int grid = (int)pl->k3_beg.size() - 1;
-  if (grid <= 0 || pl->k3.empty()) return PSGD_OK;
-  const K3Maps* maps = nullptr;
-  int rc = k3_maps_for(pl, work, &maps);
-  if (rc) return rc;
-  auto kern = k3_q_ef<RM>;
-  const size_t smem = pl->k3l.total;
-  PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  PSGD_CUDA_CHECK(launch_ex(kern, grid, kTmaThreads, smem, st, true, (const MatDev*)pl->d_mats,
-                            (const Slab3*)pl->d_k3, (const int*)pl->d_k3_beg, pl->k3l, *maps, work, p,
-                            divisor, repl, phat, qout, e, bias_out, (long long)pl->nbias,
-                            (long long)pl->p_bias_off, (long long)pl->flag_off, pl->nflags,
-                            pl->world == 1 ? 1 : 0, status));
-  return PSGD_OK;
-}
-
 template <int R, bool EXACT>
-struct RunK3Tall {
-  static int run(const psgd_plan* pl, const Group& gp, const float* work, const float* phat, float* qout,
+struct RunK3 {
+  static int run(const psgd_plan* pl, const Group& gp, float* work, const float* phat, float* qout, float* e,
                  const int* status, cudaStream_t st) {
     const int nitems = gp.end - gp.beg;
     if (nitems <= 0) return PSGD_OK;
-    auto kern = k3_tall<R, EXACT>;
+    auto kern = k3_slab<R, EXACT>;
     if (gp.smem > 48 * 1024)
       PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gp.smem));
-    kern<<<nitems, kThreads, gp.smem, st>>>(pl->d_mats, pl->d_k3t + gp.beg, work, phat, qout, pl->d_wsq,
-                                            pl->d_counters, status);
-    PSGD_CUDA_CHECK(cudaGetLastError());
+    PSGD_CUDA_CHECK(launch_ex(kern, nitems, kThreads, gp.smem, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
+                              (const SlabItem*)(pl->d_k3 + gp.beg), work, phat, qout, e, pl->d_wsq,
+                              pl->d_counters, pl->world == 1 ? 1 : 0, status));
     return PSGD_OK;
   }
 };
@@ -1698,17 +1449,20 @@ bool check_dev(const psgd_plan* pl) {
   return dev == pl->device;
 }
 
-int launch_k2(const psgd_plan* pl, bool tall_only, bool with_bias, const float* p, float* phat,
-              int divisor, const double* repl, float* bias_out, int* status, cudaStream_t st) {
-  const int nlist = tall_only ? (int)pl->tall_list.size() : pl->nmat;
+int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, int divisor,
+              const double* repl, float* bias_out, int* status, cudaStream_t st) {
+  const int nlist = pl->nmat;
   const int bias_blocks =
       (with_bias && pl->nbias > 0) ? (int)std::min<long long>(64, (pl->nbias + kGsThreads * 4 - 1) / (kGsThreads * 4)) : 0;
   const int grid = nlist + bias_blocks;
   if (grid == 0) return PSGD_OK;
-  k2_gs<<<grid, kGsThreads, 0, st>>>(pl->d_mats, tall_only ? pl->d_tall_list : pl->d_all_list, nlist, p,
-                                     phat, divisor, repl, pl->d_gsws, bias_out, pl->p_bias_off, pl->nbias,
-                                     pl->flag_off, pl->nflags, status);
-  PSGD_CUDA_CHECK(cudaGetLastError());
+  const size_t smem = (size_t)pl->k2_smem;
+  if (smem > 48 * 1024)
+    PSGD_CUDA_CHECK(cudaFuncSetAttribute(k2_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PSGD_CUDA_CHECK(launch_ex(k2_gs, grid, kGsThreads, smem, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
+                            (const int*)pl->d_all_list, nlist, p, phat, divisor, repl, pl->d_gsws, bias_out,
+                            (long long)pl->p_bias_off, (long long)pl->nbias, (long long)pl->flag_off, pl->nflags,
+                            status));
   return PSGD_OK;
 }
 
@@ -1736,7 +1490,7 @@ int psgd_orthogonalize(const psgd_plan* pl, const float* p, int32_t divisor, con
   if (!pl || !p || !p_hat || !status || divisor < 1 || (pl->nmat > 0 && !repl) ||
       (pl->nbias > 0 && !bias_out))
     return fail(PSGD_EINVAL, "psgd_orthogonalize: bad argument");
-  return launch_k2(pl, false, true, p, p_hat, divisor, repl, bias_out, (int*)status,
+  return launch_k2(pl, true, p, p_hat, divisor, repl, bias_out, (int*)status,
                    static_cast<cudaStream_t>(stream));
 }
 
@@ -1747,22 +1501,10 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
     return fail(PSGD_EINVAL, "psgd_q_ef: bad argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int rc = PSGD_OK;
-  const bool fused = !pl->k3.empty();
-  switch (pl->rmax) {
-    case 1: rc = run_k3<1>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
-    case 2: rc = run_k3<2>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
-    case 4: rc = run_k3<4>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
-    case 8: rc = run_k3<8>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
-    default: rc = run_k3<16>(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, (int*)status, st); break;
-  }
+  rc = launch_k2(pl, true, p, p_hat, divisor, repl, bias_out, (int*)status, st);  // K2: P-hat, bias mean
   if (rc) return rc;
-  if (pl->n_tall > 0 || (!fused && pl->nbias > 0)) {
-    rc = launch_k2(pl, true, !fused, p, p_hat, divisor, repl, bias_out, (int*)status, st);
-    if (rc) return rc;
-  }
-  for (const Group& gp : pl->g3t) {
-    rc = dispatch_r<RunK3Tall>(gp.r, pl, gp, (const float*)work, (const float*)p_hat, q_out,
-                               (const int*)status, st);
+  for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab
+    rc = dispatch_r<RunK3>(gp.r, pl, gp, work, (const float*)p_hat, q_out, e, (const int*)status, st);
     if (rc) return rc;
   }
   for (const Group& gp : pl->g4) {
