@@ -50,7 +50,7 @@ constexpr int kCons = 512;         // consumer threads of the TMA kernels (16 wa
 constexpr int kConsWarps = kCons / 32;
 constexpr int kTmaThreads = kCons + 32;  // + 1 producer warp
 constexpr int kRowItemElems = 4096;
-constexpr int kGsThreads = 512;
+constexpr int kGsThreads = 1024;
 constexpr int kFusedNMax = 512;    // K3 fused path holds all rows of a slab
 constexpr int K1_STAGES = 3;
 constexpr int K1_CHUNK = 4608;     // floats of g (and of e) per chunk
@@ -259,21 +259,25 @@ struct ConsumerReducer {  // the consumer threads of a TMA CTA, named barrier 1
 
 template <class Red>
 __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ repl, int tid, int nth,
-                            const Red& red, int* status) {
+                            const Red& red, int* status, int rs = -1, int cs = 1) {
+  // element (i, j) lives at x[i * rs + j * cs]; default row-major n x r
+  if (rs < 0) rs = r;
   for (int j = 0; j < r; ++j) {
+    double* xj = x + j * cs;
     double s = 0.0;
-    for (int i = tid; i < n; i += nth) s += x[i * r + j] * x[i * r + j];
+    for (int i = tid; i < n; i += nth) s += xj[i * rs] * xj[i * rs];
     double before = sqrt(red.sum(s));
     double nrm = before;
     if (j > 0) {
       for (int i2 = 0; i2 < j; ++i2) {
+        const double* xi = x + i2 * cs;
         s = 0.0;
-        for (int i = tid; i < n; i += nth) s += x[i * r + i2] * x[i * r + j];
+        for (int i = tid; i < n; i += nth) s += xi[i * rs] * xj[i * rs];
         const double c = red.sum(s);
-        for (int i = tid; i < n; i += nth) x[i * r + j] -= c * x[i * r + i2];
+        for (int i = tid; i < n; i += nth) xj[i * rs] -= c * xi[i * rs];
       }
       s = 0.0;
-      for (int i = tid; i < n; i += nth) s += x[i * r + j] * x[i * r + j];
+      for (int i = tid; i < n; i += nth) s += xj[i * rs] * xj[i * rs];
       nrm = sqrt(red.sum(s));
     }
     int attempt = 0;
@@ -282,21 +286,22 @@ __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ 
         if (tid == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
         break;
       }
-      for (int i = tid; i < n; i += nth) x[i * r + j] = repl[(long long)j * n + i];
+      for (int i = tid; i < n; i += nth) xj[i * rs] = repl[(long long)j * n + i];
       before = 1.0;
       for (int i2 = 0; i2 < j; ++i2) {
+        const double* xi = x + i2 * cs;
         s = 0.0;
-        for (int i = tid; i < n; i += nth) s += x[i * r + i2] * x[i * r + j];
+        for (int i = tid; i < n; i += nth) s += xi[i * rs] * xj[i * rs];
         const double c = red.sum(s);
-        for (int i = tid; i < n; i += nth) x[i * r + j] -= c * x[i * r + i2];
+        for (int i = tid; i < n; i += nth) xj[i * rs] -= c * xi[i * rs];
       }
       s = 0.0;
-      for (int i = tid; i < n; i += nth) s += x[i * r + j] * x[i * r + j];
+      for (int i = tid; i < n; i += nth) s += xj[i * rs] * xj[i * rs];
       nrm = sqrt(red.sum(s));
       ++attempt;
     }
     const double inv = 1.0 / nrm;  // one fp64 divide; the column scales by the reciprocal
-    for (int i = tid; i < n; i += nth) x[i * r + j] *= inv;
+    for (int i = tid; i < n; i += nth) xj[i * rs] *= inv;
   }
 }
 
@@ -379,7 +384,9 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
         const float4 gv = g4[c];
         const float4 ev = has_e ? e4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 d = make_float4(gv.x + ev.x, gv.y + ev.y, gv.z + ev.z, gv.w + ev.w);
+#ifndef PSGD_K1_NOSTORE
         st_hint(w4 + c, d, keep);
+#endif
         float qv[4][RM];
         k1_q4<RM, QS>(qrow + (long long)(4 * c) * r, qal, r, qv);
 #pragma unroll
@@ -415,7 +422,11 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
       }
     }
   }
+#ifdef PSGD_K1_NORED
+  if (false) {
+#else
   if (G > 32) {
+#endif
     bar_consumers();
     const int nw = G >> 5;
     for (int o = t; o < ch.nrows * r; o += kCons) {
@@ -639,13 +650,18 @@ __global__ void __launch_bounds__(kGsThreads)
   }
   const MatDev md = mats[list[blockIdx.x]];
   const int n = md.n, r = md.r;
-  double* __restrict__ x = (n * r <= K2_SMEM_DOUBLES) ? k2smem : ws + md.p_off;
+  // small: row-major in smem; tall: column-major in the global (L2-resident)
+  // workspace so every pass over a column is coalesced
+  const bool in_smem = n * r <= K2_SMEM_DOUBLES;
+  double* __restrict__ x = in_smem ? k2smem : ws + md.p_off;
+  const int rs = in_smem ? r : 1, cs = in_smem ? 1 : n;
   const double inv_div = 1.0 / (double)divisor;
   int bad = 0;
   for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
     const float v = P[md.p_off + idx];
     bad |= !finite1(v);
-    x[idx] = (double)v * inv_div;
+    const int i = idx / r, j = idx - i * r;
+    x[i * rs + j * cs] = (double)v * inv_div;
   }
   if (__syncthreads_or(bad)) {  // linalg.py:35-36 (ContractViolation)
     if (threadIdx.x == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
@@ -653,9 +669,175 @@ __global__ void __launch_bounds__(kGsThreads)
   }
   int par = 0;
   SyncReducer sr{red, &par};
-  mgs_inplace(x, n, r, repl + md.repl_off, threadIdx.x, blockDim.x, sr, status);
+  mgs_inplace(x, n, r, repl + md.repl_off, threadIdx.x, blockDim.x, sr, status, rs, cs);
   __syncthreads();  // rows were thread-owned above; the copy-out mapping differs
-  for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) Phat[md.p_off + idx] = (float)x[idx];
+  for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
+    const int i = idx / r, j = idx - i * r;
+    Phat[md.p_off + idx] = (float)x[i * rs + j * cs];
+  }
+}
+
+// ---- K2 for very tall matrices (n * r beyond the smem budget, e.g. the LSTM
+// encoder 28869 x 650): modified Gram-Schmidt carried out in Gram space.
+// Pass 1 (k2_gram, many CTAs): partial Gram matrices of [P / W, R] (R: the
+// attempt-0 replacement columns, linalg.py:54-58), reduced in block order by
+// the last-arriving CTA, whose warp 0 then runs the reference's MGS sequence
+// (linalg.py:61-90, same projections, same degeneracy test and replacement
+// rule) on coefficient vectors, producing T (2r x r) with P-hat = [P / W, R] T.
+// Pass 2 (k2_apply): P-hat rows.  Exactly dependent fp32 columns are resolved
+// to ~1e-8 relative here instead of ~1e-16 ("tall GS").
+
+struct GramItem {
+  int mat, row0, nrows, blk, nblk, gidx;
+  long long gbase;  // first partial slot of this matrix in the Gram workspace
+};
+
+constexpr int K2G_ROWS = 1024;
+constexpr int K2G_TILE = 64;
+
+__global__ void __launch_bounds__(256)
+    k2_gram(const MatDev* __restrict__ mats, const GramItem* __restrict__ items, const float* __restrict__ P,
+            int divisor, const double* __restrict__ repl, double* __restrict__ wsg, double* __restrict__ wsT,
+            int* __restrict__ counters, long long flag_off, int nflags, int* status) {
+  __shared__ double X[K2G_TILE][2 * PSGD_MAX_RANK + 1];
+  __shared__ double G[2 * PSGD_MAX_RANK][2 * PSGD_MAX_RANK];
+  __shared__ double cvec[2 * PSGD_MAX_RANK];
+  __shared__ double Tm[PSGD_MAX_RANK][2 * PSGD_MAX_RANK];
+  __shared__ int s_last;
+  pdl_wait();
+  {
+    int bad = 0;
+    for (int x = threadIdx.x; x < nflags; x += blockDim.x) bad |= P[flag_off + x] != 0.f;
+    if (__syncthreads_or(bad)) {
+      if (threadIdx.x == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+      return;
+    }
+  }
+  const GramItem it = items[blockIdx.x];
+  const MatDev md = mats[it.mat];
+  const int n = md.n, r = md.r, R2 = 2 * r;
+  const int npairs = R2 * (R2 + 1) / 2;
+  const double inv_div = 1.0 / (double)divisor;
+  const int t = threadIdx.x;
+  double acc[3] = {0.0, 0.0, 0.0};
+  int pk[3], pl[3];
+  for (int u = 0; u < 3; ++u) {  // pair index -> (k, l), k <= l
+    int p = t + 256 * u, k = 0;
+    pk[u] = pl[u] = -1;
+    if (p < npairs) {
+      while (p >= R2 - k) { p -= R2 - k; ++k; }
+      pk[u] = k;
+      pl[u] = k + p;
+    }
+  }
+  int bad = 0;
+  for (int r0 = it.row0; r0 < it.row0 + it.nrows; r0 += K2G_TILE) {
+    for (int idx = t; idx < K2G_TILE * R2; idx += 256) {
+      const int i = idx / R2, k = idx - i * R2, row = r0 + i;
+      double v = 0.0;
+      if (row < it.row0 + it.nrows) {
+        if (k < r) {
+          const float f = P[md.p_off + (long long)row * r + k];
+          bad |= !finite1(f);
+          v = (double)f * inv_div;
+        } else {
+          v = repl[md.repl_off + (long long)(k - r) * n + row];
+        }
+      }
+      X[i][k] = v;
+    }
+    __syncthreads();
+    for (int u = 0; u < 3; ++u)
+      if (pk[u] >= 0)
+        for (int i = 0; i < K2G_TILE; ++i) acc[u] += X[i][pk[u]] * X[i][pl[u]];
+    __syncthreads();
+  }
+  if (__syncthreads_or(bad)) {  // linalg.py:35-36
+    if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
+  }
+  for (int u = 0; u < 3; ++u)
+    if (pk[u] >= 0) wsg[it.gbase + (long long)it.blk * npairs + t + 256 * u] = acc[u];
+  __threadfence();
+  __syncthreads();
+  if (t == 0) s_last = atomicAdd(counters + it.gidx, 1) == it.nblk - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int p = t; p < npairs; p += 256) {  // fixed block order
+    double s = 0.0;
+    for (int b = 0; b < it.nblk; ++b) s += __ldcg(wsg + it.gbase + (long long)b * npairs + p);
+    int k = 0, q = p;
+    while (q >= R2 - k) { q -= R2 - k; ++k; }
+    G[k][k + q] = s;
+    G[k + q][k] = s;
+  }
+  if (t == 0) counters[it.gidx] = 0;
+  __syncthreads();
+  if (t >= 32) return;
+  // ---- MGS on coefficient vectors: value(c) = [P/W, R] c ; <a, b> = a^T G b
+  const int lane = t;
+  auto gdot = [&](const double* a, const double* b) {  // warp-parallel a^T G b
+    double s = 0.0;
+    if (lane < R2) {
+      double gb = 0.0;
+      for (int l = 0; l < R2; ++l) gb += G[lane][l] * b[l];
+      s = a[lane] * gb;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    return s;
+  };
+  for (int j = 0; j < r; ++j) {
+    if (lane < R2) cvec[lane] = lane == j ? 1.0 : 0.0;
+    __syncwarp();
+    double before = sqrt(fmax(gdot(cvec, cvec), 0.0));
+    double nrm = before;
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) {  // degenerate: the seeded replacement column, before := 1
+        if (lane < R2) cvec[lane] = lane == r + j ? 1.0 : 0.0;
+        __syncwarp();
+        before = 1.0;
+      }
+      for (int i2 = 0; i2 < j; ++i2) {
+        const double c = gdot(Tm[i2], cvec);
+        __syncwarp();
+        if (lane < R2) cvec[lane] -= c * Tm[i2][lane];
+        __syncwarp();
+      }
+      if (j > 0 || pass == 1) nrm = sqrt(fmax(gdot(cvec, cvec), 0.0));
+      if (!(nrm < 1e-12 * (before + 1.0))) break;
+      if (pass == 1 && lane == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
+    }
+    const double inv = 1.0 / nrm;
+    if (lane < R2) Tm[j][lane] = cvec[lane] * inv;
+    __syncwarp();
+  }
+  for (int x = lane; x < R2 * r; x += 32) wsT[(long long)it.gidx * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK + x] =
+      Tm[x % r][x / r];  // row-major [k][j]
+}
+
+__global__ void __launch_bounds__(256)
+    k2_apply(const MatDev* __restrict__ mats, const int* __restrict__ gram_list, const int* __restrict__ blk_mat,
+             const int* __restrict__ blk_row0, const float* __restrict__ P, int divisor,
+             const double* __restrict__ repl, const double* __restrict__ wsT, float* __restrict__ Phat,
+             const int* status) {
+  pdl_wait();
+  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
+  const int gidx = blk_mat[blockIdx.x];
+  const MatDev md = mats[gram_list[gidx]];
+  const int n = md.n, r = md.r;
+  const int i = blk_row0[blockIdx.x] + threadIdx.x;
+  if (i >= n) return;
+  const double* T = wsT + (long long)gidx * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK;
+  const double inv_div = 1.0 / (double)divisor;
+  double x[2 * PSGD_MAX_RANK];
+  for (int k = 0; k < r; ++k) x[k] = (double)P[md.p_off + (long long)i * r + k] * inv_div;
+  for (int k = 0; k < r; ++k) x[r + k] = repl[md.repl_off + (long long)k * n + i];
+  for (int j = 0; j < r; ++j) {
+    double s = 0.0;
+    for (int k = 0; k < 2 * r; ++k) s += x[k] * T[k * r + j];
+    Phat[md.p_off + (long long)i * r + j] = (float)s;
+  }
 }
 
 // ============================================================================= K3
@@ -996,6 +1178,10 @@ struct psgd_plan {
   long long psplit_elems = 0;
   // K3 fused
   int k2_smem = 0;
+  std::vector<int> small_list, gram_list;   // K2 in smem / in Gram space
+  std::vector<GramItem> gram_items;
+  std::vector<int> apply_mat, apply_row0;   // k2_apply blocks
+  long long wsg_elems = 0;
   std::vector<SlabItem> k3;          // fused and tall slabs, grouped by r
   std::vector<Group> g3;
 
@@ -1014,7 +1200,11 @@ struct psgd_plan {
   float* d_psplit = nullptr;
   int* d_split_cnt = nullptr;
   SlabItem* d_k3 = nullptr;
-  int *d_tall_list = nullptr, *d_all_list = nullptr;
+  int *d_tall_list = nullptr, *d_all_list = nullptr, *d_small_list = nullptr, *d_gram_list = nullptr;
+  GramItem* d_gram_items = nullptr;
+  int *d_apply_mat = nullptr, *d_apply_row0 = nullptr;
+  double *d_wsg = nullptr, *d_wsT = nullptr;
+  int* d_gram_cnt = nullptr;
   RowItem *d_k4 = nullptr, *d_k5 = nullptr;
   double* d_gsws = nullptr;
   float* d_wsq = nullptr;
@@ -1214,8 +1404,26 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->q_elems = std::max(4LL, qo);
   pl->repl_elems = std::max(1LL, ro);
 
-  for (auto& md : pl->mats)
-    if ((long long)md.n * md.r <= K2_SMEM_DOUBLES) pl->k2_smem = std::max(pl->k2_smem, md.n * md.r * 8);
+  for (int mi = 0; mi < nmat; ++mi) {
+    const MatDev& md = pl->mats[mi];
+    if ((long long)md.n * md.r <= K2_SMEM_DOUBLES) {
+      pl->k2_smem = std::max(pl->k2_smem, md.n * md.r * 8);
+      pl->small_list.push_back(mi);
+    } else {
+      const int gidx = (int)pl->gram_list.size();
+      pl->gram_list.push_back(mi);
+      const int nblk = (md.n + K2G_ROWS - 1) / K2G_ROWS;
+      const int npairs = (2 * md.r) * (2 * md.r + 1) / 2;
+      for (int b2 = 0; b2 < nblk; ++b2)
+        pl->gram_items.push_back({mi, b2 * K2G_ROWS, std::min(K2G_ROWS, md.n - b2 * K2G_ROWS), b2, nblk, gidx,
+                                  pl->wsg_elems});
+      pl->wsg_elems += (long long)nblk * npairs;
+      for (int r0 = 0; r0 < md.n; r0 += 256) {
+        pl->apply_mat.push_back(gidx);
+        pl->apply_row0.push_back(r0);
+      }
+    }
+  }
   // ---- K3 slabs, grouped by r (one launch per group): fused slabs hold all rows
   {
     std::vector<int> rs;
@@ -1267,6 +1475,14 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_k3 = take(pl->k3.size() * sizeof(SlabItem));
   const size_t o_tl = take(pl->tall_list.size() * sizeof(int));
   const size_t o_al = take(pl->all_list.size() * sizeof(int));
+  const size_t o_sl = take(pl->small_list.size() * sizeof(int));
+  const size_t o_gl = take(pl->gram_list.size() * sizeof(int));
+  const size_t o_gi = take(pl->gram_items.size() * sizeof(GramItem));
+  const size_t o_am = take(pl->apply_mat.size() * sizeof(int));
+  const size_t o_ar = take(pl->apply_row0.size() * sizeof(int));
+  const size_t o_wg = take((size_t)std::max(1LL, pl->wsg_elems) * sizeof(double));
+  const size_t o_wt = take(std::max<size_t>(1, pl->gram_list.size()) * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK * sizeof(double));
+  const size_t o_gc = take(std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
   const size_t o_k4 = take(pl->k4.size() * sizeof(RowItem));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
@@ -1287,6 +1503,14 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_k3 = reinterpret_cast<SlabItem*>(b + o_k3);
   pl->d_tall_list = reinterpret_cast<int*>(b + o_tl);
   pl->d_all_list = reinterpret_cast<int*>(b + o_al);
+  pl->d_small_list = reinterpret_cast<int*>(b + o_sl);
+  pl->d_gram_list = reinterpret_cast<int*>(b + o_gl);
+  pl->d_gram_items = reinterpret_cast<GramItem*>(b + o_gi);
+  pl->d_apply_mat = reinterpret_cast<int*>(b + o_am);
+  pl->d_apply_row0 = reinterpret_cast<int*>(b + o_ar);
+  pl->d_wsg = reinterpret_cast<double*>(b + o_wg);
+  pl->d_wsT = reinterpret_cast<double*>(b + o_wt);
+  pl->d_gram_cnt = reinterpret_cast<int*>(b + o_gc);
   pl->d_k4 = reinterpret_cast<RowItem*>(b + o_k4);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
@@ -1302,6 +1526,12 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_k3, pl->k3.data(), pl->k3.size() * sizeof(SlabItem));
   if (ce == cudaSuccess) ce = up(pl->d_tall_list, pl->tall_list.data(), pl->tall_list.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_all_list, pl->all_list.data(), pl->all_list.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_small_list, pl->small_list.data(), pl->small_list.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_gram_list, pl->gram_list.data(), pl->gram_list.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_gram_items, pl->gram_items.data(), pl->gram_items.size() * sizeof(GramItem));
+  if (ce == cudaSuccess) ce = up(pl->d_apply_mat, pl->apply_mat.data(), pl->apply_mat.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_apply_row0, pl->apply_row0.data(), pl->apply_row0.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = cudaMemset(pl->d_gram_cnt, 0, std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
@@ -1344,7 +1574,9 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   const bool any_fused = pl->n_tall < pl->nmat;
   o->launches_ef_p = (pl->k1.empty() && pl->nbias == 0) ? 0 : 1;
   o->launches_orthogonalize = (pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0;
-  o->launches_q_ef = ((pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0) + nonempty(pl->g3) + nonempty(pl->g4);
+  o->launches_orthogonalize = ((pl->small_list.size() + (pl->nbias > 0)) > 0 ? 1 : 0) +
+                              (pl->gram_items.empty() ? 0 : 2);
+  o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4);
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
   return PSGD_OK;
@@ -1451,18 +1683,28 @@ bool check_dev(const psgd_plan* pl) {
 
 int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, int divisor,
               const double* repl, float* bias_out, int* status, cudaStream_t st) {
-  const int nlist = pl->nmat;
+  const int nlist = (int)pl->small_list.size();
   const int bias_blocks =
       (with_bias && pl->nbias > 0) ? (int)std::min<long long>(64, (pl->nbias + kGsThreads * 4 - 1) / (kGsThreads * 4)) : 0;
   const int grid = nlist + bias_blocks;
-  if (grid == 0) return PSGD_OK;
-  const size_t smem = (size_t)pl->k2_smem;
-  if (smem > 48 * 1024)
-    PSGD_CUDA_CHECK(cudaFuncSetAttribute(k2_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  PSGD_CUDA_CHECK(launch_ex(k2_gs, grid, kGsThreads, smem, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
-                            (const int*)pl->d_all_list, nlist, p, phat, divisor, repl, pl->d_gsws, bias_out,
-                            (long long)pl->p_bias_off, (long long)pl->nbias, (long long)pl->flag_off, pl->nflags,
-                            status));
+  if (grid > 0) {
+    const size_t smem = (size_t)pl->k2_smem;
+    if (smem > 48 * 1024)
+      PSGD_CUDA_CHECK(cudaFuncSetAttribute(k2_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PSGD_CUDA_CHECK(launch_ex(k2_gs, grid, kGsThreads, smem, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
+                              (const int*)pl->d_small_list, nlist, p, phat, divisor, repl, pl->d_gsws, bias_out,
+                              (long long)pl->p_bias_off, (long long)pl->nbias, (long long)pl->flag_off,
+                              pl->nflags, status));
+  }
+  if (!pl->gram_items.empty()) {
+    PSGD_CUDA_CHECK(launch_ex(k2_gram, (int)pl->gram_items.size(), 256, 0, st, false, (const MatDev*)pl->d_mats,
+                              (const GramItem*)pl->d_gram_items, p, divisor, repl, pl->d_wsg, pl->d_wsT,
+                              pl->d_gram_cnt, (long long)pl->flag_off, pl->nflags, status));
+    PSGD_CUDA_CHECK(launch_ex(k2_apply, (int)pl->apply_mat.size(), 256, 0, st, false, (const MatDev*)pl->d_mats,
+                              (const int*)pl->d_gram_list, (const int*)pl->d_apply_mat,
+                              (const int*)pl->d_apply_row0, p, divisor, repl, (const double*)pl->d_wsT, phat,
+                              (const int*)status));
+  }
   return PSGD_OK;
 }
 

@@ -149,8 +149,8 @@ __global__ void copy_stream(const float4* src, float4* dst, long long n4) {
     dst[i] = __ldcs(src + i);
 }
 
-int main() {
-  const long long total = 1LL << 30;  // 1 GiB read
+int main(int argc, char** argv) {
+  const long long total = argc > 1 ? atoll(argv[1]) : (1LL << 30);  // bytes read
   char* src; float* sink; char* dst; char* flush;
   cudaMalloc(&src, total); cudaMalloc(&dst, total); cudaMalloc(&sink, 64); cudaMalloc(&flush, 256 << 20);
   cudaMemset(src, 1, total);
@@ -174,7 +174,7 @@ int main() {
     float ms = timeit([&] { copy_stream<<<nsm * 8, 256>>>((const float4*)src, (float4*)dst, total / 16); });
     printf("LDG/STG copy (r+w)          : %.1f GB/s\n", 2.0 * total / ms / 1e6);
   }
-  for (int cb : {4096, 8192, 16384, 32768}) for (int st : {2, 4, 8}) for (int ctas : {1, 2}) {
+  for (int cb : {16384, 18432, 36864}) for (int st : {2, 3, 4, 6}) for (int ctas : {1, 2}) {
     size_t smem = (size_t)st * cb + 2 * st * 8;
     if (smem * ctas > 220 * 1024) continue;
     cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

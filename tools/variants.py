@@ -28,6 +28,8 @@ for path in sys.argv[1:]:
         ev[0].record()
         _lib.check(lib.psgd_ef_p(h, ptr(eng.g[0]), ptr(eng.e[0]), ptr(eng.work[0]), ptr(eng.Q), ptr(eng.P[0]),
                                  ptr(eng.bias_g[0]), ptr(eng.status), sp), "ef_p")
+        if os.environ.get("MIDFLUSH"):
+            flush.zero_()
         ev[1].record()
         _lib.check(lib.psgd_q_ef(h, ptr(eng.work[0]), ptr(eng.P[0]), 1, ptr(eng.repl), ptr(eng.Phat), ptr(eng.Q),
                                  ptr(eng.e[0]), ptr(eng.bias_out), ptr(eng.status), sp), "q_ef")
