@@ -40,7 +40,7 @@ extern "C" {
 #define PSGD_ECUDA    -2   /* CUDA launch / allocation error -> RuntimeError */
 #define PSGD_ENOMEM   -3
 
-/* device status word bits (int32, caller-owned; zero it before each step) */
+/* device status word bits (int32, caller-owned; psgd_ef_p resets it each step) */
 #define PSGD_STATUS_NONFINITE_GRAD  1  /* optimizer.py:72-76 NonFiniteGradient */
 #define PSGD_STATUS_NONFINITE_P     2  /* linalg.py:35-36 via orthogonalize(as_matrix) */
 #define PSGD_STATUS_REPLACEMENT     4  /* linalg.py:82-88 needed a 2nd replacement draw */
@@ -93,8 +93,9 @@ int psgd_plan_matrix(const psgd_plan* plan, int32_t i, psgd_matrix_info* out);
  * (P_w = delta Q) and the bias pack for optimizer.py:111-113.
  * g, e: flat_elems (e may be NULL: error feedback off, optimizer.py:118-119).
  * work: out delta.  q: warm-start Q (q_elems).  p: out P (p_elems; the bias
- * tail receives bias_g).  status: OR-ed with PSGD_STATUS_NONFINITE_GRAD; the caller
- * zeroes it once per step (psgd_step_single does).  */
+ * tail receives bias_g, the flag tail one non-finite flag per CTA, so the P
+ * all-reduce carries them to every worker).  status: reset to 0 (the next
+ * kernels raise PSGD_STATUS_* from the flags).  */
 int psgd_ef_p(const psgd_plan* plan, const float* g, const float* e, float* work,
               const float* q, float* p, const float* bias_g, int32_t* status, void* stream);
 
@@ -127,7 +128,7 @@ int psgd_decompress(const psgd_plan* plan, const float* p_hat, const float* q_su
                     int32_t divisor, float* q_store, float* mhat, const int32_t* status,
                     void* stream);
 
-/* One W == 1 step: zero status, psgd_ef_p, psgd_q_ef (2 kernel launches). */
+/* One W == 1 step: psgd_ef_p + psgd_q_ef. */
 int psgd_step_single(const psgd_plan* plan, const float* g, float* e, float* work, float* q,
                      float* p, float* p_hat, const float* bias_g, const double* repl,
                      float* bias_out, int32_t* status, void* stream);

@@ -166,6 +166,9 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 #ifndef PSGD_PDL
 #define PSGD_PDL 1
 #endif
+#ifndef PSGD_K3_OWNER_GS
+#define PSGD_K3_OWNER_GS 0  // 1: fused matrices orthogonalised inside K3 (measured slower)
+#endif
 __device__ __forceinline__ void st_hint(float4* p, float4 v, uint64_t pol) {
 #if !PSGD_STORE_HINT
   *p = v;
@@ -185,6 +188,14 @@ __device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
 __device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
@@ -257,6 +268,31 @@ struct ConsumerReducer {  // the consumer threads of a TMA CTA, named barrier 1
   }
 };
 
+// strided column helpers: 4 independent accumulators / loads in flight, so
+// the loops are throughput- rather than latency-bound
+__device__ __forceinline__ double col_dot(const double* a, const double* b, int n, int rs, int tid, int nth) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int i = tid;
+  for (; i + 3 * nth < n; i += 4 * nth) {
+    const double a0 = a[i * rs], a1 = a[(i + nth) * rs], a2 = a[(i + 2 * nth) * rs], a3 = a[(i + 3 * nth) * rs];
+    const double b0 = b[i * rs], b1 = b[(i + nth) * rs], b2 = b[(i + 2 * nth) * rs], b3 = b[(i + 3 * nth) * rs];
+    s0 = fma(a0, b0, s0);
+    s1 = fma(a1, b1, s1);
+    s2 = fma(a2, b2, s2);
+    s3 = fma(a3, b3, s3);
+  }
+  for (; i < n; i += nth) s0 = fma(a[i * rs], b[i * rs], s0);
+  return (s0 + s1) + (s2 + s3);
+}
+__device__ __forceinline__ void col_axpy(double* y, double c, const double* x, int n, int rs, int tid, int nth) {
+#pragma unroll 4
+  for (int i = tid; i < n; i += nth) y[i * rs] -= c * x[i * rs];
+}
+__device__ __forceinline__ void col_scale(double* y, double c, int n, int rs, int tid, int nth) {
+#pragma unroll 4
+  for (int i = tid; i < n; i += nth) y[i * rs] *= c;
+}
+
 template <class Red>
 __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ repl, int tid, int nth,
                             const Red& red, int* status, int rs = -1, int cs = 1) {
@@ -264,21 +300,15 @@ __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ 
   if (rs < 0) rs = r;
   for (int j = 0; j < r; ++j) {
     double* xj = x + j * cs;
-    double s = 0.0;
-    for (int i = tid; i < n; i += nth) s += xj[i * rs] * xj[i * rs];
-    double before = sqrt(red.sum(s));
+    double before = sqrt(red.sum(col_dot(xj, xj, n, rs, tid, nth)));
     double nrm = before;
     if (j > 0) {
       for (int i2 = 0; i2 < j; ++i2) {
         const double* xi = x + i2 * cs;
-        s = 0.0;
-        for (int i = tid; i < n; i += nth) s += xi[i * rs] * xj[i * rs];
-        const double c = red.sum(s);
-        for (int i = tid; i < n; i += nth) xj[i * rs] -= c * xi[i * rs];
+        const double c = red.sum(col_dot(xi, xj, n, rs, tid, nth));
+        col_axpy(xj, c, xi, n, rs, tid, nth);
       }
-      s = 0.0;
-      for (int i = tid; i < n; i += nth) s += xj[i * rs] * xj[i * rs];
-      nrm = sqrt(red.sum(s));
+      nrm = sqrt(red.sum(col_dot(xj, xj, n, rs, tid, nth)));
     }
     int attempt = 0;
     while (nrm < 1e-12 * (before + 1.0)) {
@@ -290,18 +320,13 @@ __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ 
       before = 1.0;
       for (int i2 = 0; i2 < j; ++i2) {
         const double* xi = x + i2 * cs;
-        s = 0.0;
-        for (int i = tid; i < n; i += nth) s += xi[i * rs] * xj[i * rs];
-        const double c = red.sum(s);
-        for (int i = tid; i < n; i += nth) xj[i * rs] -= c * xi[i * rs];
+        const double c = red.sum(col_dot(xi, xj, n, rs, tid, nth));
+        col_axpy(xj, c, xi, n, rs, tid, nth);
       }
-      s = 0.0;
-      for (int i = tid; i < n; i += nth) s += xj[i * rs] * xj[i * rs];
-      nrm = sqrt(red.sum(s));
+      nrm = sqrt(red.sum(col_dot(xj, xj, n, rs, tid, nth)));
       ++attempt;
     }
-    const double inv = 1.0 / nrm;  // one fp64 divide; the column scales by the reciprocal
-    for (int i = tid; i < n; i += nth) xj[i * rs] *= inv;
+    col_scale(xj, 1.0 / nrm, n, rs, tid, nth);  // one fp64 divide; scale by the reciprocal
   }
 }
 
@@ -492,6 +517,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
     *sflag = 0;
     fence_mbar_init();
+    if (blockIdx.x == 0) *status = 0;  // the step's status word: nothing else writes it during K1
   }
   __syncthreads();
 #if PSGD_PDL
@@ -589,7 +615,120 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   bar_consumers();
   if (t == 0) {
     P[flag_off + blockIdx.x] = *sflag ? 1.f : 0.f;  // carried to every rank by the P all-reduce
-    if (*sflag) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+    // (status is raised from these flags by K2 / K3, after every K1 CTA is done)
+  }
+}
+
+struct WarpReducer {  // one warp, shuffles only
+  __device__ double sum(double v) const {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  }
+};
+
+// ---- register-resident warp MGS (n <= 32 * RPL, r == R <= 4): each lane
+// owns rows lane + 32 k; dot products are RPL fused multiply-adds plus one
+// shuffle reduction, so the whole orthogonalisation of a 512 x 2 P is ~1 us.
+// Same sequence, threshold and replacement rule as mgs_inplace (linalg.py:61-90).
+template <int RPL, int R>
+__device__ __forceinline__ void warp_mgs_reg(const float* __restrict__ P, int n, double inv_div,
+                                             const double* __restrict__ repl, float* __restrict__ out,
+                                             int* status) {
+  const int lane = threadIdx.x & 31;
+  double x[R][RPL];
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int i = lane + 32 * k;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const float v = i < n ? P[i * R + j] : 0.f;
+      bad |= !finite1(v);
+      x[j][k] = (double)v * inv_div;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) {  // linalg.py:35-36 (ContractViolation)
+    if (lane == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
+    return;
+  }
+  auto wsum = [](double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  };
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
+    double before = sqrt(wsum(s));
+    double nrm = before;
+    for (int attempt = 0;; ++attempt) {
+      if (attempt == 1 || j > 0) {
+#pragma unroll
+        for (int i2 = 0; i2 < j; ++i2) {
+          double d = 0.0;
+#pragma unroll
+          for (int k = 0; k < RPL; ++k) d = fma(x[i2][k], x[j][k], d);
+          const double c = wsum(d);
+#pragma unroll
+          for (int k = 0; k < RPL; ++k) x[j][k] -= c * x[i2][k];
+        }
+        s = 0.0;
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
+        nrm = sqrt(wsum(s));
+      }
+      if (!(nrm < 1e-12 * (before + 1.0))) break;
+      if (attempt == 1) {  // the table holds attempt 0 only
+        if (lane == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
+        break;
+      }
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        const int i = lane + 32 * k;
+        x[j][k] = i < n ? repl[(long long)j * n + i] : 0.0;
+      }
+      before = 1.0;
+    }
+    const double inv = 1.0 / nrm;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) x[j][k] *= inv;
+  }
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int i = lane + 32 * k;
+    if (i < n)
+#pragma unroll
+      for (int j = 0; j < R; ++j) out[i * R + j] = (float)x[j][k];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ bool warp_mgs_dispatch_r(int rpl_log2, const float* P, int n, double inv_div,
+                                                    const double* repl, float* out, int* status) {
+  switch (rpl_log2) {
+    case 0: warp_mgs_reg<1, R>(P, n, inv_div, repl, out, status); return true;
+    case 1: warp_mgs_reg<2, R>(P, n, inv_div, repl, out, status); return true;
+    case 2: warp_mgs_reg<4, R>(P, n, inv_div, repl, out, status); return true;
+    case 3: warp_mgs_reg<8, R>(P, n, inv_div, repl, out, status); return true;
+    case 4: warp_mgs_reg<16, R>(P, n, inv_div, repl, out, status); return true;
+    default: return false;
+  }
+}
+
+// P-hat of one matrix by one warp when n <= 512 and r <= 4; false otherwise
+__device__ __forceinline__ bool warp_mgs(const float* P, int n, int r, double inv_div, const double* repl,
+                                         float* out, int* status) {
+  if (n > 512 || r > 4) return false;
+  int l = 0;
+  while ((32 << l) < n) ++l;
+  switch (r) {
+    case 1: return warp_mgs_dispatch_r<1>(l, P, n, inv_div, repl, out, status);
+    case 2: return warp_mgs_dispatch_r<2>(l, P, n, inv_div, repl, out, status);
+    case 3: return warp_mgs_dispatch_r<3>(l, P, n, inv_div, repl, out, status);
+    default: return warp_mgs_dispatch_r<4>(l, P, n, inv_div, repl, out, status);
   }
 }
 
@@ -617,12 +756,17 @@ struct SyncReducer {  // all threads of the CTA, one __syncthreads per reduction
   }
 };
 
-constexpr int K2_SMEM_DOUBLES = 12288;  // 96 KB: n * r up to this stays in smem
+constexpr int K2_SMEM_DOUBLES = 12288;  // 96 KB: n * r up to this stays in smem (CTA item)
+constexpr int K2_WARP_DOUBLES = 2048;   // n * r up to this: one warp per matrix (no barriers)
+constexpr int K2_THREADS = 256;
 
-__global__ void __launch_bounds__(kGsThreads)
-    k2_gs(const MatDev* __restrict__ mats, const int* __restrict__ list, int nlist,
-          const float* __restrict__ P, float* __restrict__ Phat, int divisor,
-          const double* __restrict__ repl, double* __restrict__ ws, float* __restrict__ bias_out,
+// items: [warp blocks | CTA blocks | bias blocks].  A warp block orthogonalises
+// up to 8 small matrices, one per warp, reductions by shuffles only; a CTA
+// block one medium matrix with 8 warps and a __syncthreads per reduction.
+__global__ void __launch_bounds__(K2_THREADS)
+    k2_gs(const MatDev* __restrict__ mats, const int* __restrict__ wlist, int nw_items, int nwblocks,
+          const int* __restrict__ clist, int nc_items, int wregion, const float* __restrict__ P,
+          float* __restrict__ Phat, int divisor, const double* __restrict__ repl, float* __restrict__ bias_out,
           long long bias_off, long long nbias, long long flag_off, int nflags, int* status) {
   extern __shared__ __align__(16) double k2smem[];
   __shared__ double red[64];
@@ -636,10 +780,12 @@ __global__ void __launch_bounds__(kGsThreads)
       return;
     }
   }
-  if ((int)blockIdx.x >= nlist) {  // bias mean: P tail / W
-    const long long nb = gridDim.x - nlist;
+  const int b = blockIdx.x;
+  const double inv_div = 1.0 / (double)divisor;
+  if (b >= nwblocks + nc_items) {  // bias mean: P tail / W
+    const long long nb = gridDim.x - nwblocks - nc_items;
     bool bad = false;
-    for (long long x = (blockIdx.x - nlist) * (long long)blockDim.x + threadIdx.x; x < nbias;
+    for (long long x = (b - nwblocks - nc_items) * (long long)blockDim.x + threadIdx.x; x < nbias;
          x += nb * blockDim.x) {
       const float v = P[bias_off + x];
       bad |= !finite1(v);
@@ -648,20 +794,45 @@ __global__ void __launch_bounds__(kGsThreads)
     if (bad) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
     return;
   }
-  const MatDev md = mats[list[blockIdx.x]];
+  if (b < nwblocks) {  // ---- one warp per small matrix
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int item = b * (K2_THREADS / 32) + warp;
+    if (item >= nw_items) return;
+    const MatDev md = mats[wlist[item]];
+    const int n = md.n, r = md.r;
+    if (warp_mgs(P + md.p_off, n, r, inv_div, repl + md.repl_off, Phat + md.p_off, status)) return;
+    double* x = k2smem + warp * wregion;  // column-major: lanes hit consecutive banks
+    int bad = 0;
+#pragma unroll 8
+    for (int idx = lane; idx < n * r; idx += 32) {  // (loads independent of the smem stores)
+      const float v = P[md.p_off + idx];
+      bad |= !finite1(v);
+      const int i = idx / r, j = idx - i * r;
+      x[j * n + i] = (double)v * inv_div;
+    }
+    if (__any_sync(0xffffffffu, bad)) {  // linalg.py:35-36 (ContractViolation)
+      if (lane == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
+      return;
+    }
+    __syncwarp();
+    mgs_inplace(x, n, r, repl + md.repl_off, lane, 32, WarpReducer{}, status, 1, n);
+    __syncwarp();
+    for (int idx = lane; idx < n * r; idx += 32) {
+      const int i = idx / r, j = idx - i * r;
+      Phat[md.p_off + idx] = (float)x[j * n + i];
+    }
+    return;
+  }
+  // ---- one CTA per medium matrix
+  const MatDev md = mats[clist[b - nwblocks]];
   const int n = md.n, r = md.r;
-  // small: row-major in smem; tall: column-major in the global (L2-resident)
-  // workspace so every pass over a column is coalesced
-  const bool in_smem = n * r <= K2_SMEM_DOUBLES;
-  double* __restrict__ x = in_smem ? k2smem : ws + md.p_off;
-  const int rs = in_smem ? r : 1, cs = in_smem ? 1 : n;
-  const double inv_div = 1.0 / (double)divisor;
+  double* x = k2smem;  // column-major
   int bad = 0;
   for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
     const float v = P[md.p_off + idx];
     bad |= !finite1(v);
     const int i = idx / r, j = idx - i * r;
-    x[i * rs + j * cs] = (double)v * inv_div;
+    x[j * n + i] = (double)v * inv_div;
   }
   if (__syncthreads_or(bad)) {  // linalg.py:35-36 (ContractViolation)
     if (threadIdx.x == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
@@ -669,11 +840,11 @@ __global__ void __launch_bounds__(kGsThreads)
   }
   int par = 0;
   SyncReducer sr{red, &par};
-  mgs_inplace(x, n, r, repl + md.repl_off, threadIdx.x, blockDim.x, sr, status, rs, cs);
+  mgs_inplace(x, n, r, repl + md.repl_off, threadIdx.x, blockDim.x, sr, status, 1, n);
   __syncthreads();  // rows were thread-owned above; the copy-out mapping differs
   for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
     const int i = idx / r, j = idx - i * r;
-    Phat[md.p_off + idx] = (float)x[i * rs + j * cs];
+    Phat[md.p_off + idx] = (float)x[j * n + i];
   }
 }
 
@@ -843,7 +1014,8 @@ __global__ void __launch_bounds__(256)
 // ============================================================================= K3
 // One CTA per column slab (all n rows x C cols of one matrix, or a chunk of
 // rows for tall matrices), the slab held in registers: every load is issued
-// up front (64 KB in flight per CTA), then the CTA waits (PDL) for K2's P-hat.
+// up front (64 KB in flight per CTA).  Fused matrices are orthogonalised by
+// their first slab's CTA (the others wait on a flag); tall ones by K2.
 //   fused (n <= rows per CTA): q_w = delta^T P-hat, e = delta - P-hat q_w^T and
 //     M-hat at W = 1 from the same registers: delta is read once
 //     (compressors.py:339,375-378, optimizer.py:124-127).
@@ -854,11 +1026,14 @@ __global__ void __launch_bounds__(256)
 template <int R, bool EXACT>
 __global__ void __launch_bounds__(kThreads, 2)
     k3_slab(const MatDev* __restrict__ mats, const SlabItem* __restrict__ items, float* __restrict__ work,
-            const float* __restrict__ Phat, float* __restrict__ qout, float* __restrict__ e,
-            float* __restrict__ wsq, int* __restrict__ counters, int write_mhat, const int* status) {
+            const float* __restrict__ P, int divisor, const double* __restrict__ repl, float* __restrict__ Phat,
+            float* __restrict__ qout, float* __restrict__ e, float* __restrict__ wsq, int* __restrict__ counters,
+            int* __restrict__ gs_flag, int* __restrict__ gs_done, float* __restrict__ bias_out, long long nbias,
+            long long bias_off, long long flag_off, int nflags, int write_mhat, int* status) {
   constexpr int DCAP = k3_dcap(R);
   extern __shared__ __align__(16) unsigned char k3smem[];
   __shared__ int s_flag;
+  __shared__ double sred[64];
   const SlabItem it = items[blockIdx.x];
   const int t = threadIdx.x;
   const bool fused = it.nchunks == 1;
@@ -879,12 +1054,25 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int rbeg = it.chunk * rows_chunk;
   const int nrows = min(n - rbeg, rows_chunk);
   const int ncols = min(C, m - it.c0);
-  float* ps = reinterpret_cast<float*>(k3smem);  // nrows x r
-  float* red = ps + rows_chunk * r;              // RG x C x r
-  float* qs = red + RG * C * r;                  // C x r
+  double* gsd = reinterpret_cast<double*>(k3smem);                  // fused owner: n x r float64
+  float* ps = reinterpret_cast<float*>(gsd + (fused && PSGD_K3_OWNER_GS ? n * r : 0));  // nrows x r
+  float* red = ps + rows_chunk * r;                                   // RG x C x r
+  float* qs = red + RG * C * r;                                       // C x r
 
-  // 1. every load of the slab in flight at once (delta is final: K2 started
-  //    after K1 completed, and this grid starts after K2's trigger)
+#if PSGD_K3_OWNER_GS
+  pdl_wait();  // K3 follows K1 directly: delta / P must be complete before any load
+  if (fused) {  // a non-finite gradient on any worker (flags ride in P): mutate nothing
+    int bad = 0;
+    for (int x = t; x < nflags; x += kThreads) bad |= P[flag_off + x] != 0.f;
+    if (__syncthreads_or(bad)) {
+      if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+      return;
+    }
+  } else if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) {
+    return;
+  }
+#endif
+  // 1. every load of the slab in flight at once
   float d[DCAP];
   const long long base = md.flat_off + (long long)rbeg * m + col;
   if (vec == 4) {
@@ -902,10 +1090,88 @@ __global__ void __launch_bounds__(kThreads, 2)
       d[s] = (colok && li < nrows) ? __ldcs(work + base + (long long)li * m) : 0.f;
     }
   }
-  // 2. P-hat of the rows, from K2 (wait for it; nothing is mutated on failure)
+#if !PSGD_K3_OWNER_GS
+  // K3 follows K2, which started only after K1 completed: delta was final when
+  // the loads above were issued.  Now wait for K2's P-hat and status.
   pdl_wait();
-  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
-  {
+  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;  // mutate nothing
+#endif
+  if (blockIdx.x < 64 && nbias > 0) {  // bias mean (optimizer.py:111-113), first CTAs of the launch
+    bool bad = false;
+    const long long nb = min(64, (int)gridDim.x);
+    for (long long x = (long long)blockIdx.x * kThreads + t; x < nbias; x += nb * kThreads) {
+      const float v = P[bias_off + x];
+      bad |= !finite1(v);
+      bias_out[x] = divisor == 1 ? v : v / (float)divisor;
+    }
+    if (bad) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+  }
+  // 2. P-hat of the rows.  Fused: the matrix's first slab CTA orthogonalises
+  //    P / W (linalg.py:61-90, float64) while its loads fly and publishes it;
+  //    the other slabs of the matrix (dispatched after it) wait for the flag.
+  //    Tall: from K2.
+  if (fused && PSGD_K3_OWNER_GS) {
+    int state;
+    if (it.c0 == 0 && n <= 512 && r <= 4) {  // register warp MGS by warp 0
+      if (t == 0) s_flag = 0;
+      __syncthreads();
+      if (t < 32) {
+        const int before = *status;
+        warp_mgs(P + md.p_off, n, r, 1.0 / (double)divisor, repl + md.repl_off, Phat + md.p_off, status);
+        __threadfence();
+        if (t == 0 && (ld_acquire(status) & PSGD_STATUS_NONFINITE_P) && !(before & PSGD_STATUS_NONFINITE_P))
+          s_flag = 2;
+      }
+      __syncthreads();
+      state = s_flag == 2 ? 2 : 1;
+      if (state == 1)
+        for (int x = t; x < nrows * r; x += kThreads) ps[x] = __ldcg(Phat + md.p_off + (long long)rbeg * r + x);
+      __syncthreads();
+      if (t == 0) st_release(gs_flag + it.mat, state);
+    } else if (it.c0 == 0) {
+      const double inv_div = 1.0 / (double)divisor;
+      int bad = 0;
+      for (int idx = t; idx < n * r; idx += kThreads) {
+        const float v = P[md.p_off + idx];
+        bad |= !finite1(v);
+        const int i = idx / r, j = idx - i * r;
+        gsd[j * n + i] = (double)v * inv_div;  // column-major: conflict-free
+      }
+      state = __syncthreads_or(bad) ? 2 : 1;
+      if (state == 1) {
+        int par = 0;
+        SyncReducer sr{sred, &par};
+        mgs_inplace(gsd, n, r, repl + md.repl_off, t, kThreads, sr, status, 1, n);
+        __syncthreads();
+        for (int idx = t; idx < n * r; idx += kThreads) {
+          const int i = idx / r, j = idx - i * r;
+          const float v = (float)gsd[j * n + i];
+          ps[idx] = v;
+          Phat[md.p_off + idx] = v;
+        }
+        __threadfence();
+      } else if (t == 0) {
+        atomicOr(status, PSGD_STATUS_NONFINITE_P);  // linalg.py:35-36
+      }
+      __syncthreads();
+      if (t == 0) st_release(gs_flag + it.mat, state);
+    } else {
+      if (t == 0) {
+        int v;
+        while ((v = ld_acquire(gs_flag + it.mat)) == 0) __nanosleep(100);
+        s_flag = v;
+      }
+      __syncthreads();
+      state = s_flag;
+      if (state == 1)
+        for (int x = t; x < nrows * r; x += kThreads) ps[x] = __ldcg(Phat + md.p_off + (long long)rbeg * r + x);
+    }
+    if (t == 0 && atomicAdd(gs_done + it.mat, 1) == it.pad - 1) {  // last reader resets (self-cleaning)
+      gs_flag[it.mat] = 0;
+      gs_done[it.mat] = 0;
+    }
+    if (state != 1) return;
+  } else {
     const float* src = Phat + md.p_off + (long long)rbeg * r;
     for (int x = t; x < nrows * r; x += kThreads) ps[x] = src[x];
   }
@@ -1179,6 +1445,8 @@ struct psgd_plan {
   // K3 fused
   int k2_smem = 0;
   std::vector<int> small_list, gram_list;   // K2 in smem / in Gram space
+  std::vector<int> wlist, clist;             // K2 small: warp items / CTA items
+  int k2_wregion = 0, k2_wblocks = 0;
   std::vector<GramItem> gram_items;
   std::vector<int> apply_mat, apply_row0;   // k2_apply blocks
   long long wsg_elems = 0;
@@ -1204,6 +1472,8 @@ struct psgd_plan {
   GramItem* d_gram_items = nullptr;
   int *d_apply_mat = nullptr, *d_apply_row0 = nullptr;
   double *d_wsg = nullptr, *d_wsT = nullptr;
+  int *d_gs_flag = nullptr, *d_gs_done = nullptr;
+  std::vector<int> wlist_t, clist_t;        // K2 restricted to tall matrices
   int* d_gram_cnt = nullptr;
   RowItem *d_k4 = nullptr, *d_k5 = nullptr;
   double* d_gsws = nullptr;
@@ -1406,9 +1676,14 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
 
   for (int mi = 0; mi < nmat; ++mi) {
     const MatDev& md = pl->mats[mi];
-    if ((long long)md.n * md.r <= K2_SMEM_DOUBLES) {
-      pl->k2_smem = std::max(pl->k2_smem, md.n * md.r * 8);
+    if ((long long)md.n * md.r <= K2_WARP_DOUBLES) {
+      pl->wlist.push_back(mi);
       pl->small_list.push_back(mi);
+      pl->k2_wregion = std::max(pl->k2_wregion, (int)align4((long long)md.n * md.r));
+    } else if ((long long)md.n * md.r <= K2_SMEM_DOUBLES) {
+      pl->clist.push_back(mi);
+      pl->small_list.push_back(mi);
+      pl->k2_smem = std::max(pl->k2_smem, md.n * md.r * 8);
     } else {
       const int gidx = (int)pl->gram_list.size();
       pl->gram_list.push_back(mi);
@@ -1424,6 +1699,12 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       }
     }
   }
+  for (int mi : pl->wlist)
+    if (pl->mats[mi].tall) pl->wlist_t.push_back(mi);
+  for (int mi : pl->clist)
+    if (pl->mats[mi].tall) pl->clist_t.push_back(mi);
+  pl->k2_wblocks = ((int)pl->wlist.size() + K2_THREADS / 32 - 1) / (K2_THREADS / 32);
+  pl->k2_smem = std::max(pl->k2_smem, pl->k2_wregion * (K2_THREADS / 32) * 8);
   // ---- K3 slabs, grouped by r (one launch per group): fused slabs hold all rows
   {
     std::vector<int> rs;
@@ -1446,9 +1727,10 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
             pl->wsq_elems += (long long)cf.nchunks * C * r;
           }
           for (int ch = 0; ch < cf.nchunks; ++ch)
-            pl->k3.push_back({wo, mi, s * C, ch, cf.nchunks, slab_id, cf.vec, cf.cql, 0});
+            pl->k3.push_back({wo, mi, s * C, ch, cf.nchunks, slab_id, cf.vec, cf.cql, nslab});
         }
-        const int smem = (cf.rows_chunk * r + RG * C * r + C * r) * (int)sizeof(float);
+        const int smem = (cf.nchunks == 1 && PSGD_K3_OWNER_GS ? md.n * r * 8 : 0) +
+                         (cf.rows_chunk * r + RG * C * r + C * r) * (int)sizeof(float);
         gp.smem = std::max(gp.smem, smem);
       }
       gp.end = (int)pl->k3.size();
@@ -1475,7 +1757,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_k3 = take(pl->k3.size() * sizeof(SlabItem));
   const size_t o_tl = take(pl->tall_list.size() * sizeof(int));
   const size_t o_al = take(pl->all_list.size() * sizeof(int));
-  const size_t o_sl = take(pl->small_list.size() * sizeof(int));
+  const size_t o_sl = take((pl->wlist.size() + pl->clist.size() + pl->wlist_t.size() + pl->clist_t.size()) * sizeof(int));
   const size_t o_gl = take(pl->gram_list.size() * sizeof(int));
   const size_t o_gi = take(pl->gram_items.size() * sizeof(GramItem));
   const size_t o_am = take(pl->apply_mat.size() * sizeof(int));
@@ -1483,6 +1765,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_wg = take((size_t)std::max(1LL, pl->wsg_elems) * sizeof(double));
   const size_t o_wt = take(std::max<size_t>(1, pl->gram_list.size()) * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK * sizeof(double));
   const size_t o_gc = take(std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
+  const size_t o_gf = take((size_t)std::max(1, nmat) * 2 * sizeof(int));
   const size_t o_k4 = take(pl->k4.size() * sizeof(RowItem));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
@@ -1511,6 +1794,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_wsg = reinterpret_cast<double*>(b + o_wg);
   pl->d_wsT = reinterpret_cast<double*>(b + o_wt);
   pl->d_gram_cnt = reinterpret_cast<int*>(b + o_gc);
+  pl->d_gs_flag = reinterpret_cast<int*>(b + o_gf);
+  pl->d_gs_done = pl->d_gs_flag + std::max(1, nmat);
   pl->d_k4 = reinterpret_cast<RowItem*>(b + o_k4);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
@@ -1526,12 +1811,19 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_k3, pl->k3.data(), pl->k3.size() * sizeof(SlabItem));
   if (ce == cudaSuccess) ce = up(pl->d_tall_list, pl->tall_list.data(), pl->tall_list.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_all_list, pl->all_list.data(), pl->all_list.size() * sizeof(int));
-  if (ce == cudaSuccess) ce = up(pl->d_small_list, pl->small_list.data(), pl->small_list.size() * sizeof(int));
+  {
+    std::vector<int> wc(pl->wlist);
+    wc.insert(wc.end(), pl->clist.begin(), pl->clist.end());
+    wc.insert(wc.end(), pl->wlist_t.begin(), pl->wlist_t.end());
+    wc.insert(wc.end(), pl->clist_t.begin(), pl->clist_t.end());
+    if (ce == cudaSuccess) ce = up(pl->d_small_list, wc.data(), wc.size() * sizeof(int));
+  }
   if (ce == cudaSuccess) ce = up(pl->d_gram_list, pl->gram_list.data(), pl->gram_list.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_gram_items, pl->gram_items.data(), pl->gram_items.size() * sizeof(GramItem));
   if (ce == cudaSuccess) ce = up(pl->d_apply_mat, pl->apply_mat.data(), pl->apply_mat.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_apply_row0, pl->apply_row0.data(), pl->apply_row0.size() * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gram_cnt, 0, std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
+  if (ce == cudaSuccess) ce = cudaMemset(pl->d_gs_flag, 0, (size_t)std::max(1, nmat) * 2 * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
@@ -1637,16 +1929,19 @@ int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, con
 
 template <int R, bool EXACT>
 struct RunK3 {
-  static int run(const psgd_plan* pl, const Group& gp, float* work, const float* phat, float* qout, float* e,
-                 const int* status, cudaStream_t st) {
+  static int run(const psgd_plan* pl, const Group& gp, float* work, const float* p, int divisor,
+                 const double* repl, float* phat, float* qout, float* e, float* bias_out, long long nbias,
+                 int* status, cudaStream_t st) {
     const int nitems = gp.end - gp.beg;
     if (nitems <= 0) return PSGD_OK;
     auto kern = k3_slab<R, EXACT>;
     if (gp.smem > 48 * 1024)
       PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gp.smem));
     PSGD_CUDA_CHECK(launch_ex(kern, nitems, kThreads, gp.smem, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
-                              (const SlabItem*)(pl->d_k3 + gp.beg), work, phat, qout, e, pl->d_wsq,
-                              pl->d_counters, pl->world == 1 ? 1 : 0, status));
+                              (const SlabItem*)(pl->d_k3 + gp.beg), work, p, divisor, repl, phat, qout, e,
+                              pl->d_wsq, pl->d_counters, pl->d_gs_flag, pl->d_gs_done, bias_out, nbias,
+                              (long long)pl->p_bias_off, (long long)pl->flag_off, pl->nflags,
+                              pl->world == 1 ? 1 : 0, status));
     return PSGD_OK;
   }
 };
@@ -1681,20 +1976,24 @@ bool check_dev(const psgd_plan* pl) {
   return dev == pl->device;
 }
 
-int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, int divisor,
+int launch_k2(const psgd_plan* pl, bool tall_only, bool with_bias, const float* p, float* phat, int divisor,
               const double* repl, float* bias_out, int* status, cudaStream_t st) {
-  const int nlist = (int)pl->small_list.size();
+  const int nw = (int)(tall_only ? pl->wlist_t.size() : pl->wlist.size());
+  const int nci = (int)(tall_only ? pl->clist_t.size() : pl->clist.size());
+  const int* wl = pl->d_small_list + (tall_only ? pl->wlist.size() + pl->clist.size() : 0);
+  const int* cl = wl + nw;
+  const int nwb = (nw + K2_THREADS / 32 - 1) / (K2_THREADS / 32);
   const int bias_blocks =
-      (with_bias && pl->nbias > 0) ? (int)std::min<long long>(64, (pl->nbias + kGsThreads * 4 - 1) / (kGsThreads * 4)) : 0;
-  const int grid = nlist + bias_blocks;
+      (with_bias && pl->nbias > 0) ? (int)std::min<long long>(64, (pl->nbias + K2_THREADS * 4 - 1) / (K2_THREADS * 4)) : 0;
+  const int grid = nwb + nci + bias_blocks;
   if (grid > 0) {
     const size_t smem = (size_t)pl->k2_smem;
     if (smem > 48 * 1024)
       PSGD_CUDA_CHECK(cudaFuncSetAttribute(k2_gs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PSGD_CUDA_CHECK(launch_ex(k2_gs, grid, kGsThreads, smem, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
-                              (const int*)pl->d_small_list, nlist, p, phat, divisor, repl, pl->d_gsws, bias_out,
-                              (long long)pl->p_bias_off, (long long)pl->nbias, (long long)pl->flag_off,
-                              pl->nflags, status));
+    PSGD_CUDA_CHECK(launch_ex(k2_gs, grid, K2_THREADS, smem, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats, wl, nw,
+                              nwb, cl, nci, pl->k2_wregion, p, phat, divisor, repl, bias_out,
+                              (long long)pl->p_bias_off, (long long)pl->nbias, (long long)pl->flag_off, pl->nflags,
+                              status));
   }
   if (!pl->gram_items.empty()) {
     PSGD_CUDA_CHECK(launch_ex(k2_gram, (int)pl->gram_items.size(), 256, 0, st, false, (const MatDev*)pl->d_mats,
@@ -1732,7 +2031,7 @@ int psgd_orthogonalize(const psgd_plan* pl, const float* p, int32_t divisor, con
   if (!pl || !p || !p_hat || !status || divisor < 1 || (pl->nmat > 0 && !repl) ||
       (pl->nbias > 0 && !bias_out))
     return fail(PSGD_EINVAL, "psgd_orthogonalize: bad argument");
-  return launch_k2(pl, true, p, p_hat, divisor, repl, bias_out, (int*)status,
+  return launch_k2(pl, false, true, p, p_hat, divisor, repl, bias_out, (int*)status,
                    static_cast<cudaStream_t>(stream));
 }
 
@@ -1743,11 +2042,23 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
     return fail(PSGD_EINVAL, "psgd_q_ef: bad argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int rc = PSGD_OK;
-  rc = launch_k2(pl, true, p, p_hat, divisor, repl, bias_out, (int*)status, st);  // K2: P-hat, bias mean
-  if (rc) return rc;
-  for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab
-    rc = dispatch_r<RunK3>(gp.r, pl, gp, work, (const float*)p_hat, q_out, e, (const int*)status, st);
+#if PSGD_K3_OWNER_GS
+  const bool any_fused = pl->n_tall < pl->nmat;
+  if (pl->n_tall > 0 || (!any_fused && pl->nbias > 0)) {  // K2: P-hat of the tall matrices (+ bias)
+    rc = launch_k2(pl, true, !any_fused, p, p_hat, divisor, repl, bias_out, (int*)status, st);
     if (rc) return rc;
+  }
+  bool bias_done = !any_fused;
+#else
+  rc = launch_k2(pl, false, true, p, p_hat, divisor, repl, bias_out, (int*)status, st);  // K2: every P-hat + bias
+  if (rc) return rc;
+  bool bias_done = true;
+#endif
+  for (const Group& gp : pl->g3) {  // K3: q (+ GS, EF, M-hat) per slab
+    rc = dispatch_r<RunK3>(gp.r, pl, gp, work, p, (int)divisor, repl, p_hat, q_out, e, bias_out,
+                           bias_done ? 0LL : (long long)pl->nbias, (int*)status, st);
+    if (rc) return rc;
+    bias_done = true;
   }
   for (const Group& gp : pl->g4) {
     rc = dispatch_r<RunK4>(gp.r, pl, (const RowItem*)pl->d_k4, gp, work, e, (const float*)p_hat,
@@ -1777,7 +2088,6 @@ int psgd_step_single(const psgd_plan* pl, const float* g, float* e, float* work,
   if (!pl) return fail(PSGD_EINVAL, "NULL plan");
   if (pl->world != 1) return fail(PSGD_EINVAL, "psgd_step_single needs a world-1 plan");
   if (!status) return fail(PSGD_EINVAL, "NULL status");
-  PSGD_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
   int rc = psgd_ef_p(pl, g, e, work, q, p, bias_g, status, stream);
   if (!rc) rc = psgd_q_ef(pl, work, p, 1, repl, p_hat, q, e, bias_out, status, stream);
   return rc;

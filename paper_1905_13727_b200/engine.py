@@ -165,7 +165,6 @@ class PowerSGDEngine:
                                             ptr(self.P[0]), ptr(self.Phat), ptr(self.bias_g[0]), ptr(self.repl),
                                             ptr(self.bias_out), ptr(self.status), sp), "psgd_step_single")
             return
-        self.status.zero_()
         for w in range(self.nlocal):      # K1: delta = g + e, P = delta Q  (e NULL: EF off)
             _lib.check(lib.psgd_ef_p(h, ptr(self.g[w]), ptr(ein[w]), ptr(self.work[w]), ptr(self.Q),
                                      ptr(self.P[w]), ptr(self.bias_g[w]), ptr(self.status), sp), "psgd_ef_p")
