@@ -274,7 +274,7 @@ def run_ours(a):
         eng.status.zero_()
         ev[0].record(stream)
         _lib.check(lib.psgd_ef_p(h, ptr(eng.g[0]), ptr(eng.e[0]), ptr(eng.work[0]), ptr(eng.Q), ptr(eng.P[0]),
-                                 ptr(eng.bias_g[0]), ptr(eng.status), sp), "ef_p")
+                                 ptr(eng.Phat), ptr(eng.repl), ptr(eng.bias_g[0]), ptr(eng.status), sp), "ef_p")
         ev[1].record(stream)
         if world > 1:
             comm.all_reduce_sum_(eng.P[0])

@@ -94,10 +94,15 @@ int psgd_plan_matrix(const psgd_plan* plan, int32_t i, psgd_matrix_info* out);
  * g, e: flat_elems (e may be NULL: error feedback off, optimizer.py:118-119).
  * work: out delta.  q: warm-start Q (q_elems).  p: out P (p_elems; the bias
  * tail receives bias_g, the flag tail one non-finite flag per CTA, so the P
- * all-reduce carries them to every worker).  status: reset to 0 (the next
- * kernels raise PSGD_STATUS_* from the flags).  */
+ * all-reduce carries them to every worker).  status: reset to 0; raised to
+ * PSGD_STATUS_NONFINITE_GRAD by the last CTA when any flag is set.
+ * World-1 plans also orthogonalise (compressors.py:338, linalg.py:61-90) every
+ * matrix with n <= 512 and r_eff <= 4 as soon as its last chunk is done,
+ * writing P-hat to p_hat (seeded replacement columns from repl); p_hat and
+ * repl may be NULL when the plan's world > 1. */
 int psgd_ef_p(const psgd_plan* plan, const float* g, const float* e, float* work,
-              const float* q, float* p, const float* bias_g, int32_t* status, void* stream);
+              const float* q, float* p, float* p_hat, const double* repl, const float* bias_g,
+              int32_t* status, void* stream);
 
 /* K2 — standalone Gram-Schmidt: replaces compressors.py:337-338 after the sum,
  * P = P_sum / divisor (comm.py:97-98; divisor 1 = the W=1 copy), then

@@ -61,7 +61,7 @@ _SIGNATURES = {
     "psgd_plan_destroy": (_I32, [_P]),
     "psgd_plan_get_info": (_I32, [_P, ctypes.POINTER(PlanInfo)]),
     "psgd_plan_matrix": (_I32, [_P, _I32, ctypes.POINTER(MatrixInfo)]),
-    "psgd_ef_p": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "psgd_ef_p": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psgd_orthogonalize": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P]),
     "psgd_q_ef": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "psgd_decompress": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P]),

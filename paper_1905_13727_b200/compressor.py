@@ -203,6 +203,7 @@ class PowerSGD(Compressor):
         pl.q_view(q_in, 0).copy_(self._q_for(ctx, n, m, dev))
         status = torch.zeros(1, dtype=torch.int32, device=dev)
         repl = pl.repl_table()
+        phat = torch.zeros(pl.p_elems, **f32)
         works, ps = [], []
         with torch.cuda.device(dev):
             for d in ds:       # low_rank_iteration :336 (delta comes in already EF-added)
@@ -210,8 +211,8 @@ class PowerSGD(Compressor):
                 pl.matrix_view(g, 0).copy_(d)
                 w = torch.empty(pl.flat_elems, **f32)
                 p = torch.zeros(pl.p_elems, **f32)
-                _lib.check(lib.psgd_ef_p(h, ptr(g), None, ptr(w), ptr(q_in), ptr(p), None, ptr(status), sp),
-                           "psgd_ef_p")
+                _lib.check(lib.psgd_ef_p(h, ptr(g), None, ptr(w), ptr(q_in), ptr(p), ptr(phat), ptr(repl), None,
+                                         ptr(status), sp), "psgd_ef_p")
                 works.append(w)
                 ps.append(p)
             if dist:                      # :337
@@ -224,7 +225,6 @@ class PowerSGD(Compressor):
                 tree_mean_(ps, pm)
             else:
                 pm, div = ps[0], 1
-            phat = torch.zeros(pl.p_elems, **f32)
             qws, escratch = [], torch.empty(pl.flat_elems, **f32)
             for w in works:               # :338-339 (GS, q_w) and the EF locals (:376-378)
                 qw = torch.zeros(pl.q_elems, **f32)

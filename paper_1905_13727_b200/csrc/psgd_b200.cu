@@ -77,7 +77,8 @@ int fail(int code, const std::string& msg) {
 struct MatDev {
   long long flat_off, p_off, q_off, repl_off;
   int n, m, r, tall;
-  int lg1, qs, pad1, pad2;  // lg1: log2 lanes per row in K1 (2..8); qs: Q staged in smem by K1
+  int lg1, qs;  // lg1: log2 lanes per row in K1 (2..9); qs: Q staged in smem by K1
+  int nck, gs1;  // nck: K1 chunks of the matrix; gs1: orthogonalised by K1 (W = 1, n <= 512, r <= 4)
 };
 
 struct RowItem {   // K4 / K5 warp item: rows [row0, row0 + nrows) of `mat`, 2^lg lanes per row
@@ -165,6 +166,9 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 #endif
 #ifndef PSGD_PDL
 #define PSGD_PDL 1
+#endif
+#ifndef PSGD_K1_GS
+#define PSGD_K1_GS 0  // 1: at W = 1 the last K1 CTA orthogonalises (measured slower: register pressure)
 #endif
 #ifndef PSGD_K3_OWNER_GS
 #define PSGD_K3_OWNER_GS 0  // 1: fused matrices orthogonalised inside K3 (measured slower)
@@ -327,6 +331,119 @@ __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ 
       ++attempt;
     }
     col_scale(xj, 1.0 / nrm, n, rs, tid, nth);  // one fp64 divide; scale by the reciprocal
+  }
+}
+
+struct WarpReducer {  // one warp, shuffles only
+  __device__ double sum(double v) const {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  }
+};
+
+// ---- register-resident warp MGS (n <= 32 * RPL, r == R <= 4): each lane
+// owns rows lane + 32 k; dot products are RPL fused multiply-adds plus one
+// shuffle reduction, so the whole orthogonalisation of a 512 x 2 P is ~1 us.
+// Same sequence, threshold and replacement rule as mgs_inplace (linalg.py:61-90).
+template <int RPL, int R>
+__device__ __forceinline__ void warp_mgs_reg(const float* __restrict__ P, int n, double inv_div,
+                                             const double* __restrict__ repl, float* __restrict__ out,
+                                             int* status) {
+  const int lane = threadIdx.x & 31;
+  double x[R][RPL];
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int i = lane + 32 * k;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const float v = i < n ? __ldcg(P + i * R + j) : 0.f;
+      bad |= !finite1(v);
+      x[j][k] = (double)v * inv_div;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) {  // linalg.py:35-36 (ContractViolation)
+    if (lane == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
+    return;
+  }
+  auto wsum = [](double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  };
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
+    double before = sqrt(wsum(s));
+    double nrm = before;
+    for (int attempt = 0;; ++attempt) {
+      if (attempt == 1 || j > 0) {
+#pragma unroll
+        for (int i2 = 0; i2 < j; ++i2) {
+          double d = 0.0;
+#pragma unroll
+          for (int k = 0; k < RPL; ++k) d = fma(x[i2][k], x[j][k], d);
+          const double c = wsum(d);
+#pragma unroll
+          for (int k = 0; k < RPL; ++k) x[j][k] -= c * x[i2][k];
+        }
+        s = 0.0;
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
+        nrm = sqrt(wsum(s));
+      }
+      if (!(nrm < 1e-12 * (before + 1.0))) break;
+      if (attempt == 1) {  // the table holds attempt 0 only
+        if (lane == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
+        break;
+      }
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        const int i = lane + 32 * k;
+        x[j][k] = i < n ? repl[(long long)j * n + i] : 0.0;
+      }
+      before = 1.0;
+    }
+    const double inv = 1.0 / nrm;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) x[j][k] *= inv;
+  }
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int i = lane + 32 * k;
+    if (i < n)
+#pragma unroll
+      for (int j = 0; j < R; ++j) out[i * R + j] = (float)x[j][k];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ bool warp_mgs_dispatch_r(int rpl_log2, const float* P, int n, double inv_div,
+                                                    const double* repl, float* out, int* status) {
+  switch (rpl_log2) {
+    case 0: warp_mgs_reg<1, R>(P, n, inv_div, repl, out, status); return true;
+    case 1: warp_mgs_reg<2, R>(P, n, inv_div, repl, out, status); return true;
+    case 2: warp_mgs_reg<4, R>(P, n, inv_div, repl, out, status); return true;
+    case 3: warp_mgs_reg<8, R>(P, n, inv_div, repl, out, status); return true;
+    case 4: warp_mgs_reg<16, R>(P, n, inv_div, repl, out, status); return true;
+    default: return false;
+  }
+}
+
+// P-hat of one matrix by one warp when n <= 512 and r <= 4; false otherwise
+__device__ __forceinline__ bool warp_mgs(const float* P, int n, int r, double inv_div, const double* repl,
+                                         float* out, int* status) {
+  if (n > 512 || r > 4) return false;
+  int l = 0;
+  while ((32 << l) < n) ++l;
+  switch (r) {
+    case 1: return warp_mgs_dispatch_r<1>(l, P, n, inv_div, repl, out, status);
+    case 2: return warp_mgs_dispatch_r<2>(l, P, n, inv_div, repl, out, status);
+    case 3: return warp_mgs_dispatch_r<3>(l, P, n, inv_div, repl, out, status);
+    default: return warp_mgs_dispatch_r<4>(l, P, n, inv_div, repl, out, status);
   }
 }
 
@@ -493,8 +610,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const float* __restrict__ g, const float* __restrict__ e, float* __restrict__ work,
             const float* __restrict__ Q, float* __restrict__ P, float* __restrict__ psplit,
             int* __restrict__ split_cnt, const float* __restrict__ bias_g, long long nbias,
-            long long bias_off, long long flag_off, int* status) {
+            long long bias_off, long long flag_off, int nflags, const double* __restrict__ repl,
+            float* __restrict__ Phat, int nmat, int k1_tail, int* __restrict__ k1_done, int* status) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ int s_gs;
   float* sgb = reinterpret_cast<float*>(smem_raw);
   float* seb = sgb + K1_STAGES * K1_STAGE_FLOATS;
   float* qsl = reinterpret_cast<float*>(smem_raw + L.off_q);
@@ -613,122 +732,29 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   }
   if (bad) atomicOr(sflag, 1);
   bar_consumers();
+  if (t == 0) P[flag_off + blockIdx.x] = *sflag ? 1.f : 0.f;  // rides in the P all-reduce
+  if (!k1_tail) return;  // K2 raises the status from the flags and orthogonalises
+  // The last CTA to finish (every thread's P / delta writes fenced first)
+  // raises the status from all flags and, at W = 1, orthogonalises every
+  // eligible matrix, one warp each (compressors.py:338, linalg.py:61-90).
+  __threadfence();
+  bar_consumers();
+  if (t == 0) s_gs = atomicAdd(k1_done, 1) == (int)gridDim.x - 1;
+  bar_consumers();
+  if (!s_gs) return;
+  __threadfence();
   if (t == 0) {
-    P[flag_off + blockIdx.x] = *sflag ? 1.f : 0.f;  // carried to every rank by the P all-reduce
-    // (status is raised from these flags by K2 / K3, after every K1 CTA is done)
+    int any = 0;
+    for (int x = 0; x < nflags; ++x) any |= __ldcg(P + flag_off + x) != 0.f;
+    if (any) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+    s_gs = any;
+    *k1_done = 0;
   }
-}
-
-struct WarpReducer {  // one warp, shuffles only
-  __device__ double sum(double v) const {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    return v;
-  }
-};
-
-// ---- register-resident warp MGS (n <= 32 * RPL, r == R <= 4): each lane
-// owns rows lane + 32 k; dot products are RPL fused multiply-adds plus one
-// shuffle reduction, so the whole orthogonalisation of a 512 x 2 P is ~1 us.
-// Same sequence, threshold and replacement rule as mgs_inplace (linalg.py:61-90).
-template <int RPL, int R>
-__device__ __forceinline__ void warp_mgs_reg(const float* __restrict__ P, int n, double inv_div,
-                                             const double* __restrict__ repl, float* __restrict__ out,
-                                             int* status) {
-  const int lane = threadIdx.x & 31;
-  double x[R][RPL];
-  bool bad = false;
-#pragma unroll
-  for (int k = 0; k < RPL; ++k) {
-    const int i = lane + 32 * k;
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const float v = i < n ? P[i * R + j] : 0.f;
-      bad |= !finite1(v);
-      x[j][k] = (double)v * inv_div;
-    }
-  }
-  if (__any_sync(0xffffffffu, bad)) {  // linalg.py:35-36 (ContractViolation)
-    if (lane == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
-    return;
-  }
-  auto wsum = [](double v) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    return v;
-  };
-#pragma unroll
-  for (int j = 0; j < R; ++j) {
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
-    double before = sqrt(wsum(s));
-    double nrm = before;
-    for (int attempt = 0;; ++attempt) {
-      if (attempt == 1 || j > 0) {
-#pragma unroll
-        for (int i2 = 0; i2 < j; ++i2) {
-          double d = 0.0;
-#pragma unroll
-          for (int k = 0; k < RPL; ++k) d = fma(x[i2][k], x[j][k], d);
-          const double c = wsum(d);
-#pragma unroll
-          for (int k = 0; k < RPL; ++k) x[j][k] -= c * x[i2][k];
-        }
-        s = 0.0;
-#pragma unroll
-        for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
-        nrm = sqrt(wsum(s));
-      }
-      if (!(nrm < 1e-12 * (before + 1.0))) break;
-      if (attempt == 1) {  // the table holds attempt 0 only
-        if (lane == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
-        break;
-      }
-#pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = lane + 32 * k;
-        x[j][k] = i < n ? repl[(long long)j * n + i] : 0.0;
-      }
-      before = 1.0;
-    }
-    const double inv = 1.0 / nrm;
-#pragma unroll
-    for (int k = 0; k < RPL; ++k) x[j][k] *= inv;
-  }
-#pragma unroll
-  for (int k = 0; k < RPL; ++k) {
-    const int i = lane + 32 * k;
-    if (i < n)
-#pragma unroll
-      for (int j = 0; j < R; ++j) out[i * R + j] = (float)x[j][k];
-  }
-}
-
-template <int R>
-__device__ __forceinline__ bool warp_mgs_dispatch_r(int rpl_log2, const float* P, int n, double inv_div,
-                                                    const double* repl, float* out, int* status) {
-  switch (rpl_log2) {
-    case 0: warp_mgs_reg<1, R>(P, n, inv_div, repl, out, status); return true;
-    case 1: warp_mgs_reg<2, R>(P, n, inv_div, repl, out, status); return true;
-    case 2: warp_mgs_reg<4, R>(P, n, inv_div, repl, out, status); return true;
-    case 3: warp_mgs_reg<8, R>(P, n, inv_div, repl, out, status); return true;
-    case 4: warp_mgs_reg<16, R>(P, n, inv_div, repl, out, status); return true;
-    default: return false;
-  }
-}
-
-// P-hat of one matrix by one warp when n <= 512 and r <= 4; false otherwise
-__device__ __forceinline__ bool warp_mgs(const float* P, int n, int r, double inv_div, const double* repl,
-                                         float* out, int* status) {
-  if (n > 512 || r > 4) return false;
-  int l = 0;
-  while ((32 << l) < n) ++l;
-  switch (r) {
-    case 1: return warp_mgs_dispatch_r<1>(l, P, n, inv_div, repl, out, status);
-    case 2: return warp_mgs_dispatch_r<2>(l, P, n, inv_div, repl, out, status);
-    case 3: return warp_mgs_dispatch_r<3>(l, P, n, inv_div, repl, out, status);
-    default: return warp_mgs_dispatch_r<4>(l, P, n, inv_div, repl, out, status);
+  bar_consumers();
+  if (s_gs || Phat == nullptr) return;  // non-finite: the next kernels mutate nothing
+  for (int mi = warp; mi < nmat; mi += kConsWarps) {
+    const MatDev mdx = mats[mi];
+    if (mdx.gs1) warp_mgs(P + mdx.p_off, mdx.n, mdx.r, 1.0, repl + mdx.repl_off, Phat + mdx.p_off, status);
   }
 }
 
@@ -1029,7 +1055,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             const float* __restrict__ P, int divisor, const double* __restrict__ repl, float* __restrict__ Phat,
             float* __restrict__ qout, float* __restrict__ e, float* __restrict__ wsq, int* __restrict__ counters,
             int* __restrict__ gs_flag, int* __restrict__ gs_done, float* __restrict__ bias_out, long long nbias,
-            long long bias_off, long long flag_off, int nflags, int write_mhat, int* status) {
+            long long bias_off, long long flag_off, int nflags, int write_mhat, int wait_first,
+            int* status) {
   constexpr int DCAP = k3_dcap(R);
   extern __shared__ __align__(16) unsigned char k3smem[];
   __shared__ int s_flag;
@@ -1072,6 +1099,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     return;
   }
 #endif
+  if (wait_first) pdl_wait();  // K3 follows K1 directly: delta must be complete before any load
   // 1. every load of the slab in flight at once
   float d[DCAP];
   const long long base = md.flat_off + (long long)rbeg * m + col;
@@ -1472,7 +1500,8 @@ struct psgd_plan {
   GramItem* d_gram_items = nullptr;
   int *d_apply_mat = nullptr, *d_apply_row0 = nullptr;
   double *d_wsg = nullptr, *d_wsT = nullptr;
-  int *d_gs_flag = nullptr, *d_gs_done = nullptr;
+  int *d_gs_flag = nullptr, *d_gs_done = nullptr, *d_gs_cnt = nullptr, *d_k1_done = nullptr;
+  bool need_k2 = true;  // false: K1 orthogonalises every matrix (W = 1, n <= 512, r <= 4)
   std::vector<int> wlist_t, clist_t;        // K2 restricted to tall matrices
   int* d_gram_cnt = nullptr;
   RowItem *d_k4 = nullptr, *d_k5 = nullptr;
@@ -1602,6 +1631,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     md.tall = k3_tall_config(md.n, md.m, md.r).nchunks > 1;
     md.lg1 = lanes_log2_for(md.m, 9);
     md.qs = 0;  // decided below, once the K1 smem budget is known
+    md.gs1 = (PSGD_K1_GS && world == 1 && md.n <= 512 && md.r <= 4) ? 1 : 0;
     md.flat_off = fo;
     md.p_off = po;
     md.q_off = qo;
@@ -1643,6 +1673,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       }
     }
   }
+  for (auto& c : pl->k1) pl->mats[c.mat].nck++;
   {
     std::vector<double> w;
     for (auto& c : pl->k1) w.push_back((double)c.nrows * c.ncols + 64.0);
@@ -1700,10 +1731,11 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     }
   }
   for (int mi : pl->wlist)
-    if (pl->mats[mi].tall) pl->wlist_t.push_back(mi);
+    if (!pl->mats[mi].gs1) pl->wlist_t.push_back(mi);
   for (int mi : pl->clist)
-    if (pl->mats[mi].tall) pl->clist_t.push_back(mi);
+    if (!pl->mats[mi].gs1) pl->clist_t.push_back(mi);
   pl->k2_wblocks = ((int)pl->wlist.size() + K2_THREADS / 32 - 1) / (K2_THREADS / 32);
+  pl->need_k2 = !pl->wlist_t.empty() || !pl->clist_t.empty() || !pl->gram_items.empty();
   pl->k2_smem = std::max(pl->k2_smem, pl->k2_wregion * (K2_THREADS / 32) * 8);
   // ---- K3 slabs, grouped by r (one launch per group): fused slabs hold all rows
   {
@@ -1765,7 +1797,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_wg = take((size_t)std::max(1LL, pl->wsg_elems) * sizeof(double));
   const size_t o_wt = take(std::max<size_t>(1, pl->gram_list.size()) * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK * sizeof(double));
   const size_t o_gc = take(std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
-  const size_t o_gf = take((size_t)std::max(1, nmat) * 2 * sizeof(int));
+  const size_t o_gf = take((size_t)std::max(1, nmat) * 3 * sizeof(int) + 16);
   const size_t o_k4 = take(pl->k4.size() * sizeof(RowItem));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
@@ -1796,6 +1828,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_gram_cnt = reinterpret_cast<int*>(b + o_gc);
   pl->d_gs_flag = reinterpret_cast<int*>(b + o_gf);
   pl->d_gs_done = pl->d_gs_flag + std::max(1, nmat);
+  pl->d_gs_cnt = pl->d_gs_done + std::max(1, nmat);
+  pl->d_k1_done = pl->d_gs_cnt + std::max(1, nmat);
   pl->d_k4 = reinterpret_cast<RowItem*>(b + o_k4);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
@@ -1823,7 +1857,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_apply_mat, pl->apply_mat.data(), pl->apply_mat.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_apply_row0, pl->apply_row0.data(), pl->apply_row0.size() * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gram_cnt, 0, std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
-  if (ce == cudaSuccess) ce = cudaMemset(pl->d_gs_flag, 0, (size_t)std::max(1, nmat) * 2 * sizeof(int));
+  if (ce == cudaSuccess) ce = cudaMemset(pl->d_gs_flag, 0, (size_t)std::max(1, nmat) * 3 * sizeof(int) + 16);
   if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
@@ -1913,7 +1947,7 @@ cudaError_t launch_ex(Kern kern, int grid, int block, size_t smem, cudaStream_t 
 
 template <int RM>
 int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, const float* q, float* p,
-           const float* bias_g, int* status, cudaStream_t st) {
+           float* phat, const double* repl, const float* bias_g, int* status, cudaStream_t st) {
   const int grid = (int)pl->k1_beg.size() - 1;
   if (pl->k1.empty() && pl->nbias == 0) return PSGD_OK;
   auto kern = k1_ef_p<RM>;
@@ -1923,7 +1957,8 @@ int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, con
                             (const MatDev*)pl->d_mats, (const Chunk1*)pl->d_k1, (const int*)pl->d_k1_beg,
                             (const SplitRow*)pl->d_splits, pl->k1l, g, e, work, q, p, pl->d_psplit,
                             pl->d_split_cnt, bias_g, (long long)pl->nbias, (long long)pl->p_bias_off,
-                            (long long)pl->flag_off, status));
+                            (long long)pl->flag_off, pl->nflags, repl, phat, pl->nmat, pl->need_k2 ? 0 : 1,
+                            pl->d_k1_done, status));
   return PSGD_OK;
 }
 
@@ -1931,7 +1966,7 @@ template <int R, bool EXACT>
 struct RunK3 {
   static int run(const psgd_plan* pl, const Group& gp, float* work, const float* p, int divisor,
                  const double* repl, float* phat, float* qout, float* e, float* bias_out, long long nbias,
-                 int* status, cudaStream_t st) {
+                 bool wait_first, int* status, cudaStream_t st) {
     const int nitems = gp.end - gp.beg;
     if (nitems <= 0) return PSGD_OK;
     auto kern = k3_slab<R, EXACT>;
@@ -1941,7 +1976,7 @@ struct RunK3 {
                               (const SlabItem*)(pl->d_k3 + gp.beg), work, p, divisor, repl, phat, qout, e,
                               pl->d_wsq, pl->d_counters, pl->d_gs_flag, pl->d_gs_done, bias_out, nbias,
                               (long long)pl->p_bias_off, (long long)pl->flag_off, pl->nflags,
-                              pl->world == 1 ? 1 : 0, status));
+                              pl->world == 1 ? 1 : 0, wait_first ? 1 : 0, status));
     return PSGD_OK;
   }
 };
@@ -2012,17 +2047,19 @@ int launch_k2(const psgd_plan* pl, bool tall_only, bool with_bias, const float* 
 extern "C" {
 
 int psgd_ef_p(const psgd_plan* pl, const float* g, const float* e, float* work, const float* q,
-              float* p, const float* bias_g, int32_t* status, void* stream) {
+              float* p, float* p_hat, const double* repl, const float* bias_g, int32_t* status, void* stream) {
   if (!pl || !status || !p || (pl->nmat > 0 && (!g || !work || !q)) || (pl->nbias > 0 && !bias_g))
     return fail(PSGD_EINVAL, "psgd_ef_p: NULL argument");
+  if (pl->world == 1 && pl->nmat > 0 && (!p_hat || !repl))
+    return fail(PSGD_EINVAL, "psgd_ef_p: a world-1 plan orthogonalises in K1 and needs p_hat and repl");
   if (!check_dev(pl)) return fail(PSGD_EINVAL, "psgd_ef_p: plan belongs to another device");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (pl->rmax) {
-    case 1: return run_k1<1>(pl, g, e, work, q, p, bias_g, (int*)status, st);
-    case 2: return run_k1<2>(pl, g, e, work, q, p, bias_g, (int*)status, st);
-    case 4: return run_k1<4>(pl, g, e, work, q, p, bias_g, (int*)status, st);
-    case 8: return run_k1<8>(pl, g, e, work, q, p, bias_g, (int*)status, st);
-    default: return run_k1<16>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+    case 1: return run_k1<1>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
+    case 2: return run_k1<2>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
+    case 4: return run_k1<4>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
+    case 8: return run_k1<8>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
+    default: return run_k1<16>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
   }
 }
 
@@ -2050,13 +2087,20 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
   }
   bool bias_done = !any_fused;
 #else
-  rc = launch_k2(pl, false, true, p, p_hat, divisor, repl, bias_out, (int*)status, st);  // K2: every P-hat + bias
-  if (rc) return rc;
-  bool bias_done = true;
+  // K2: P-hat of the matrices K1 did not orthogonalise (all of them when W > 1) + bias mean
+  const bool k2 = pl->need_k2 || pl->world > 1 || divisor != 1;
+  if (k2) {
+    rc = launch_k2(pl, pl->world == 1 && divisor == 1, true, p, p_hat, divisor, repl, bias_out, (int*)status, st);
+    if (rc) return rc;
+  }
+  bool bias_done = k2;
 #endif
-  for (const Group& gp : pl->g3) {  // K3: q (+ GS, EF, M-hat) per slab
+  bool first = true;
+  for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab
+    // right after K1 (no K2 in between) a K3 CTA must wait before loading delta
     rc = dispatch_r<RunK3>(gp.r, pl, gp, work, p, (int)divisor, repl, p_hat, q_out, e, bias_out,
-                           bias_done ? 0LL : (long long)pl->nbias, (int*)status, st);
+                           bias_done ? 0LL : (long long)pl->nbias, first && !k2, (int*)status, st);
+    first = false;
     if (rc) return rc;
     bias_done = true;
   }
@@ -2088,7 +2132,7 @@ int psgd_step_single(const psgd_plan* pl, const float* g, float* e, float* work,
   if (!pl) return fail(PSGD_EINVAL, "NULL plan");
   if (pl->world != 1) return fail(PSGD_EINVAL, "psgd_step_single needs a world-1 plan");
   if (!status) return fail(PSGD_EINVAL, "NULL status");
-  int rc = psgd_ef_p(pl, g, e, work, q, p, bias_g, status, stream);
+  int rc = psgd_ef_p(pl, g, e, work, q, p, p_hat, repl, bias_g, status, stream);
   if (!rc) rc = psgd_q_ef(pl, work, p, 1, repl, p_hat, q, e, bias_out, status, stream);
   return rc;
 }

@@ -167,7 +167,8 @@ class PowerSGDEngine:
             return
         for w in range(self.nlocal):      # K1: delta = g + e, P = delta Q  (e NULL: EF off)
             _lib.check(lib.psgd_ef_p(h, ptr(self.g[w]), ptr(ein[w]), ptr(self.work[w]), ptr(self.Q),
-                                     ptr(self.P[w]), ptr(self.bias_g[w]), ptr(self.status), sp), "psgd_ef_p")
+                                     ptr(self.P[w]), ptr(self.Phat), ptr(self.repl), ptr(self.bias_g[w]),
+                                     ptr(self.status), sp), "psgd_ef_p")
         if self.distributed:              # AR1 (P + bias + flags), / W fused into K3
             self.comm.all_reduce_sum_(self.P[0])
             div = self.world

@@ -27,7 +27,7 @@ for path in sys.argv[1:]:
         eng.status.zero_()
         ev[0].record()
         _lib.check(lib.psgd_ef_p(h, ptr(eng.g[0]), ptr(eng.e[0]), ptr(eng.work[0]), ptr(eng.Q), ptr(eng.P[0]),
-                                 ptr(eng.bias_g[0]), ptr(eng.status), sp), "ef_p")
+                                 ptr(eng.Phat), ptr(eng.repl), ptr(eng.bias_g[0]), ptr(eng.status), sp), "ef_p")
         if os.environ.get("MIDFLUSH"):
             flush.zero_()
         ev[1].record()
