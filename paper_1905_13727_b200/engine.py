@@ -28,6 +28,7 @@ import torch
 
 from . import _lib
 from .comm import CommStats, tree_mean_
+from .distributed import first_nonfinite_site, step_charges
 from .linalg import ContractViolation
 from .plan import Plan, ptr, stream_ptr
 from .seeding import warm_start_q
@@ -106,18 +107,8 @@ class PowerSGDEngine:
             pl.q_view(self.Q, k).copy_(torch.from_numpy(q0))
         self.step_count = 0
         self._graph = None
-        # host-side accounting per step (integers)
-        bits = flops = dec = 0
-        for k, pi in enumerate(self.mat_index):
-            mi = pl.matrices[k]
-            n, m, r = mi.n, mi.m, mi.r_eff
-            flops += self.world * (4 * n * m * r + 2 * n * r * r + 3 * n * r)  # compressors.py:389-391
-            dec += 2 * n * m * r                                              # compressors.py:176-182
-            if self.world > 1:
-                bits += 32 * n * r + 32 * m * r                               # compressors.py:337,340
-        if self.world > 1:
-            bits += 32 * self.nbias                                           # optimizer.py:111-113
-        self._charge = (bits, flops, dec)
+        # host-side accounting per step (integers), charged as the reference does
+        self._charge = step_charges([(mi.n, mi.m, mi.r_eff) for mi in pl.matrices], self.nbias, self.world)
 
     # ------------------------------------------------------------------ views
     def grad_view(self, param_index, worker=0):
@@ -259,13 +250,5 @@ class PowerSGDEngine:
                 break
         if not self.distributed:
             return None if local is None else (self.specs[local[1]].name, local[0])
-        import torch.distributed as dist
-        big = len(self.specs) + 1
-        mine = torch.tensor([local[1] if local is not None else big], dtype=torch.int64,
-                            device=self.device)
-        allv = [torch.zeros_like(mine) for _ in range(self.world)]
-        dist.all_gather(allv, mine, group=self.comm.group)
-        for rank, v in enumerate(allv):
-            if int(v.item()) < big:
-                return (self.specs[int(v.item())].name, rank)
-        return None
+        site = first_nonfinite_site(None if local is None else local[1], self.comm, len(self.specs))
+        return None if site is None else (self.specs[site[0]].name, site[1])
