@@ -257,8 +257,8 @@ def run_ours(a):
     ms, ms_median = float(t[0]), float(t[1])
     eng.check()
     info = eng.plan.info
-    launches_per_step = (info.launches_ef_p + info.launches_q_ef
-                         + (info.launches_decompress if world > 1 else 0))
+    launches_per_step = (info.launches_step_single if world == 1 else
+                         info.launches_ef_p + info.launches_q_ef + info.launches_decompress)
 
     # ---------------- per-kernel breakdown (eager, same stream, L2 flushed)
     lib = _lib.lib()

@@ -67,6 +67,8 @@ typedef struct {
     int32_t launches_orthogonalize;
     int32_t launches_q_ef;
     int32_t launches_decompress;
+    int32_t launches_step_single; /* psgd_step_single: 1 when the fused single-kernel step applies */
+    int32_t fused_step;           /* 1: psgd_step_single runs k_step_w1 (one cooperative kernel) */
 } psgd_plan_info;
 
 typedef struct {

@@ -40,6 +40,7 @@ class PlanInfo(ctypes.Structure):
         ("n_tall", ctypes.c_int32), ("items_k1", ctypes.c_int64), ("items_k3", ctypes.c_int64),
         ("launches_ef_p", ctypes.c_int32), ("launches_orthogonalize", ctypes.c_int32),
         ("launches_q_ef", ctypes.c_int32), ("launches_decompress", ctypes.c_int32),
+        ("launches_step_single", ctypes.c_int32), ("fused_step", ctypes.c_int32),
     ]
 
 

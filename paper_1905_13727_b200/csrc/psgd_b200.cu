@@ -67,6 +67,18 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+bool psgd_force_multi() {
+  // The fused single-kernel step (k_step_w1) is correct but measured slower than
+  // the three-kernel step on B200 (GS latency and per-CTA imbalance sit on its
+  // critical path).  PSGD_FUSED_STEP=1 opts in for A/B measurement.
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("PSGD_FUSED_STEP");
+    v = (s && s[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 #define PSGD_CUDA_CHECK(expr)                                                        \
   do {                                                                               \
     cudaError_t _e = (expr);                                                         \
@@ -765,6 +777,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 // dependent launch: it waits for K1 (or the all-reduce), then immediately lets
 // K3 launch, so K3's CTAs stream their delta slabs in while this runs.
 
+struct GroupReducer {  // one 256-thread group of a CTA (named barrier 2 + gi), double-buffered partials
+  double* red;          // 2 x 8 doubles
+  int* parity;
+  int gi;
+  __device__ double sum(double v) const {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, w = (threadIdx.x >> 5) & 7;
+    double* buf = red + 8 * (*parity & 1);
+    ++*parity;
+    if (lane == 0) buf[w] = v;
+    asm volatile("bar.sync %0, 256;" ::"r"(2 + gi) : "memory");
+    double t = lane < 8 ? buf[lane] : 0.0;
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    return __shfl_sync(0xffffffffu, t, 0);
+  }
+};
+
 struct SyncReducer {  // all threads of the CTA, one __syncthreads per reduction
   double* red;        // 2 x 32 doubles, double-buffered by call parity
   int* parity;
@@ -776,8 +807,9 @@ struct SyncReducer {  // all threads of the CTA, one __syncthreads per reduction
     ++*parity;
     if (lane == 0) buf[warp] = v;
     __syncthreads();
-    double t = 0.0;
-    for (int w = 0; w < nw; ++w) t += buf[w];
+    double t = lane < nw ? buf[lane] : 0.0;  // every warp reduces the partials itself
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
     return t;
   }
 };
@@ -1314,6 +1346,333 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// ============================================================================= fused W=1 step
+// One persistent cooperative kernel per step (1 CTA per SM, 512 threads) when
+// the plan allows it (W = 1; every matrix has n <= rows a K3 CTA holds,
+// n <= 512, one r_eff <= 4): K1 phase (TMA ring, thread 0 refills) -> grid
+// barrier -> GS phase (one warp per matrix, register MGS) + bias mean -> grid
+// barrier -> K3 phase (two 256-thread register-slab groups per CTA).  Saves the
+// two kernel boundaries and K2's launch of the three-kernel step.
+
+__device__ __forceinline__ void bar_group(int gi) {
+  asm volatile("bar.sync %0, 256;" ::"r"(2 + gi) : "memory");
+}
+
+__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while ((unsigned)ld_acquire(reinterpret_cast<const int*>(ctr)) < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int KS_QSLOTS = 3;
+
+struct KsLayout {  // dynamic smem of the fused step
+  int qslot_floats;
+  int off_q, off_red, off_bar, total;
+};
+
+// one register slab (all rows x C cols) by a 256-thread group: q, e, M-hat (W = 1)
+template <int R>
+__device__ __forceinline__ void ks_slab(const SlabItem& it, const MatDev& md, float* __restrict__ work,
+                                        float* __restrict__ Q, float* __restrict__ e, float* smem, int gtid,
+                                        int gi) {
+  constexpr int DCAP = k3_dcap(R);
+  const int n = md.n, m = md.m, r = R;
+  const int vec = it.vec, cql = it.cq_log2;
+  const int CQ = 1 << cql, C = CQ * vec, RG = kThreads >> cql;
+  const int cq = gtid & (CQ - 1), rg = gtid >> cql;
+  const int col = it.c0 + cq * vec;
+  const bool colok = col < m;
+  const int ncols = min(C, m - it.c0);
+  float* ps = smem;                  // n x r
+  float* red = ps + kFusedNMax * r;  // RG x C x r
+  float* qs = red + RG * C * r;      // C x r
+  float d[DCAP];
+  const long long base = md.flat_off + col;
+  if (vec == 4) {
+#pragma unroll
+    for (int s = 0; s < DCAP / 4; ++s) {
+      const int li = rg + RG * s;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (colok && li < n) v = __ldcs(reinterpret_cast<const float4*>(work + base + (long long)li * m));
+      d[4 * s + 0] = v.x; d[4 * s + 1] = v.y; d[4 * s + 2] = v.z; d[4 * s + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < DCAP; ++s) {
+      const int li = rg + RG * s;
+      d[s] = (colok && li < n) ? __ldcs(work + base + (long long)li * m) : 0.f;
+    }
+  }
+  float qp[4][R];
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int k = 0; k < R; ++k) qp[v][k] = 0.f;
+  if (vec == 4) {
+#pragma unroll
+    for (int s = 0; s < DCAP / 4; ++s) {
+      const int li = rg + RG * s;
+      if (li < n) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+          const float pk = ps[li * r + k];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) qp[v][k] = fmaf(d[4 * s + v], pk, qp[v][k]);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < DCAP; ++s) {
+      const int li = rg + RG * s;
+      if (li < n)
+#pragma unroll
+        for (int k = 0; k < R; ++k) qp[0][k] = fmaf(d[s], ps[li * r + k], qp[0][k]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if (v < vec) red[(rg * C + cq * vec + v) * r + k] = qp[v][k];
+  bar_group(gi);
+  for (int o = gtid; o < C * r; o += kThreads) {
+    float s = 0.f;
+    for (int gidx = 0; gidx < RG; ++gidx) s += red[gidx * C * r + o];
+    qs[o] = s;
+  }
+  bar_group(gi);
+  {
+    float* qdst = Q + md.q_off + (long long)it.c0 * r;  // W = 1: q_w is the next warm start
+    for (int o = gtid; o < ncols * r; o += kThreads) qdst[o] = qs[o];
+  }
+  float qv[4][R];
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int k = 0; k < R; ++k) qv[v][k] = v < vec ? qs[(cq * vec + v) * r + k] : 0.f;
+  if (colok) {
+    if (vec == 4) {
+#pragma unroll
+      for (int s = 0; s < DCAP / 4; ++s) {
+        const int li = rg + RG * s;
+        if (li < n) {
+          float mh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const float pk = ps[li * r + k];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) mh[v] = fmaf(pk, qv[v][k], mh[v]);
+          }
+          const long long a = base + (long long)li * m;
+          st_stream(reinterpret_cast<float4*>(e + a), make_float4(d[4 * s] - mh[0], d[4 * s + 1] - mh[1],
+                                                                  d[4 * s + 2] - mh[2], d[4 * s + 3] - mh[3]));
+          st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < DCAP; ++s) {
+        const int li = rg + RG * s;
+        if (li < n) {
+          float mh = 0.f;
+#pragma unroll
+          for (int k = 0; k < R; ++k) mh = fmaf(ps[li * r + k], qv[0][k], mh);
+          const long long a = base + (long long)li * m;
+          st_stream(e + a, d[s] - mh);
+          st_stream(work + a, mh);
+        }
+      }
+    }
+  }
+  bar_group(gi);  // ps / red / qs free for the group's next slab
+}
+
+template <int R>
+__global__ void __launch_bounds__(kCons, 1)
+    k_step_w1(const MatDev* __restrict__ mats, int nmat, const Chunk1* __restrict__ chunks,
+              const int* __restrict__ k1_beg, const SplitRow* __restrict__ splits, KsLayout L,
+              const SlabItem* __restrict__ slabs, int nslabs, const float* __restrict__ g,
+              float* __restrict__ e, float* __restrict__ work, float* __restrict__ Q, float* __restrict__ P,
+              float* __restrict__ Phat, const double* __restrict__ repl, float* __restrict__ psplit,
+              int* __restrict__ split_cnt, const float* __restrict__ bias_g, float* __restrict__ bias_out,
+              long long nbias, long long bias_off, long long flag_off, unsigned* __restrict__ gbar,
+              int* __restrict__ status) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* sgb = reinterpret_cast<float*>(smem_raw);
+  float* seb = sgb + K1_STAGES * K1_STAGE_FLOATS;
+  float* qsl = reinterpret_cast<float*>(smem_raw + L.off_q);
+  float* red = reinterpret_cast<float*>(smem_raw + L.off_red);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
+  uint64_t* qfull = full + K1_STAGES;
+  __shared__ int s_flag;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int cb = k1_beg[blockIdx.x], ce = k1_beg[blockIdx.x + 1];
+  const unsigned grid = gridDim.x;
+#ifdef PSGD_KS_TIMING
+  unsigned long long tm[6];
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm[0]));
+#define KS_T(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm[i]))
+#else
+#define KS_T(i)
+#endif
+
+  // ------------------------------------------------ phase 1: delta = g + e, P = delta Q
+  if (t == 0) {
+    for (int s = 0; s < K1_STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < KS_QSLOTS; ++s) mbar_init(&qfull[s], 1);
+    s_flag = 0;
+    fence_mbar_init();
+    if (blockIdx.x == 0) *status = 0;
+  }
+  __syncthreads();
+  // thread 0 is the producer: chunk k goes to stage k % S; a new matrix's Q to slot mseq % 3
+  int p_cur = -1, p_qseq = -1;
+  const uint64_t pol = pol_evict_first(), polq = pol_evict_last();
+  auto issue = [&](int k) {
+    const Chunk1 ch = chunks[k];
+    const MatDev md = mats[ch.mat];
+    if (ch.mat != p_cur) {
+      p_cur = ch.mat;
+      if (md.qs) {
+        const int qsi = ++p_qseq % KS_QSLOTS;
+        const uint32_t qb = (uint32_t)((((long long)md.m * md.r + 3) & ~3LL) * 4);
+        mbar_expect_tx(&qfull[qsi], qb);
+        tma_load(qsl + qsi * L.qslot_floats, Q + md.q_off, qb, &qfull[qsi], polq);
+      }
+    }
+    const int s = (k - cb) % K1_STAGES;
+    const long long a4 = ch.off & ~3LL;
+    const long long span = (long long)(ch.nrows - 1) * md.m + ch.ncols;
+    const uint32_t bytes = (uint32_t)((((ch.off + span + 3) & ~3LL) - a4) * 4);
+    mbar_expect_tx(&full[s], 2 * bytes);
+    tma_load(sgb + s * K1_STAGE_FLOATS, g + a4, bytes, &full[s], pol);
+    tma_load(seb + s * K1_STAGE_FLOATS, e + a4, bytes, &full[s], pol);
+  };
+  if (t == 0)
+    for (int k = cb; k < min(ce, cb + K1_STAGES); ++k) issue(k);
+  bool bad = false;
+  for (long long x = (long long)blockIdx.x * kCons + t; x < nbias; x += (long long)grid * kCons) {
+    const float v = bias_g[x];
+    bad |= !finite1(v);
+    P[bias_off + x] = v;
+  }
+  {
+    const uint64_t keep = pol_evict_last();
+    int cur = -1, mseq = -1, rpar = 0;
+    MatDev md{};
+    for (int k = cb; k < ce; ++k) {
+      const int s = (k - cb) % K1_STAGES;
+      const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
+      const Chunk1 ch = chunks[k];
+      if (ch.mat != cur) {
+        md = mats[ch.mat];
+        cur = ch.mat;
+        if (md.qs) {
+          ++mseq;  // counts Q-slot uses only
+          mbar_wait(&qfull[mseq % KS_QSLOTS], (mseq / KS_QSLOTS) & 1);
+        }
+      }
+      mbar_wait(&full[s], ph);
+      float* rb = red + (rpar & 1) * (K1_RED_ROWS * kConsWarps * R + R);
+      if ((1 << md.lg1) > 32) ++rpar;
+      if (md.qs)
+        k1_chunk<R, true>(ch, md, qsl + (mseq % KS_QSLOTS) * L.qslot_floats, sgb + s * K1_STAGE_FLOATS,
+                          seb + s * K1_STAGE_FLOATS, true, work, P, splits, psplit, split_cnt, rb, keep, bad);
+      else
+        k1_chunk<R, false>(ch, md, Q + md.q_off, sgb + s * K1_STAGE_FLOATS, seb + s * K1_STAGE_FLOATS, true,
+                           work, P, splits, psplit, split_cnt, rb, keep, bad);
+      __syncthreads();  // stage s (and, three matrices back, its Q slot) is free
+      if (t == 0 && k + K1_STAGES < ce) issue(k + K1_STAGES);
+    }
+  }
+  if (bad) atomicOr(&s_flag, 1);
+  __syncthreads();
+  if (t == 0) P[flag_off + blockIdx.x] = s_flag ? 1.f : 0.f;
+  KS_T(1);
+  grid_sync(gbar, grid);
+  KS_T(2);
+
+  // ------------------------------------------------ phase 2+3: per-slab-group GS, q, e, M-hat
+  // No second grid barrier: each 256-thread group takes slabs from a global
+  // counter (dynamic balance) and orthogonalises a slab's matrix itself when it
+  // is new to the group (float64 MGS in smem, while the slab's loads fly).
+  int any = 0;
+  for (unsigned x = t; x < grid; x += kCons) any |= __ldcg(P + flag_off + x) != 0.f;
+  const bool poisoned = __syncthreads_or(any) != 0;
+  KS_T(3);
+  KS_T(4);
+  if (poisoned) {
+    if (blockIdx.x == 0 && t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);  // mutate nothing
+  } else {
+    for (long long x2 = (long long)blockIdx.x * kCons + t; x2 < nbias; x2 += (long long)grid * kCons)
+      bias_out[x2] = __ldcg(P + bias_off + x2);
+    const int gi = warp >> 3, gtid = t & 255;
+    float* gsm = reinterpret_cast<float*>(smem_raw) + gi * (L.off_q / 8);              // ps | red | qs
+    double* gsd = reinterpret_cast<double*>(smem_raw + L.off_q) + gi * (L.qslot_floats * KS_QSLOTS / 4);
+    __shared__ int s_k[2];
+    __shared__ double gred[2][2][8];
+    int cached = -1, gpar = 0;
+    bool skip = false;
+    MatDev md{};
+    for (;;) {
+      if (gtid == 0) s_k[gi] = (int)atomicAdd(gbar + 3, 1u);
+      bar_group(gi);
+      const int k = s_k[gi];
+      if (k >= nslabs) break;
+      const SlabItem it = slabs[k];
+      if (it.mat != cached) {
+        md = mats[it.mat];
+        cached = it.mat;
+        // P / 1 -> float64 column-major; MGS with group reductions (linalg.py:61-90)
+        const int n = md.n, r = md.r;
+        int pbad = 0;
+        for (int idx = gtid; idx < n * r; idx += kThreads) {
+          const float v = __ldcg(P + md.p_off + idx);
+          pbad |= !finite1(v);
+          const int i = idx / r, j = idx - i * r;
+          gsd[j * n + i] = (double)v;
+        }
+        GroupReducer grd{&gred[gi][0][0], &gpar, gi};
+        skip = grd.sum(pbad ? 1.0 : 0.0) != 0.0;
+        if (skip) {
+          if (gtid == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);  // linalg.py:35-36
+        } else {
+          mgs_inplace(gsd, n, r, repl + md.repl_off, gtid, kThreads, grd, status, 1, n);
+          bar_group(gi);
+          for (int idx = gtid; idx < n * r; idx += kThreads) {
+            const int i = idx / r, j = idx - i * r;
+            const float v = (float)gsd[j * n + i];
+            gsm[idx] = v;  // ps of the group
+            if (it.c0 == 0) Phat[md.p_off + idx] = v;
+          }
+        }
+        bar_group(gi);
+      }
+      if (!skip) ks_slab<R>(it, md, work, Q, e, gsm, gtid, gi);
+    }
+  }
+  __syncthreads();
+  KS_T(5);
+#ifdef PSGD_KS_TIMING
+  if (t == 0)
+    printf("ks blk %d: p1 %.1f  bar1 %.1f  p2 %.1f  bar2 %.1f  p3 %.1f us\n", blockIdx.x, (tm[1] - tm[0]) * 1e-3,
+           (tm[2] - tm[1]) * 1e-3, (tm[3] - tm[2]) * 1e-3, (tm[4] - tm[3]) * 1e-3, (tm[5] - tm[4]) * 1e-3);
+#endif
+  if (t == 0 && atomicAdd(gbar + 2, 1u) == grid - 1) {  // last CTA out resets the barriers
+    gbar[0] = 0;
+    gbar[1] = 0;
+    gbar[2] = 0;
+    gbar[3] = 0;
+  }
+}
+
 // K4 / K5 row streaming.  MODE 0 (K4): e = delta - P-hat q^T (+ M-hat in place
 // when write_mhat).  MODE 1 (K5): M-hat = P-hat (q / div)^T; items with
 // row0 == 0 store Q-bar = q / div.
@@ -1472,6 +1831,13 @@ struct psgd_plan {
   long long psplit_elems = 0;
   // K3 fused
   int k2_smem = 0;
+  // fused single-kernel W = 1 step (k_step_w1)
+  bool ks_ok = false;
+  int ks_r = 0;
+  KsLayout ksl{};
+  std::vector<int> ks_grp;
+  int* d_ks_grp = nullptr;
+  unsigned* d_gbar = nullptr;
   std::vector<int> small_list, gram_list;   // K2 in smem / in Gram space
   std::vector<int> wlist, clist;             // K2 small: warp items / CTA items
   int k2_wregion = 0, k2_wblocks = 0;
@@ -1676,7 +2042,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   for (auto& c : pl->k1) pl->mats[c.mat].nck++;
   {
     std::vector<double> w;
-    for (auto& c : pl->k1) w.push_back((double)c.nrows * c.ncols + 64.0);
+    for (auto& c : pl->k1) w.push_back((double)c.nrows * c.ncols + 2048.0);  // + per-chunk overhead
     pl->k1_beg = balance(w, pl->nsm);
   }
   pl->nflags = std::max(1, (int)pl->k1_beg.size() - 1);
@@ -1772,6 +2138,33 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   build_row_items(pl->mats, true, pl->k4, pl->g4);
   build_row_items(pl->mats, false, pl->k5, pl->g5);
 
+  // ---- fused W = 1 step eligibility and layout
+  {
+    bool ok = world == 1 && nmat > 0 && pl->n_tall == 0 && pl->g3.size() == 1;
+    const int r0 = nmat > 0 ? pl->mats[0].r : 0;
+    for (auto& md : pl->mats) ok = ok && md.r == r0 && md.n <= 512 && md.qs;
+    ok = ok && r0 >= 1 && r0 <= 4 && (int)pl->k1_beg.size() - 1 <= pl->nsm;
+    KsLayout& L = pl->ksl;
+    L.qslot_floats = pl->k1l.qslot_floats;
+    int off = 2 * K1_STAGES * K1_STAGE_FLOATS * 4;
+    L.off_q = off;   off += KS_QSLOTS * L.qslot_floats * 4;
+    L.off_red = off; off += 2 * (K1_RED_ROWS * kConsWarps * std::max(r0, 1) + std::max(r0, 1)) * 4;
+    off = (off + 15) & ~15;
+    L.off_bar = off; off += (K1_STAGES + KS_QSLOTS) * 8 + 16;
+    L.total = off;
+    ok = ok && L.total <= 227 * 1024;
+    // each 256-thread group needs (512 + 1024 + 1024) * r floats of the stage area half
+    ok = ok && (512 + 2048) * r0 * 4 <= L.off_q / 2;
+    if (ok) {
+      const int groups = 2 * ((int)pl->k1_beg.size() - 1);
+      std::vector<double> w;
+      for (auto& it : pl->k3) w.push_back((double)pl->mats[it.mat].n * (it.vec << it.cq_log2) + 256.0);
+      pl->ks_grp = balance(w, groups);
+      while ((int)pl->ks_grp.size() < groups + 1) pl->ks_grp.push_back((int)pl->k3.size());
+    }
+    pl->ks_ok = ok;
+    pl->ks_r = r0;
+  }
   // ---- device block
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t off = 0;
@@ -1798,6 +2191,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_wt = take(std::max<size_t>(1, pl->gram_list.size()) * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK * sizeof(double));
   const size_t o_gc = take(std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
   const size_t o_gf = take((size_t)std::max(1, nmat) * 3 * sizeof(int) + 16);
+  const size_t o_ksg = take(pl->ks_grp.size() * sizeof(int));
+  const size_t o_gbar = take(4 * sizeof(unsigned));
   const size_t o_k4 = take(pl->k4.size() * sizeof(RowItem));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
@@ -1830,6 +2225,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_gs_done = pl->d_gs_flag + std::max(1, nmat);
   pl->d_gs_cnt = pl->d_gs_done + std::max(1, nmat);
   pl->d_k1_done = pl->d_gs_cnt + std::max(1, nmat);
+  pl->d_ks_grp = reinterpret_cast<int*>(b + o_ksg);
+  pl->d_gbar = reinterpret_cast<unsigned*>(b + o_gbar);
   pl->d_k4 = reinterpret_cast<RowItem*>(b + o_k4);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
@@ -1858,6 +2255,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_apply_row0, pl->apply_row0.data(), pl->apply_row0.size() * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gram_cnt, 0, std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gs_flag, 0, (size_t)std::max(1, nmat) * 3 * sizeof(int) + 16);
+  if (ce == cudaSuccess) ce = up(pl->d_ks_grp, pl->ks_grp.data(), pl->ks_grp.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = cudaMemset(pl->d_gbar, 0, 4 * sizeof(unsigned));
   if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
@@ -1905,6 +2304,9 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4);
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
+  const bool fused_step = pl->ks_ok && !psgd_force_multi();
+  o->launches_step_single = fused_step ? 1 : o->launches_ef_p + o->launches_q_ef;
+  o->fused_step = fused_step ? 1 : 0;
   return PSGD_OK;
 }
 
@@ -2042,6 +2444,43 @@ int launch_k2(const psgd_plan* pl, bool tall_only, bool with_bias, const float* 
   return PSGD_OK;
 }
 
+template <int R>
+int run_ks_r(const psgd_plan* pl, const float* g, float* e, float* work, float* q, float* p, float* p_hat,
+             const float* bias_g, const double* repl, float* bias_out, int* status, cudaStream_t st) {
+  auto kern = k_step_w1<R>;
+  const int grid = (int)pl->k1_beg.size() - 1;
+  PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->ksl.total));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kCons);
+  cfg.dynamicSmemBytes = pl->ksl.total;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: grid barriers are safe
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PSGD_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (const MatDev*)pl->d_mats, pl->nmat, (const Chunk1*)pl->d_k1,
+                                     (const int*)pl->d_k1_beg, (const SplitRow*)pl->d_splits, pl->ksl,
+                                     (const SlabItem*)pl->d_k3, (int)pl->k3.size(), g, e, work, q, p,
+                                     p_hat, repl, pl->d_psplit, pl->d_split_cnt, bias_g, bias_out,
+                                     (long long)pl->nbias, (long long)pl->p_bias_off, (long long)pl->flag_off,
+                                     pl->d_gbar, status));
+  return PSGD_OK;
+}
+
+int run_ks(const psgd_plan* pl, const float* g, float* e, float* work, float* q, float* p, float* p_hat,
+           const float* bias_g, const double* repl, float* bias_out, int* status, cudaStream_t st) {
+  switch (pl->ks_r) {
+    case 1: return run_ks_r<1>(pl, g, e, work, q, p, p_hat, bias_g, repl, bias_out, status, st);
+    case 2: return run_ks_r<2>(pl, g, e, work, q, p, p_hat, bias_g, repl, bias_out, status, st);
+    case 3: return run_ks_r<3>(pl, g, e, work, q, p, p_hat, bias_g, repl, bias_out, status, st);
+    default: return run_ks_r<4>(pl, g, e, work, q, p, p_hat, bias_g, repl, bias_out, status, st);
+  }
+}
+
+
+
 }  // namespace
 
 extern "C" {
@@ -2132,6 +2571,9 @@ int psgd_step_single(const psgd_plan* pl, const float* g, float* e, float* work,
   if (!pl) return fail(PSGD_EINVAL, "NULL plan");
   if (pl->world != 1) return fail(PSGD_EINVAL, "psgd_step_single needs a world-1 plan");
   if (!status) return fail(PSGD_EINVAL, "NULL status");
+  if (pl->ks_ok && e != nullptr && !psgd_force_multi()) return run_ks(pl, g, e, work, q, p, p_hat, bias_g, repl,
+                                                                      bias_out, (int*)status,
+                                                                      static_cast<cudaStream_t>(stream));
   int rc = psgd_ef_p(pl, g, e, work, q, p, p_hat, repl, bias_g, status, stream);
   if (!rc) rc = psgd_q_ef(pl, work, p, 1, repl, p_hat, q, e, bias_out, status, stream);
   return rc;
