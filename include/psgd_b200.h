@@ -54,7 +54,7 @@ typedef struct {
     int64_t flat_elems;   /* length of the g / e / work buffers (matrices packed, 16-B aligned starts) */
     int64_t p_elems;      /* length of the packed P buffer: sum n*r_eff (aligned) + bias tail + flags */
     int64_t p_bias_off;   /* offset of the bias tail inside the P buffer */
-    int64_t q_elems;      /* length of the packed Q buffers: sum m*r_eff (aligned) */
+    int64_t q_elems;      /* length of the packed Q buffers: sum r_eff * q_ld */
     int64_t repl_elems;   /* doubles in the degenerate-column replacement table */
     int64_t nbias;        /* bias scalars carried uncompressed */
     int32_t nmat;
@@ -74,10 +74,12 @@ typedef struct {
 typedef struct {
     int64_t flat_off;     /* element offset of the n x m row-major matrix in g / e / work */
     int64_t p_off;        /* element offset of its n x r_eff P block */
-    int64_t q_off;        /* element offset of its m x r_eff Q block */
+    int64_t q_off;        /* element offset of its Q block: column-major, (j, k) at q_off + k * q_ld + j */
     int64_t repl_off;     /* double offset of its r_eff replacement columns (column-major, n each) */
     int32_t n, m, r_eff;
     int32_t tall;         /* 1: n > fused limit, q via split-n partials + separate EF pass */
+    int32_t q_ld;         /* column stride of the Q block (m rounded up to a multiple of 4) */
+    int32_t pad;
 } psgd_matrix_info;
 
 /* Plan: shapes -> packed layout, per-kernel work lists, plan-owned scratch.

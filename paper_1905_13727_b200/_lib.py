@@ -48,7 +48,8 @@ class MatrixInfo(ctypes.Structure):
     _fields_ = [
         ("flat_off", ctypes.c_int64), ("p_off", ctypes.c_int64), ("q_off", ctypes.c_int64),
         ("repl_off", ctypes.c_int64), ("n", ctypes.c_int32), ("m", ctypes.c_int32),
-        ("r_eff", ctypes.c_int32), ("tall", ctypes.c_int32),
+        ("r_eff", ctypes.c_int32), ("tall", ctypes.c_int32), ("q_ld", ctypes.c_int32),
+        ("pad", ctypes.c_int32),
     ]
 
 

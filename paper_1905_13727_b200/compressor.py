@@ -262,7 +262,7 @@ class PowerSGD(Compressor):
             raise ContractViolation("orthogonalize input contains non-finite entries")
         if st & _lib.STATUS_REPLACEMENT:
             raise RuntimeError("Gram-Schmidt needed more than one replacement draw")
-        q_new = pl.q_view(qbar, 0).clone()
+        q_new = pl.q_view(qbar, 0).contiguous()
         self.q_memory[ctx.param_index] = q_new           # :373
         comm.stats.decode_ops += 2 * n * m * r           # :374
         payload = LowRank(_out(pl.p_view(phat, 0).clone(), as_np), _out(q_new, as_np))

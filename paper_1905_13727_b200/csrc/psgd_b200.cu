@@ -52,8 +52,8 @@ constexpr int kTmaThreads = kCons + 32;  // + 1 producer warp
 constexpr int kRowItemElems = 4096;
 constexpr int kGsThreads = 1024;
 constexpr int kFusedNMax = 512;    // K3 fused path holds all rows of a slab
-constexpr int K1_STAGES = 3;
-constexpr int K1_CHUNK = 4608;     // floats of g (and of e) per chunk
+constexpr int K1_STAGES = 3;       // max stages (the plan picks 2 or 3 and the stage size)
+constexpr int K1_CHUNK = 4608;     // floats of g (and of e) per chunk at the smallest stage
 constexpr int K1_QSLOT_CAP = 12288;  // floats of Q per smem slot (2 slots)
 constexpr int K1_RED_ROWS = 16;
 constexpr int K1_STAGE_FLOATS = K1_CHUNK + 8;  // + misalignment slack of a chunk
@@ -91,6 +91,7 @@ struct MatDev {
   int n, m, r, tall;
   int lg1, qs;  // lg1: log2 lanes per row in K1 (2..9); qs: Q staged in smem by K1
   int nck, gs1;  // nck: K1 chunks of the matrix; gs1: orthogonalised by K1 (W = 1, n <= 512, r <= 4)
+  int qld, pad3;  // Q is column-major: element (j, k) at q_off + k * qld + j, qld = align4(m)
 };
 
 struct RowItem {   // K4 / K5 warp item: rows [row0, row0 + nrows) of `mat`, 2^lg lanes per row
@@ -223,23 +224,27 @@ __device__ __forceinline__ bool finite4(float4 v) {
   return finite1(v.x) & finite1(v.y) & finite1(v.z) & finite1(v.w);
 }
 
-// Q rows j0..j0+3 (4*r consecutive floats at q) -> qv[4][RM]; r <= RM.
-template <int RM>
-__device__ __forceinline__ void load_q4(const float* __restrict__ q, bool aligned, int r,
+// Q rows j0..j0+3 of every column k < r (Q column-major, column stride ld) -> qv[4][RM].
+// Lanes handle consecutive j0, so each column read is a run of consecutive
+// 16-B words across the warp (bank-conflict free in smem, coalesced in L1).
+template <int RM, bool SMEM>
+__device__ __forceinline__ void load_q4(const float* __restrict__ q, int ld, bool aligned, int r,
                                         float (&qv)[4][RM]) {
-  if (r == RM && aligned) {
 #pragma unroll
-    for (int t = 0; t < RM; ++t) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(q) + t);
-      const float vv[4] = {v.x, v.y, v.z, v.w};
+  for (int k = 0; k < RM; ++k) {
+    if (k < r) {
+      const float* qk = q + (long long)k * ld;
+      if (aligned) {
+        const float4 v = SMEM ? *reinterpret_cast<const float4*>(qk) : __ldg(reinterpret_cast<const float4*>(qk));
+        qv[0][k] = v.x; qv[1][k] = v.y; qv[2][k] = v.z; qv[3][k] = v.w;
+      } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) qv[(4 * t + u) / RM][(4 * t + u) % RM] = vv[u];
+        for (int jj = 0; jj < 4; ++jj) qv[jj][k] = SMEM ? qk[jj] : __ldg(qk + jj);
+      }
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) qv[jj][k] = 0.f;
     }
-  } else {
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-      for (int k = 0; k < RM; ++k) qv[jj][k] = k < r ? __ldg(q + jj * r + k) : 0.f;
   }
 }
 
@@ -465,29 +470,8 @@ __device__ __forceinline__ bool warp_mgs(const float* P, int n, int r, double in
 struct K1Layout {  // dynamic smem: g stages | e stages | Q slots | red | barriers
   int qslot_floats;
   int off_q, off_red, off_bar, total;
+  int stages, stage_floats;  // chosen per plan: the largest stage that fits beside the Q slots
 };
-
-template <int RM, bool QS>
-__device__ __forceinline__ void k1_q4(const float* __restrict__ q, bool aligned, int r, float (&qv)[4][RM]) {
-  if (QS) {  // Q staged in shared memory
-    if (r == RM && aligned) {
-#pragma unroll
-      for (int t = 0; t < RM; ++t) {
-        const float4 v = reinterpret_cast<const float4*>(q)[t];
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) qv[(4 * t + u) / RM][(4 * t + u) % RM] = vv[u];
-      }
-    } else {
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-        for (int k = 0; k < RM; ++k) qv[jj][k] = k < r ? q[jj * r + k] : 0.f;
-    }
-  } else {
-    load_q4<RM>(q, aligned, r, qv);
-  }
-}
 
 // One chunk: rows of the chunk to row groups of G = 2^lg consumer threads.
 template <int RM, bool QS>
@@ -523,16 +507,16 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
         const float gv = sg[sm + j];
         const float d = has_e ? gv + se[sm + j] : gv;
         st_hint(work + og + j, d, keep);
-        const float* qj = Qm + (long long)(ch.c0 + j) * r;
+        const float* qj = Qm + ch.c0 + j;
 #pragma unroll
         for (int q = 0; q < RM; ++q)
-          if (q < r) acc[q] = fmaf(d, QS ? qj[q] : __ldg(qj + q), acc[q]);
+          if (q < r) acc[q] = fmaf(d, QS ? qj[(long long)q * md.qld] : __ldg(qj + (long long)q * md.qld), acc[q]);
       }
       const float4* __restrict__ g4 = reinterpret_cast<const float4*>(sg + sm + head);
       const float4* __restrict__ e4 = reinterpret_cast<const float4*>(se + sm + head);
       float4* __restrict__ w4 = reinterpret_cast<float4*>(work + og + head);
-      const float* __restrict__ qrow = Qm + (long long)(ch.c0 + head) * r;
-      const bool qal = (((ch.c0 + head) * r) & 3) == 0;
+      const float* __restrict__ qrow = Qm + ch.c0 + head;
+      const bool qal = ((ch.c0 + head) & 3) == 0;
 #pragma unroll 2
       for (int c = gl; c < body4; c += G) {
         const float4 gv = g4[c];
@@ -542,7 +526,7 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
         st_hint(w4 + c, d, keep);
 #endif
         float qv[4][RM];
-        k1_q4<RM, QS>(qrow + (long long)(4 * c) * r, qal, r, qv);
+        load_q4<RM, QS>(qrow + 4 * c, md.qld, qal, r, qv);
 #pragma unroll
         for (int q = 0; q < RM; ++q) {
           acc[q] = fmaf(d.x, qv[0][q], acc[q]);
@@ -627,18 +611,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ int s_gs;
   float* sgb = reinterpret_cast<float*>(smem_raw);
-  float* seb = sgb + K1_STAGES * K1_STAGE_FLOATS;
+  float* seb = sgb + L.stages * L.stage_floats;
   float* qsl = reinterpret_cast<float*>(smem_raw + L.off_q);
   float* red = reinterpret_cast<float*>(smem_raw + L.off_red);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
-  uint64_t* empty = full + K1_STAGES;
-  uint64_t* qfull = empty + K1_STAGES;
+  uint64_t* empty = full + L.stages;
+  uint64_t* qfull = empty + L.stages;
   uint64_t* qempty = qfull + 2;
   int* sflag = reinterpret_cast<int*>(qempty + 2);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int cb = cta_beg[blockIdx.x], ce = cta_beg[blockIdx.x + 1];
   if (t == 0) {
-    for (int s = 0; s < K1_STAGES; ++s) {
+    for (int s = 0; s < L.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsWarps);
     }
@@ -663,8 +647,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       Chunk1 nx = chunks[cb < ce ? cb : 0];
       MatDev md{};
       for (int k = cb; k < ce; ++k) {
-        const int s = (k - cb) % K1_STAGES;
-        const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
+        const int s = (k - cb) % L.stages;
+        const uint32_t ph = ((k - cb) / L.stages) & 1;
         const Chunk1 ch = nx;
         if (k + 1 < ce) nx = chunks[k + 1];  // next descriptor in flight
         if (ch.mat != cur) {  // Q of the next matrix into a smem slot (double-buffered)
@@ -674,7 +658,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
           if (md.qs) {
             const int qs = mseq & 1;
             mbar_wait(&qempty[qs], ((mseq >> 1) & 1) ^ 1);
-            const uint32_t qb = (uint32_t)((((long long)md.m * md.r + 3) & ~3LL) * 4);
+            const uint32_t qb = (uint32_t)((long long)md.r * md.qld * 4);
             mbar_expect_tx(&qfull[qs], qb);
             tma_load(qsl + qs * L.qslot_floats, Q + md.q_off, qb, &qfull[qs], polq);
           }
@@ -685,8 +669,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const long long b4 = (ch.off + span + 3) & ~3LL;
         const uint32_t bytes = (uint32_t)((b4 - a4) * 4);
         mbar_expect_tx(&full[s], e ? 2 * bytes : bytes);
-        tma_load(sgb + s * K1_STAGE_FLOATS, g + a4, bytes, &full[s], pol);
-        if (e) tma_load(seb + s * K1_STAGE_FLOATS, e + a4, bytes, &full[s], pol);
+        tma_load(sgb + s * L.stage_floats, g + a4, bytes, &full[s], pol);
+        if (e) tma_load(seb + s * L.stage_floats, e + a4, bytes, &full[s], pol);
       }
     }
     return;
@@ -705,8 +689,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   Chunk1 nx = chunks[cb < ce ? cb : 0];
   MatDev md{};
   for (int k = cb; k < ce; ++k) {
-    const int s = (k - cb) % K1_STAGES;
-    const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
+    const int s = (k - cb) % L.stages;
+    const uint32_t ph = ((k - cb) / L.stages) & 1;
     const Chunk1 ch = nx;
     if (k + 1 < ce) nx = chunks[k + 1];  // next descriptor in flight
     if (ch.mat != cur) {
@@ -721,8 +705,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       if (cur_qs) mbar_wait(&qfull[mseq & 1], (mseq >> 1) & 1);
     }
     mbar_wait(&full[s], ph);
-    const float* sg = sgb + s * K1_STAGE_FLOATS;
-    const float* se = seb + s * K1_STAGE_FLOATS;
+    const float* sg = sgb + s * L.stage_floats;
+    const float* se = seb + s * L.stage_floats;
     float* rb = red + (rpar & 1) * (K1_RED_ROWS * kConsWarps * RM + RM);
     if ((1 << md.lg1) > 32) ++rpar;
 #ifdef PSGD_K1_NOCOMPUTE
@@ -1281,7 +1265,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     qs[o] = s;
   }
   __syncthreads();
-  float* __restrict__ qdst = qout + md.q_off + (long long)it.c0 * r;
+  float* __restrict__ qdst = qout + md.q_off + it.c0;  // column-major: (c, k) at k * qld + c
   if (!fused) {  // partial of a tall slab; the last chunk combines in chunk order
     float* part = wsq + it.ws_off;
     for (int o = t; o < ncols * r; o += kThreads) part[(long long)it.chunk * C * r + o] = qs[o];
@@ -1292,15 +1276,19 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (s_flag) {
       __threadfence();
       for (int o = t; o < ncols * r; o += kThreads) {
+        const int k = o / ncols, cc = o - k * ncols;
         float s = 0.f;
-        for (int ch = 0; ch < it.nchunks; ++ch) s += __ldcg(part + (long long)ch * C * r + o);
-        qdst[o] = s;
+        for (int ch = 0; ch < it.nchunks; ++ch) s += __ldcg(part + (long long)ch * C * r + cc * r + k);
+        qdst[(long long)k * md.qld + cc] = s;
       }
       if (t == 0) counters[it.slab] = 0;
     }
     return;
   }
-  for (int o = t; o < ncols * r; o += kThreads) qdst[o] = qs[o];
+  for (int o = t; o < ncols * r; o += kThreads) {
+    const int k = o / ncols, cc = o - k * ncols;
+    qdst[(long long)k * md.qld + cc] = qs[cc * r + k];
+  }
   // 5. error feedback (and M-hat at W=1) from the registers
   float qv[4][R];
 #pragma unroll
@@ -1374,6 +1362,7 @@ constexpr int KS_QSLOTS = 3;
 struct KsLayout {  // dynamic smem of the fused step
   int qslot_floats;
   int off_q, off_red, off_bar, total;
+  int stages, stage_floats;
 };
 
 // one register slab (all rows x C cols) by a 256-thread group: q, e, M-hat (W = 1)
@@ -1449,8 +1438,11 @@ __device__ __forceinline__ void ks_slab(const SlabItem& it, const MatDev& md, fl
   }
   bar_group(gi);
   {
-    float* qdst = Q + md.q_off + (long long)it.c0 * r;  // W = 1: q_w is the next warm start
-    for (int o = gtid; o < ncols * r; o += kThreads) qdst[o] = qs[o];
+    float* qdst = Q + md.q_off + it.c0;  // W = 1: q_w is the next warm start (column-major)
+    for (int o = gtid; o < ncols * r; o += kThreads) {
+      const int k = o / ncols, cc = o - k * ncols;
+      qdst[(long long)k * md.qld + cc] = qs[cc * r + k];
+    }
   }
   float qv[4][R];
 #pragma unroll
@@ -1506,11 +1498,11 @@ __global__ void __launch_bounds__(kCons, 1)
               int* __restrict__ status) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* sgb = reinterpret_cast<float*>(smem_raw);
-  float* seb = sgb + K1_STAGES * K1_STAGE_FLOATS;
+  float* seb = sgb + L.stages * L.stage_floats;
   float* qsl = reinterpret_cast<float*>(smem_raw + L.off_q);
   float* red = reinterpret_cast<float*>(smem_raw + L.off_red);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
-  uint64_t* qfull = full + K1_STAGES;
+  uint64_t* qfull = full + L.stages;
   __shared__ int s_flag;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int cb = k1_beg[blockIdx.x], ce = k1_beg[blockIdx.x + 1];
@@ -1525,7 +1517,7 @@ __global__ void __launch_bounds__(kCons, 1)
 
   // ------------------------------------------------ phase 1: delta = g + e, P = delta Q
   if (t == 0) {
-    for (int s = 0; s < K1_STAGES; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < L.stages; ++s) mbar_init(&full[s], 1);
     for (int s = 0; s < KS_QSLOTS; ++s) mbar_init(&qfull[s], 1);
     s_flag = 0;
     fence_mbar_init();
@@ -1542,21 +1534,21 @@ __global__ void __launch_bounds__(kCons, 1)
       p_cur = ch.mat;
       if (md.qs) {
         const int qsi = ++p_qseq % KS_QSLOTS;
-        const uint32_t qb = (uint32_t)((((long long)md.m * md.r + 3) & ~3LL) * 4);
+        const uint32_t qb = (uint32_t)((long long)md.r * md.qld * 4);
         mbar_expect_tx(&qfull[qsi], qb);
         tma_load(qsl + qsi * L.qslot_floats, Q + md.q_off, qb, &qfull[qsi], polq);
       }
     }
-    const int s = (k - cb) % K1_STAGES;
+    const int s = (k - cb) % L.stages;
     const long long a4 = ch.off & ~3LL;
     const long long span = (long long)(ch.nrows - 1) * md.m + ch.ncols;
     const uint32_t bytes = (uint32_t)((((ch.off + span + 3) & ~3LL) - a4) * 4);
     mbar_expect_tx(&full[s], 2 * bytes);
-    tma_load(sgb + s * K1_STAGE_FLOATS, g + a4, bytes, &full[s], pol);
-    tma_load(seb + s * K1_STAGE_FLOATS, e + a4, bytes, &full[s], pol);
+    tma_load(sgb + s * L.stage_floats, g + a4, bytes, &full[s], pol);
+    tma_load(seb + s * L.stage_floats, e + a4, bytes, &full[s], pol);
   };
   if (t == 0)
-    for (int k = cb; k < min(ce, cb + K1_STAGES); ++k) issue(k);
+    for (int k = cb; k < min(ce, cb + L.stages); ++k) issue(k);
   bool bad = false;
   for (long long x = (long long)blockIdx.x * kCons + t; x < nbias; x += (long long)grid * kCons) {
     const float v = bias_g[x];
@@ -1568,8 +1560,8 @@ __global__ void __launch_bounds__(kCons, 1)
     int cur = -1, mseq = -1, rpar = 0;
     MatDev md{};
     for (int k = cb; k < ce; ++k) {
-      const int s = (k - cb) % K1_STAGES;
-      const uint32_t ph = ((k - cb) / K1_STAGES) & 1;
+      const int s = (k - cb) % L.stages;
+      const uint32_t ph = ((k - cb) / L.stages) & 1;
       const Chunk1 ch = chunks[k];
       if (ch.mat != cur) {
         md = mats[ch.mat];
@@ -1583,13 +1575,13 @@ __global__ void __launch_bounds__(kCons, 1)
       float* rb = red + (rpar & 1) * (K1_RED_ROWS * kConsWarps * R + R);
       if ((1 << md.lg1) > 32) ++rpar;
       if (md.qs)
-        k1_chunk<R, true>(ch, md, qsl + (mseq % KS_QSLOTS) * L.qslot_floats, sgb + s * K1_STAGE_FLOATS,
-                          seb + s * K1_STAGE_FLOATS, true, work, P, splits, psplit, split_cnt, rb, keep, bad);
+        k1_chunk<R, true>(ch, md, qsl + (mseq % KS_QSLOTS) * L.qslot_floats, sgb + s * L.stage_floats,
+                          seb + s * L.stage_floats, true, work, P, splits, psplit, split_cnt, rb, keep, bad);
       else
-        k1_chunk<R, false>(ch, md, Q + md.q_off, sgb + s * K1_STAGE_FLOATS, seb + s * K1_STAGE_FLOATS, true,
+        k1_chunk<R, false>(ch, md, Q + md.q_off, sgb + s * L.stage_floats, seb + s * L.stage_floats, true,
                            work, P, splits, psplit, split_cnt, rb, keep, bad);
       __syncthreads();  // stage s (and, three matrices back, its Q slot) is free
-      if (t == 0 && k + K1_STAGES < ce) issue(k + K1_STAGES);
+      if (t == 0 && k + L.stages < ce) issue(k + L.stages);
     }
   }
   if (bad) atomicOr(&s_flag, 1);
@@ -1696,7 +1688,7 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
   const int m = md.m;
   const float* __restrict__ Q = qsrc + md.q_off;
   if (MODE == 1 && it.row0 == 0 && qstore != nullptr && qstore != qsrc) {
-    for (int x = lane; x < m * r; x += 32) {
+    for (int x = lane; x < md.qld * r; x += 32) {
       const float v = Q[x];
       qstore[md.q_off + x] = divisor == 1 ? v : v / (float)divisor;
     }
@@ -1724,7 +1716,7 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         if (EXACT || k < r) {
-          float qk = __ldg(Q + (long long)j * r + k);
+          float qk = __ldg(Q + (long long)k * md.qld + j);
           if (MODE == 1 && divisor != 1) qk = qk / (float)divisor;
           mh = fmaf(ph[k], qk, mh);
         }
@@ -1737,20 +1729,13 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
         st_stream(work + o + j, mh);
       }
     }
-    const float* __restrict__ qrow = Q + (long long)head * r;
-    const bool qal = ((head * r + (int)(md.q_off & 3)) & 3) == 0;
+    const float* __restrict__ qrow = Q + head;
+    const bool qal = (head & 3) == 0;
     float4* __restrict__ w4 = reinterpret_cast<float4*>(work + o + head);
     float4* __restrict__ e4 = reinterpret_cast<float4*>(e + o + head);
     for (int c = gl; c < body4; c += G) {
       float qv[4][R];
-      if (EXACT) {
-        load_q4<R>(qrow + (long long)(4 * c) * r, qal, R, qv);
-      } else {
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-          for (int k = 0; k < R; ++k) qv[jj][k] = k < r ? __ldg(qrow + (long long)(4 * c + jj) * r + k) : 0.f;
-      }
+      load_q4<R, false>(qrow + 4 * c, md.qld, qal, r, qv);
       float mh[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int k = 0; k < R; ++k) {
@@ -1995,16 +1980,17 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       return fail(PSGD_EINVAL, "effective rank " + std::to_string(md.r) + " exceeds PSGD_MAX_RANK");
     }
     md.tall = k3_tall_config(md.n, md.m, md.r).nchunks > 1;
-    md.lg1 = lanes_log2_for(md.m, 9);
+    md.lg1 = 5;  // set with the K1 chunk geometry below
     md.qs = 0;  // decided below, once the K1 smem budget is known
     md.gs1 = (PSGD_K1_GS && world == 1 && md.n <= 512 && md.r <= 4) ? 1 : 0;
     md.flat_off = fo;
     md.p_off = po;
     md.q_off = qo;
+    md.qld = (int)align4(md.m);
     md.repl_off = ro;
     fo = align4(fo + (long long)md.n * md.m);
     po = align4(po + (long long)md.n * md.r);
-    qo = align4(qo + (long long)md.m * md.r);
+    qo += (long long)md.r * md.qld;
     ro += (long long)md.n * md.r;
     pl->n_tall += md.tall;
     pl->rmax = std::max(pl->rmax, rmax_of(md.r));
@@ -2014,17 +2000,56 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   }
   pl->flat_elems = std::max(4LL, fo);
 
-  // ---- K1 chunks: row-aligned, <= K1_CHUNK floats; over-long rows split into segments
-  const int seg = K1_CHUNK;
+  // ---- K1 smem layout: Q slots for the matrices whose r x q_ld block fits, then
+  // the largest 2-stage ring of g / e chunks that fits beside them (227 KB)
+  {
+    K1Layout& L = pl->k1l;
+    const long long red_b = 2LL * (K1_RED_ROWS * kConsWarps * pl->rmax + pl->rmax) * 4;
+    const long long bar_b = (2 * K1_STAGES + 4) * 8 + 16;
+    const long long min_stage = 2LL * 2 * (K1_CHUNK + 8) * 4;  // 2 stages of the smallest chunk
+    const long long cap = std::min<long long>(K1_QSLOT_CAP, ((227LL * 1024 - min_stage - red_b - bar_b - 512) / 8) & ~3LL);
+    long long qslot = 4;
+    for (auto& md : pl->mats) {
+      md.qs = (long long)md.r * md.qld <= cap ? 1 : 0;
+      if (md.qs) qslot = std::max(qslot, (long long)md.r * md.qld);
+    }
+    L.qslot_floats = (int)qslot;
+    L.stages = 2;
+    const long long room = 227LL * 1024 - 2 * qslot * 4 - red_b - bar_b - 512;
+    L.stage_floats = (int)std::min<long long>(16384 + 8, (room / (2LL * L.stages * 4)) & ~3LL);
+    int off = 2 * L.stages * L.stage_floats * 4;
+    L.off_q = off;   off += 2 * L.qslot_floats * 4;
+    L.off_red = off; off += (int)red_b;
+    off = (off + 15) & ~15;
+    L.off_bar = off; off += (int)bar_b;
+    L.total = off;
+  }
+  // ---- K1 chunks: whole rows, <= stage_floats - 8 floats; 2^lg1 lanes per row so
+  // that a pass keeps all 16 consumer warps busy (rows <= 32 lanes need no barrier)
+  const int seg = pl->k1l.stage_floats - 8;
   for (int mi = 0; mi < nmat; ++mi) {
-    const MatDev& md = pl->mats[mi];
+    MatDev& md = pl->mats[mi];
     if (md.m <= seg) {
-      const int rows = std::max(1, seg / md.m);
+      const int rows_fit = seg / md.m;
+      int lg = 2;  // ~4 float4 per lane per row, 4..32 lanes
+      while ((1 << lg) < (md.m + 15) / 16 && lg < 5) ++lg;
+      int rows;
+      if (rows_fit >= (kCons >> lg)) {
+        rows = (rows_fit / (kCons >> lg)) * (kCons >> lg);
+      } else {  // fewer rows than a pass: multi-warp rows, one reduction barrier per chunk
+        int p2 = 1;
+        while (p2 * 2 <= rows_fit) p2 *= 2;
+        lg = 0;
+        while ((1 << lg) < kCons / p2) ++lg;
+        rows = p2;
+      }
+      md.lg1 = lg;
       for (int r0 = 0; r0 < md.n; r0 += rows) {
         const int nr = std::min(rows, md.n - r0);
         pl->k1.push_back({md.flat_off + (long long)r0 * md.m, mi, r0, nr, 0, md.m, -1, 0, 0});
       }
     } else {
+      md.lg1 = 9;
       const int parts = (md.m + seg - 1) / seg;
       const int slen = (int)align4((md.m + parts - 1) / parts);  // equal segments
       for (int row = 0; row < md.n; ++row) {
@@ -2046,25 +2071,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     pl->k1_beg = balance(w, pl->nsm);
   }
   pl->nflags = std::max(1, (int)pl->k1_beg.size() - 1);
-  {
-    K1Layout& L = pl->k1l;
-    // Q slots get what the stages and reduction buffers leave of 227 KB
-    const long long fixed = 2LL * K1_STAGES * K1_STAGE_FLOATS * 4 +
-                            2LL * (K1_RED_ROWS * kConsWarps * pl->rmax + pl->rmax) * 4 + 512;
-    const long long cap = std::min<long long>(K1_QSLOT_CAP, ((227LL * 1024 - fixed) / 8) & ~3LL);
-    long long qslot = 4;
-    for (auto& md : pl->mats) {
-      md.qs = align4((long long)md.m * md.r) <= cap ? 1 : 0;
-      if (md.qs) qslot = std::max(qslot, align4((long long)md.m * md.r));
-    }
-    L.qslot_floats = (int)qslot;
-    int off = 2 * K1_STAGES * K1_STAGE_FLOATS * 4;
-    L.off_q = off;   off += 2 * L.qslot_floats * 4;
-    L.off_red = off; off += 2 * (K1_RED_ROWS * kConsWarps * pl->rmax + pl->rmax) * 4;
-    off = (off + 15) & ~15;
-    L.off_bar = off; off += (2 * K1_STAGES + 4) * 8 + 16;
-    L.total = off;
-  }
   pl->p_bias_off = po;
   pl->flag_off = align4(po + nbias);
   pl->p_elems = pl->flag_off + align4(pl->nflags);
@@ -2146,11 +2152,13 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     ok = ok && r0 >= 1 && r0 <= 4 && (int)pl->k1_beg.size() - 1 <= pl->nsm;
     KsLayout& L = pl->ksl;
     L.qslot_floats = pl->k1l.qslot_floats;
-    int off = 2 * K1_STAGES * K1_STAGE_FLOATS * 4;
+    L.stages = pl->k1l.stages;
+    L.stage_floats = pl->k1l.stage_floats;
+    int off = 2 * L.stages * L.stage_floats * 4;
     L.off_q = off;   off += KS_QSLOTS * L.qslot_floats * 4;
     L.off_red = off; off += 2 * (K1_RED_ROWS * kConsWarps * std::max(r0, 1) + std::max(r0, 1)) * 4;
     off = (off + 15) & ~15;
-    L.off_bar = off; off += (K1_STAGES + KS_QSLOTS) * 8 + 16;
+    L.off_bar = off; off += (L.stages + KS_QSLOTS) * 8 + 16;
     L.total = off;
     ok = ok && L.total <= 227 * 1024;
     // each 256-thread group needs (512 + 1024 + 1024) * r floats of the stage area half
@@ -2322,6 +2330,7 @@ int psgd_plan_matrix(const psgd_plan* pl, int32_t i, psgd_matrix_info* o) {
   o->m = md.m;
   o->r_eff = md.r;
   o->tall = md.tall;
+  o->q_ld = md.qld;
   return PSGD_OK;
 }
 

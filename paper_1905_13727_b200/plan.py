@@ -89,8 +89,10 @@ class Plan:
         return p[mi.p_off: mi.p_off + mi.n * mi.r_eff].view(mi.n, mi.r_eff)
 
     def q_view(self, q, i):
+        """(m, r_eff) view of matrix i's Q; the packed block is column-major with
+        column stride q_ld (so K1 reads it without smem bank conflicts)."""
         mi = self.matrices[i]
-        return q[mi.q_off: mi.q_off + mi.m * mi.r_eff].view(mi.m, mi.r_eff)
+        return q[mi.q_off: mi.q_off + mi.r_eff * mi.q_ld].view(mi.r_eff, mi.q_ld)[:, :mi.m].t()
 
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:
