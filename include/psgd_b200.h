@@ -68,7 +68,7 @@ typedef struct {
     int32_t launches_q_ef;
     int32_t launches_decompress;
     int32_t launches_step_single; /* psgd_step_single: 1 when the fused single-kernel step applies */
-    int32_t fused_step;           /* 1: psgd_step_single runs k_step_w1 (one cooperative kernel) */
+    int32_t fused_step;           /* psgd_step_single runs one cooperative kernel: 2 = k_resident (delta on chip), 1 = k_step_w1 */
 } psgd_plan_info;
 
 typedef struct {
@@ -146,6 +146,18 @@ int psgd_step_single(const psgd_plan* plan, const float* g, float* e, float* wor
  * for the single-GPU W-list mode: out = tree_sum(bufs[0..nbuf)) / nbuf, in the
  * reference's pairing order.  bufs is a HOST array of device pointers. */
 int psgd_tree_mean(const float* const* bufs, int32_t nbuf, int64_t count, float* out, void* stream);
+
+/* Diagnostics: with PSGD_RES_TIMING=1 set when the plan was created, copies 8
+ * globaltimer stamps per CTA of the last resident step (start, end of phase 1,
+ * end of the reductions / Gram-Schmidt, after the grid barrier, end); returns
+ * the number of values copied (0 when the plan has no resident step). */
+int psgd_debug_resident_times(const psgd_plan* plan, int64_t* out, int64_t cap);
+
+/* Host-only check of the on-chip-resident step's partition for a catalog (no GPU
+ * needed): returns 1 and stats = {CTAs, slabs, max/avg CTA load, max slots used,
+ * slot capacity}, or 0 and the reason in `why`. */
+int psgd_resident_dryrun(int32_t nmat, const int64_t* n, const int64_t* m, int32_t rank, int32_t nsm,
+                         double* stats, char* why, int32_t why_cap);
 
 const char* psgd_last_error(void);
 int32_t psgd_version(void);

@@ -8,14 +8,16 @@ import shutil
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = os.path.join(HERE, "csrc", "psgd_b200.cu")
+CSRC = os.path.join(HERE, "csrc")
+SOURCES = [os.path.join(CSRC, f) for f in ("psgd_b200.cu", "psgd_resident.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in ("common.cuh", "resident.h")]
 LIB = os.path.join(HERE, "libpsgd_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "--expt-relaxed-constexpr",
 ]
 
@@ -31,26 +33,41 @@ def stale():
     if not os.path.exists(LIB):
         return True
     mt = os.path.getmtime(LIB)
-    deps = [SRC, os.path.join(INCLUDE, "psgd_b200.h")]
+    deps = SOURCES + HEADERS + [os.path.join(INCLUDE, "psgd_b200.h")]
     return any(os.path.getmtime(d) > mt for d in deps if os.path.exists(d))
 
 
 def build(force=False, verbose=False, out=None, defines=()):
-    """Compile csrc/psgd_b200.cu -> libpsgd_b200.so (sm_100a).  Returns the path.
+    """Compile csrc/*.cu -> libpsgd_b200.so (sm_100a).  Returns the path.
     `out` / `defines` build experiment variants (e.g. PSGD_PDL=0) beside it."""
     lib = out or LIB
     if not force and out is None and not stale():
         return LIB
     tmp = lib + ".tmp"
-    cmd = [nvcc_path(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-o", tmp, SRC]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    nvcc = nvcc_path()
+    objs, procs = [], []
+    for src in SOURCES:  # translation units compile in parallel
+        obj = f"{lib}.{os.path.basename(src)}.o"
+        cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        objs.append(obj)
+        procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    errs = []
+    for p in procs:
+        _, err = p.communicate()
+        if p.returncode != 0:
+            errs.append(f"nvcc failed ({p.returncode}):\n{err[-4000:]}")
+        elif verbose:
+            print(err)
+    if errs:
+        raise RuntimeError("\n".join(errs))
+    res = subprocess.run([nvcc, "-shared", "-o", tmp, *objs, "-lcuda"], capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
+        raise RuntimeError(f"link failed ({res.returncode}):\n{res.stderr[-4000:]}")
+    for o in objs:
+        os.remove(o)
     os.replace(tmp, lib)
-    if verbose:
-        print(res.stderr)
     return lib
 
 

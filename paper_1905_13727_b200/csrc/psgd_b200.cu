@@ -29,6 +29,8 @@
 // All reductions are fixed-order: results are bitwise run-to-run stable.
 
 #include "../../include/psgd_b200.h"
+#include "common.cuh"
+#include "resident.h"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -44,6 +46,8 @@
 #include <vector>
 
 namespace {
+
+using namespace psgd;
 
 constexpr int kThreads = 256;      // plain CTA size (8 warps)
 constexpr int kCons = 512;         // consumer threads of the TMA kernels (16 warps)
@@ -217,9 +221,6 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
 
-__device__ __forceinline__ bool finite1(float x) {
-  return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
-}
 __device__ __forceinline__ bool finite4(float4 v) {
   return finite1(v.x) & finite1(v.y) & finite1(v.z) & finite1(v.w);
 }
@@ -358,111 +359,6 @@ struct WarpReducer {  // one warp, shuffles only
     return v;
   }
 };
-
-// ---- register-resident warp MGS (n <= 32 * RPL, r == R <= 4): each lane
-// owns rows lane + 32 k; dot products are RPL fused multiply-adds plus one
-// shuffle reduction, so the whole orthogonalisation of a 512 x 2 P is ~1 us.
-// Same sequence, threshold and replacement rule as mgs_inplace (linalg.py:61-90).
-template <int RPL, int R>
-__device__ __forceinline__ void warp_mgs_reg(const float* __restrict__ P, int n, double inv_div,
-                                             const double* __restrict__ repl, float* __restrict__ out,
-                                             int* status) {
-  const int lane = threadIdx.x & 31;
-  double x[R][RPL];
-  bool bad = false;
-#pragma unroll
-  for (int k = 0; k < RPL; ++k) {
-    const int i = lane + 32 * k;
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const float v = i < n ? __ldcg(P + i * R + j) : 0.f;
-      bad |= !finite1(v);
-      x[j][k] = (double)v * inv_div;
-    }
-  }
-  if (__any_sync(0xffffffffu, bad)) {  // linalg.py:35-36 (ContractViolation)
-    if (lane == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
-    return;
-  }
-  auto wsum = [](double v) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    return v;
-  };
-#pragma unroll
-  for (int j = 0; j < R; ++j) {
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
-    double before = sqrt(wsum(s));
-    double nrm = before;
-    for (int attempt = 0;; ++attempt) {
-      if (attempt == 1 || j > 0) {
-#pragma unroll
-        for (int i2 = 0; i2 < j; ++i2) {
-          double d = 0.0;
-#pragma unroll
-          for (int k = 0; k < RPL; ++k) d = fma(x[i2][k], x[j][k], d);
-          const double c = wsum(d);
-#pragma unroll
-          for (int k = 0; k < RPL; ++k) x[j][k] -= c * x[i2][k];
-        }
-        s = 0.0;
-#pragma unroll
-        for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
-        nrm = sqrt(wsum(s));
-      }
-      if (!(nrm < 1e-12 * (before + 1.0))) break;
-      if (attempt == 1) {  // the table holds attempt 0 only
-        if (lane == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
-        break;
-      }
-#pragma unroll
-      for (int k = 0; k < RPL; ++k) {
-        const int i = lane + 32 * k;
-        x[j][k] = i < n ? repl[(long long)j * n + i] : 0.0;
-      }
-      before = 1.0;
-    }
-    const double inv = 1.0 / nrm;
-#pragma unroll
-    for (int k = 0; k < RPL; ++k) x[j][k] *= inv;
-  }
-#pragma unroll
-  for (int k = 0; k < RPL; ++k) {
-    const int i = lane + 32 * k;
-    if (i < n)
-#pragma unroll
-      for (int j = 0; j < R; ++j) out[i * R + j] = (float)x[j][k];
-  }
-}
-
-template <int R>
-__device__ __forceinline__ bool warp_mgs_dispatch_r(int rpl_log2, const float* P, int n, double inv_div,
-                                                    const double* repl, float* out, int* status) {
-  switch (rpl_log2) {
-    case 0: warp_mgs_reg<1, R>(P, n, inv_div, repl, out, status); return true;
-    case 1: warp_mgs_reg<2, R>(P, n, inv_div, repl, out, status); return true;
-    case 2: warp_mgs_reg<4, R>(P, n, inv_div, repl, out, status); return true;
-    case 3: warp_mgs_reg<8, R>(P, n, inv_div, repl, out, status); return true;
-    case 4: warp_mgs_reg<16, R>(P, n, inv_div, repl, out, status); return true;
-    default: return false;
-  }
-}
-
-// P-hat of one matrix by one warp when n <= 512 and r <= 4; false otherwise
-__device__ __forceinline__ bool warp_mgs(const float* P, int n, int r, double inv_div, const double* repl,
-                                         float* out, int* status) {
-  if (n > 512 || r > 4) return false;
-  int l = 0;
-  while ((32 << l) < n) ++l;
-  switch (r) {
-    case 1: return warp_mgs_dispatch_r<1>(l, P, n, inv_div, repl, out, status);
-    case 2: return warp_mgs_dispatch_r<2>(l, P, n, inv_div, repl, out, status);
-    case 3: return warp_mgs_dispatch_r<3>(l, P, n, inv_div, repl, out, status);
-    default: return warp_mgs_dispatch_r<4>(l, P, n, inv_div, repl, out, status);
-  }
-}
 
 // ============================================================================= K1
 // delta = g + e ; P[i,:] = sum_j delta[i,j] Q[j,:]   (optimizer.py:120, compressors.py:336)
@@ -1859,6 +1755,9 @@ struct psgd_plan {
   double* d_gsws = nullptr;
   float* d_wsq = nullptr;
   int* d_counters = nullptr;
+  // on-chip-resident W = 1 step (psgd_resident.cu); nullptr when not eligible
+  psgd::ResPlan* res = nullptr;
+  std::string res_why;
 };
 
 namespace {
@@ -2274,6 +2173,11 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     delete pl;
     return fail(PSGD_ECUDA, std::string("plan upload: ") + cudaGetErrorString(ce));
   }
+  if (world == 1) {  // delta held in TMEM + smem across the step when it fits (ResNet-18 class)
+    std::vector<psgd::ResMatIn> rin;
+    for (auto& md : pl->mats) rin.push_back({md.flat_off, md.p_off, md.q_off, md.repl_off, md.n, md.m, md.r, md.qld});
+    pl->res = psgd::res_plan_create(rin.data(), nmat, nbias, pl->nsm, &pl->res_why);
+  }
   *out = pl;
   return PSGD_OK;
 }
@@ -2281,6 +2185,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
 int psgd_plan_destroy(psgd_plan* plan) {
   if (!plan) return PSGD_OK;
   if (plan->dev_block) cudaFree(plan->dev_block);
+  psgd::res_plan_destroy(plan->res);
   delete plan;
   return PSGD_OK;
 }
@@ -2313,8 +2218,8 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
   const bool fused_step = pl->ks_ok && !psgd_force_multi();
-  o->launches_step_single = fused_step ? 1 : o->launches_ef_p + o->launches_q_ef;
-  o->fused_step = fused_step ? 1 : 0;
+  o->launches_step_single = (pl->res || fused_step) ? 1 : o->launches_ef_p + o->launches_q_ef;
+  o->fused_step = pl->res ? 2 : fused_step ? 1 : 0;
   return PSGD_OK;
 }
 
@@ -2580,12 +2485,43 @@ int psgd_step_single(const psgd_plan* pl, const float* g, float* e, float* work,
   if (!pl) return fail(PSGD_EINVAL, "NULL plan");
   if (pl->world != 1) return fail(PSGD_EINVAL, "psgd_step_single needs a world-1 plan");
   if (!status) return fail(PSGD_EINVAL, "NULL status");
+  if (pl->res && e != nullptr) {
+    if (!g || !work || !q || !p || !p_hat || !repl || (pl->nbias > 0 && (!bias_g || !bias_out)))
+      return fail(PSGD_EINVAL, "psgd_step_single: NULL argument");
+    PSGD_CUDA_CHECK(psgd::res_step(pl->res, g, e, work, q, p, p_hat, repl, bias_g, bias_out, (int*)status,
+                                   static_cast<cudaStream_t>(stream)));
+    return PSGD_OK;
+  }
   if (pl->ks_ok && e != nullptr && !psgd_force_multi()) return run_ks(pl, g, e, work, q, p, p_hat, bias_g, repl,
                                                                       bias_out, (int*)status,
                                                                       static_cast<cudaStream_t>(stream));
   int rc = psgd_ef_p(pl, g, e, work, q, p, p_hat, repl, bias_g, status, stream);
   if (!rc) rc = psgd_q_ef(pl, work, p, 1, repl, p_hat, q, e, bias_out, status, stream);
   return rc;
+}
+
+int psgd_resident_dryrun(int32_t nmat, const int64_t* n, const int64_t* m, int32_t rank, int32_t nsm,
+                         double* stats, char* why, int32_t why_cap) {
+  if (nmat < 0 || (nmat > 0 && (!n || !m)) || !stats || rank < 1) return fail(PSGD_EINVAL, "bad argument");
+  std::vector<psgd::ResMatIn> rin;
+  long long fo = 0;
+  for (int i = 0; i < nmat; ++i) {
+    const int r = (int)std::min<long long>(std::min<long long>(n[i], m[i]), rank);
+    rin.push_back({fo, 0, 0, 0, (int)n[i], (int)m[i], r, (int)align4(m[i])});
+    fo = align4(fo + n[i] * m[i]);
+  }
+  std::string w;
+  const int ok = psgd::res_dryrun(rin.data(), nmat, nsm, stats, &w);
+  if (why && why_cap > 0) {
+    strncpy(why, w.c_str(), why_cap - 1);
+    why[why_cap - 1] = 0;
+  }
+  return ok;
+}
+
+int psgd_debug_resident_times(const psgd_plan* pl, int64_t* out, int64_t cap) {
+  if (!pl || !out) return fail(PSGD_EINVAL, "NULL argument");
+  return psgd::res_debug_times(pl->res, reinterpret_cast<long long*>(out), cap);
 }
 
 int psgd_tree_mean(const float* const* bufs, int32_t nbuf, int64_t count, float* out, void* stream) {
