@@ -147,6 +147,14 @@ int psgd_step_single(const psgd_plan* plan, const float* g, float* e, float* wor
  * reference's pairing order.  bufs is a HOST array of device pointers. */
 int psgd_tree_mean(const float* const* bufs, int32_t nbuf, int64_t count, float* out, void* stream);
 
+/* Heavy-ball update of every parameter in one pass (optimizer.py:131-134,
+ * reference_momentum_step :163-171): m = momentum * m + u ; x -= lr * (u + m),
+ * u = M-hat in the plan's flat layout (`work` after a step) and the bias mean.
+ * params / mom use the same flat layout (flat_elems floats) and bias layout. */
+int psgd_momentum_step(const psgd_plan* plan, float* params, float* mom, const float* update,
+                       float* bias_params, float* bias_mom, const float* bias_update, float lr,
+                       float momentum, const int32_t* status, void* stream);
+
 /* Diagnostics: with PSGD_RES_TIMING=1 set when the plan was created, copies 8
  * globaltimer stamps per CTA of the last resident step (start, end of phase 1,
  * end of the reductions / Gram-Schmidt, after the grid barrier, end); returns

@@ -27,7 +27,7 @@ MAX_TREE = 64
 EXPORTS = (
     "psgd_plan_create", "psgd_plan_destroy", "psgd_plan_get_info", "psgd_plan_matrix",
     "psgd_ef_p", "psgd_orthogonalize", "psgd_q_ef", "psgd_decompress", "psgd_step_single",
-    "psgd_tree_mean", "psgd_debug_resident_times", "psgd_resident_dryrun", "psgd_last_error", "psgd_version",
+    "psgd_tree_mean", "psgd_momentum_step", "psgd_debug_resident_times", "psgd_resident_dryrun", "psgd_last_error", "psgd_version",
 )
 
 
@@ -69,6 +69,7 @@ _SIGNATURES = {
     "psgd_decompress": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P]),
     "psgd_step_single": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psgd_tree_mean": (_I32, [ctypes.POINTER(_P), _I32, _I64, _P, _P]),
+    "psgd_momentum_step": (_I32, [_P, _P, _P, _P, _P, _P, _P, ctypes.c_float, ctypes.c_float, _P, _P]),
     "psgd_debug_resident_times": (_I32, [_P, ctypes.POINTER(_I64), _I64]),
     "psgd_resident_dryrun": (_I32, [_I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64), _I32, _I32,
                                     ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, _I32]),

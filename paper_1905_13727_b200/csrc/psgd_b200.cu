@@ -1674,6 +1674,33 @@ __global__ void k_tree_mean(TreeArgs a, int nbuf, long long count, float* __rest
   }
 }
 
+// ============================================================================= optimizer
+// optimizer.py:131-134 for every parameter in one pass over the packed buffers:
+// m = momentum * m + u ; x -= lr * (u + m).  u is M-hat (work) / the bias mean.
+// 20 B per element (read u, m, x; write m, x), HBM-bound, float4 streaming.
+__global__ void __launch_bounds__(256) k_momentum(float* __restrict__ x, float* __restrict__ mom,
+                                                  const float* __restrict__ u, long long n4, float lr,
+                                                  float momentum, float* __restrict__ bx, float* __restrict__ bm,
+                                                  const float* __restrict__ bu, long long nb) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 uu = __ldcs(reinterpret_cast<const float4*>(u) + i);
+    float4 mm = __ldcs(reinterpret_cast<const float4*>(mom) + i);
+    float4 xx = __ldcs(reinterpret_cast<const float4*>(x) + i);
+    mm.x = fmaf(momentum, mm.x, uu.x); mm.y = fmaf(momentum, mm.y, uu.y);
+    mm.z = fmaf(momentum, mm.z, uu.z); mm.w = fmaf(momentum, mm.w, uu.w);
+    xx.x -= lr * (uu.x + mm.x); xx.y -= lr * (uu.y + mm.y);
+    xx.z -= lr * (uu.z + mm.z); xx.w -= lr * (uu.w + mm.w);
+    __stcs(reinterpret_cast<float4*>(mom) + i, mm);
+    __stcs(reinterpret_cast<float4*>(x) + i, xx);
+  }
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += stride) {
+    const float m2 = fmaf(momentum, bm[i], bu[i]);
+    bm[i] = m2;
+    bx[i] -= lr * (bu[i] + m2);
+  }
+}
+
 // ============================================================================= dispatch helpers
 
 template <template <int, bool> class F, typename... A>
@@ -2522,6 +2549,23 @@ int psgd_resident_dryrun(int32_t nmat, const int64_t* n, const int64_t* m, int32
 int psgd_debug_resident_times(const psgd_plan* pl, int64_t* out, int64_t cap) {
   if (!pl || !out) return fail(PSGD_EINVAL, "NULL argument");
   return psgd::res_debug_times(pl->res, reinterpret_cast<long long*>(out), cap);
+}
+
+int psgd_momentum_step(const psgd_plan* pl, float* params, float* mom, const float* update, float* bias_params,
+                       float* bias_mom, const float* bias_update, float lr, float momentum, const int32_t* status,
+                       void* stream) {
+  if (!pl || (pl->nmat > 0 && (!params || !mom || !update)) ||
+      (pl->nbias > 0 && (!bias_params || !bias_mom || !bias_update)))
+    return fail(PSGD_EINVAL, "psgd_momentum_step: NULL argument");
+  (void)status;
+  const long long n4 = pl->nmat > 0 ? pl->flat_elems / 4 : 0;
+  const long long work = std::max(n4, (long long)pl->nbias);
+  if (work == 0) return PSGD_OK;
+  const int blocks = (int)std::min<long long>((work + 255) / 256, (long long)pl->nsm * 8);
+  k_momentum<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(params, mom, update, n4, lr, momentum, bias_params,
+                                                                     bias_mom, bias_update, pl->nbias);
+  PSGD_CUDA_CHECK(cudaGetLastError());
+  return PSGD_OK;
 }
 
 int psgd_tree_mean(const float* const* bufs, int32_t nbuf, int64_t count, float* out, void* stream) {

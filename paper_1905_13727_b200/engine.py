@@ -187,6 +187,42 @@ class PowerSGDEngine:
     def _scratch_e(self):
         return self._e_scratch
 
+    # ------------------------------------------------------------------ optimizer (optimizer.py:131-134)
+    def attach_optimizer(self, lr, momentum, params=None):
+        """Heavy-ball state on the device, in the plan's packed layout: parameters
+        x and momentum buffers m (Optimizer.params / momentum_buffers,
+        optimizer.py:47-55).  `params`: initial values in catalog order."""
+        z = dict(dtype=torch.float32, device=self.device)
+        self.lr, self.momentum = float(lr), float(momentum)
+        self.params = torch.zeros(self.plan.flat_elems, **z)
+        self.mom = torch.zeros(self.plan.flat_elems, **z)
+        self.bias_params = torch.zeros(max(1, self.nbias), **z)
+        self.bias_mom = torch.zeros(max(1, self.nbias), **z)
+        if params is not None:
+            for i, p in enumerate(params):
+                self.param_view(i).copy_(torch.as_tensor(p, dtype=torch.float32).reshape(self.specs[i].shape))
+
+    def _flat_view(self, flat, bias_flat, param_index):
+        s = self.specs[param_index]
+        if s.is_bias:
+            o = self.bias_off[param_index]
+            return bias_flat[o:o + s.size]
+        return self.plan.matrix_view(flat, self.slot[param_index]).view(s.shape)
+
+    def param_view(self, param_index):
+        return self._flat_view(self.params, self.bias_params, param_index)
+
+    def momentum_view(self, param_index):
+        return self._flat_view(self.mom, self.bias_mom, param_index)
+
+    def optimizer_step(self, stream=None):
+        """m = momentum m + u ; x -= lr (u + m) for every parameter, one kernel,
+        with u = the aggregated update of the last step (M-hat, bias mean)."""
+        _lib.check(_lib.lib().psgd_momentum_step(
+            self.plan.handle, ptr(self.params), ptr(self.mom), ptr(self.work[0]), ptr(self.bias_params),
+            ptr(self.bias_mom), ptr(self.bias_out), self.lr, self.momentum, ptr(self.status),
+            stream_ptr(stream)), "psgd_momentum_step")
+
     def run(self, stream=None):
         """Enqueue one step on `stream` (default: current) without synchronising."""
         if self._graph is not None:
