@@ -161,6 +161,10 @@ class CompressionContext:
     def param_rng(self, label):
         return derive_rng(self.shared_seed, label, self.param_index)
 
+    def rng(self, label):
+        """compressors.py:38-40: stream tied to (seed, label, parameter, step)."""
+        return derive_rng(self.shared_seed, label, self.param_index, self.step)
+
 
 @dataclass
 class LowRank:
@@ -234,6 +238,91 @@ class PowerSGD:
     def compress_cost(self, n, m):
         r = self.effective_rank(n, m)
         return 4 * n * m * r + orthogonalize_flops(n, r)
+
+
+@dataclass
+class RandomProjection:
+    """compressors.py:70-78: proj = M u; u is seed-derived and costs no bits."""
+    proj: np.ndarray
+    u: np.ndarray
+
+    def bits(self):
+        return FLOAT_BITS * self.proj.size
+
+
+class BestApproximation:
+    """compressors.py:400-438: four fresh subspace iterations per call, no state."""
+
+    name = "bestapprox"
+    linear = True
+    route = "allreduce"
+    uses_error_feedback = True
+    iterations = 4
+
+    def __init__(self, rank=1):
+        if rank < 1:
+            raise ContractViolation(f"rank must be >= 1, got {rank}")
+        self.rank = rank
+
+    def round_trip(self, mats, ctx, comm):
+        """compressors.py:407-420."""
+        n, m = mats[0].shape
+        comm.stats.compress_flops += len(mats) * self.compress_cost(n, m)
+        rank = min(n, m, self.rank)
+        q = ctx.rng("fresh_start").standard_normal((m, rank))
+        payload, qs = None, None
+        for _ in range(self.iterations):
+            payload, qs = low_rank_iteration(mats, q, comm)
+            q = payload.q
+        comm.stats.decode_ops += 2 * n * m * payload.p.shape[1]
+        return RoundTrip(payload.p @ payload.q.T, [payload.p @ qw.T for qw in qs], payload)
+
+    def compress(self, m, ctx):
+        return self.round_trip([m], ctx, Communicator(1)).payload
+
+    def payload_bits(self, n, m):
+        return self.iterations * FLOAT_BITS * min(n, m, self.rank) * (n + m)
+
+    def compress_cost(self, n, m):
+        r = min(n, m, self.rank)
+        return self.iterations * (4 * n * m * r + orthogonalize_flops(n, r))
+
+
+class UnbiasedRankK:
+    """compressors.py:444-468 with the ReduceCompressor round trip (:255-269):
+    proj_w = M_w u, u ~ N(0, 1/r) from the shared stream; aggregate mean(proj) u^T."""
+
+    name = "unbiased"
+    linear = True
+    route = "allreduce"
+    uses_error_feedback = True
+
+    def __init__(self, rank=1):
+        if rank < 1:
+            raise ContractViolation(f"rank must be >= 1, got {rank}")
+        self.rank = rank
+
+    def compress(self, m, ctx):
+        rows, cols = m.shape
+        rank = min(rows, cols, self.rank)
+        u = ctx.rng("projection").standard_normal((cols, rank)) / np.sqrt(rank)
+        return RandomProjection(m @ u, u)
+
+    def round_trip(self, mats, ctx, comm):
+        n, m = mats[0].shape
+        comm.stats.compress_flops += len(mats) * self.compress_cost(n, m)
+        payloads = [self.compress(w, ctx) for w in mats]
+        reduced = comm.all_reduce_mean([p.proj for p in payloads], payload_bits=self.payload_bits(n, m))
+        combined = RandomProjection(reduced, payloads[0].u)
+        comm.stats.decode_ops += 2 * n * m * combined.u.shape[1]   # decode_cost :183-185
+        return RoundTrip(combined.proj @ combined.u.T, [p.proj @ p.u.T for p in payloads], combined)
+
+    def payload_bits(self, n, m):
+        return FLOAT_BITS * min(n, m, self.rank) * n
+
+    def compress_cost(self, n, m):
+        rank = min(n, m, self.rank)
+        return 2 * n * m * rank + m * rank
 
 
 # --------------------------------------------------------------------------- catalogs

@@ -9,8 +9,9 @@ loaded on first use and its absence is an error, never a fallback.
 
 from .catalogs import LSTM, RESNET18, ModelCatalog, ParamSpec, get_catalog, stress  # noqa: F401
 from .comm import CommStats, Communicator, DistributedCommunicator  # noqa: F401
-from .compressor import (COMPRESSORS, CompressionContext, Compressor, LowRank,  # noqa: F401
-                         PowerSGD, RoundTrip, decode_cost, decompress, make_compressor)
+from .compressor import (COMPRESSORS, BestApproximation, CompressionContext, Compressor,  # noqa: F401
+                         LowRank, PowerSGD, RandomProjection, RoundTrip, UnbiasedRankK, decode_cost,
+                         decompress, make_compressor)
 from .engine import NonFiniteGradient, PowerSGDEngine  # noqa: F401
 from .linalg import ContractViolation, orthogonalize  # noqa: F401
 from .seeding import derive_rng  # noqa: F401

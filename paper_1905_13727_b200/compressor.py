@@ -88,15 +88,31 @@ def _plan(n, m, rank, world, device):
     return pl
 
 
+@dataclass
+class RandomProjection:
+    """proj = M @ u for a seed-derived u; u costs no bits (compressors.py:70-78)."""
+
+    proj: object  # n x r
+    u: object     # m x r
+
+    def bits(self):
+        return FLOAT_BITS * _numel(self.proj)
+
+
 def decompress(payload, device=None):
-    """compressors.py:156-173 for the low-rank payload: p @ q.T in the K5 kernel."""
-    if not isinstance(payload, LowRank):
+    """compressors.py:156-173 for the low-rank payloads: p @ q.T (LowRank) or
+    proj @ u.T (RandomProjection), in the K5 kernel."""
+    if isinstance(payload, LowRank):
+        pp, qq = payload.p, payload.q
+    elif isinstance(payload, RandomProjection):
+        pp, qq = payload.proj, payload.u
+    else:
         raise TypeError(f"unknown payload type: {type(payload).__name__}")
-    as_np = not isinstance(payload.p, torch.Tensor)
+    as_np = not isinstance(pp, torch.Tensor)
     dev = torch.device(device) if device is not None else (
-        payload.p.device if not as_np else torch.device("cuda", torch.cuda.current_device()))
-    p = _to_dev(payload.p, dev)
-    q = _to_dev(payload.q, dev)
+        pp.device if not as_np else torch.device("cuda", torch.cuda.current_device()))
+    p = _to_dev(pp, dev)
+    q = _to_dev(qq, dev)
     n, r = p.shape
     m = q.shape[0]
     pl = _plan(n, m, r, 1, dev)
@@ -113,11 +129,14 @@ def decompress(payload, device=None):
 
 
 def decode_cost(payload):
-    """compressors.py:176-182 (low-rank payload)."""
-    if not isinstance(payload, LowRank):
-        raise TypeError(f"unknown payload type: {type(payload).__name__}")
-    n, r = tuple(payload.p.shape)
-    return 2 * n * int(payload.q.shape[0]) * r
+    """compressors.py:176-185 (low-rank payloads)."""
+    if isinstance(payload, LowRank):
+        n, r = tuple(payload.p.shape)
+        return 2 * n * int(payload.q.shape[0]) * r
+    if isinstance(payload, RandomProjection):
+        n, r = tuple(payload.proj.shape)
+        return 2 * n * int(payload.u.shape[0]) * r
+    raise TypeError(f"unknown payload type: {type(payload).__name__}")
 
 
 class Compressor:
@@ -281,11 +300,217 @@ class PowerSGD(Compressor):
         return 4 * n * m * r + 2 * n * r * r + 3 * n * r
 
 
-COMPRESSORS = {PowerSGD.name: PowerSGD}
+# --------------------------------------------------------------------------- siblings on the same kernels
+
+def _device_of(mats, device):
+    if device is not None:
+        return torch.device(device)
+    if isinstance(mats[0], torch.Tensor):
+        return mats[0].device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _check_mats(mats, comm):
+    if len(mats) == 0:
+        raise ValueError("round_trip needs at least one worker matrix")
+    dist = bool(getattr(comm, "distributed", False))
+    if not dist and len(mats) != comm.world_size:
+        raise ValueError(f"expected {comm.world_size} entries, got {len(mats)}")
+    if dist and len(mats) != 1:
+        raise ValueError("a distributed worker passes its own matrix only")
+    return dist
+
+
+class _Rounds:
+    """low_rank_iteration (compressors.py:327-341) on the device for W worker
+    matrices, as many rounds as asked.  The plan has exchange semantics (K3 writes
+    q_w and e, never M-hat), so delta survives every round."""
+
+    def __init__(self, ds, comm, rank, dev):
+        n, m = ds[0].shape
+        self.n, self.m, self.dev, self.comm = n, m, dev, comm
+        self.dist = bool(getattr(comm, "distributed", False))
+        self.world = comm.world_size
+        self.pl = pl = _plan(n, m, rank, max(2, self.world), dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.f32 = f32
+        self.works = []
+        for d in ds:
+            w = torch.zeros(pl.flat_elems, **f32)
+            pl.matrix_view(w, 0).copy_(d)
+            self.works.append(w)
+        self.scratch = torch.empty(pl.flat_elems, **f32)
+        self.escratch = torch.empty(pl.flat_elems, **f32)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.repl = pl.repl_table()
+        self.phat = torch.zeros(pl.p_elems, **f32)
+        self.r = min(n, m, rank)
+
+    def products(self, q):
+        """p_w = M_w q for every worker (K1 with no EF add)."""
+        pl, lib, sp = self.pl, _lib.lib(), stream_ptr()
+        q_in = torch.zeros(pl.q_elems, **self.f32)
+        pl.q_view(q_in, 0).copy_(q)
+        ps = []
+        for w in self.works:
+            p = torch.zeros(pl.p_elems, **self.f32)
+            _lib.check(lib.psgd_ef_p(pl.handle, ptr(w), None, ptr(self.scratch), ptr(q_in), ptr(p), ptr(self.phat),
+                                     ptr(self.repl), None, ptr(self.status), sp), "psgd_ef_p")
+            ps.append(p)
+        return ps
+
+    def mean(self, bufs, bits):
+        """all_reduce_mean (comm.py:84-98): (buffer, divisor still to apply)."""
+        if self.world == 1:
+            return bufs[0], 1
+        self.comm.charge_allreduce(bits)
+        if self.dist:
+            self.comm.all_reduce_sum_(bufs[0])
+            return bufs[0], self.world
+        out = torch.empty_like(bufs[0])
+        tree_mean_(bufs, out)
+        return out, 1
+
+    def iterate(self, q):
+        pl, lib, sp = self.pl, _lib.lib(), stream_ptr()
+        pm, div = self.mean(self.products(q), FLOAT_BITS * self.n * self.r)
+        qws = []
+        for w in self.works:  # P-hat = MGS(P / div), q_w = M_w^T P-hat
+            qw = torch.zeros(pl.q_elems, **self.f32)
+            _lib.check(lib.psgd_q_ef(pl.handle, ptr(w), ptr(pm), div, ptr(self.repl), ptr(self.phat), ptr(qw),
+                                     ptr(self.escratch), None, ptr(self.status), sp), "psgd_q_ef")
+            qws.append(qw)
+        qs = [q.clone() for q in qws] if self.dist else qws
+        qbar, qdiv = self.mean(qs, FLOAT_BITS * self.m * self.r)
+        if qdiv != 1:
+            qbar = qbar / qdiv
+        return qbar, qws
+
+    def outer(self, p, q):
+        """p q^T (K5), p in the P layout and q in the Q layout of the plan."""
+        pl, lib, sp = self.pl, _lib.lib(), stream_ptr()
+        out = torch.empty(pl.flat_elems, **self.f32)
+        _lib.check(lib.psgd_decompress(pl.handle, ptr(p), ptr(q), 1, None, ptr(out), ptr(self.status), sp),
+                   "psgd_decompress")
+        return pl.matrix_view(out, 0).clone()
+
+    def check(self):
+        st = int(self.status.item())
+        if st & (_lib.STATUS_NONFINITE_GRAD | _lib.STATUS_NONFINITE_P):
+            raise ContractViolation("orthogonalize input contains non-finite entries")
+        if st & _lib.STATUS_REPLACEMENT:
+            raise RuntimeError("Gram-Schmidt needed more than one replacement draw")
+
+
+class BestApproximation(Compressor):
+    """Near-optimal rank-r reference: four fresh subspace iterations per call,
+    no state reuse (compressors.py:400-438), on K1 / K2+K3 / K5."""
+
+    name = "bestapprox"
+    linear = True
+    route = "allreduce"
+    uses_error_feedback = True
+    iterations = 4
+
+    def __init__(self, rank=1, device=None):
+        super().__init__(rank)
+        self.device = device
+
+    def round_trip(self, mats, ctx, comm):
+        """compressors.py:407-420."""
+        _check_mats(mats, comm)
+        as_np = not isinstance(mats[0], torch.Tensor)
+        dev = _device_of(mats, self.device)
+        ds = [_to_dev(x, dev) for x in mats]
+        n, m = ds[0].shape
+        self._charge_compress(comm, n, m, len(ds))
+        rank = min(n, m, self.rank)
+        q = _to_dev(ctx.rng("fresh_start").standard_normal((m, rank)), dev)
+        with torch.cuda.device(dev):
+            R = _Rounds(ds, comm, self.rank, dev)
+            for _ in range(self.iterations):
+                qbar, qws = R.iterate(q)
+                q = R.pl.q_view(qbar, 0).contiguous()
+            comm.stats.decode_ops += 2 * n * m * rank
+            agg = R.outer(R.phat, qbar)
+            locs = [R.outer(R.phat, qw) for qw in qws]
+            R.check()
+        payload = LowRank(_out(R.pl.p_view(R.phat, 0).clone(), as_np), _out(q, as_np))
+        return RoundTrip(_out(agg, as_np), [_out(x, as_np) for x in locs], payload)
+
+    def compress(self, m, ctx):
+        return self.round_trip([m], ctx, Communicator(1)).payload
+
+    def payload_bits(self, n, m):
+        return self.iterations * FLOAT_BITS * min(n, m, self.rank) * (n + m)
+
+    def compress_cost(self, n, m):
+        r = min(n, m, self.rank)
+        return self.iterations * (4 * n * m * r + 2 * n * r * r + 3 * n * r)
+
+
+class UnbiasedRankK(Compressor):
+    """Rank-r sketch M u, u ~ N(0, 1/r) from the shared stream, never
+    transmitted (compressors.py:444-468) with the reduce-route round trip
+    (:255-269): the all-reduce averages proj; aggregate = mean(proj) u^T.
+    K1 computes every proj, K5 every outer product."""
+
+    name = "unbiased"
+    linear = True
+    route = "allreduce"
+    uses_error_feedback = True
+
+    def __init__(self, rank=1, device=None):
+        super().__init__(rank)
+        self.device = device
+
+    def _u(self, ctx, n, m):
+        rank = min(n, m, self.rank)
+        return ctx.rng("projection").standard_normal((m, rank)) / np.sqrt(rank)
+
+    def round_trip(self, mats, ctx, comm):
+        _check_mats(mats, comm)
+        as_np = not isinstance(mats[0], torch.Tensor)
+        dev = _device_of(mats, self.device)
+        ds = [_to_dev(x, dev) for x in mats]
+        n, m = ds[0].shape
+        self._charge_compress(comm, n, m, len(ds))
+        u_host = self._u(ctx, n, m)
+        u = _to_dev(u_host, dev)
+        with torch.cuda.device(dev):
+            R = _Rounds(ds, comm, self.rank, dev)
+            ps = R.products(u)
+            q_in = torch.zeros(R.pl.q_elems, **R.f32)
+            R.pl.q_view(q_in, 0).copy_(u)
+            locs = [R.outer(p, q_in) for p in ps]
+            red, div = R.mean([p.clone() for p in ps] if R.dist else ps, self.payload_bits(n, m))
+            if div != 1:
+                red = red / div
+            comm.stats.decode_ops += 2 * n * m * u.shape[1]
+            agg = R.outer(red, q_in)
+            R.check()
+        proj = R.pl.p_view(red, 0).clone()
+        payload = RandomProjection(_out(proj, as_np), u_host if as_np else u)
+        return RoundTrip(_out(agg, as_np), [_out(x, as_np) for x in locs], payload)
+
+    def compress(self, m, ctx):
+        return self.round_trip([m], ctx, Communicator(1)).payload
+
+    def payload_bits(self, n, m):
+        return FLOAT_BITS * min(n, m, self.rank) * n
+
+    def compress_cost(self, n, m):
+        rank = min(n, m, self.rank)
+        return 2 * n * m * rank + m * rank
+
+
+COMPRESSORS = {PowerSGD.name: PowerSGD, BestApproximation.name: BestApproximation,
+               UnbiasedRankK.name: UnbiasedRankK}
 
 
 def make_compressor(name, rank=1):
-    """compressors.py:703-707 (only the PowerSGD hot path is B200-native here)."""
+    """compressors.py:703-707 (the low-rank family that runs on the B200 kernels:
+    powersgd, bestapprox, unbiased)."""
     if name not in COMPRESSORS:
         raise ContractViolation(f"unknown compressor {name!r}; choose from {sorted(COMPRESSORS)}")
     return COMPRESSORS[name](rank=rank)

@@ -148,9 +148,41 @@ def orth_cases():
     np.savez_compressed(os.path.join(HERE, "orthogonalize.npz"), **out)
 
 
+def sibling_cases():
+    """The reference's own BestApproximation / UnbiasedRankK round trips
+    (compressors.py:400-468 via make_compressor) on seeded worker matrices."""
+    from gradcomp.compressors import CompressionContext, make_compressor
+    out = {}
+    shapes = [(8, 6), (3, 20), (40, 32), (65, 7)]
+    for name in ("bestapprox", "unbiased"):
+        for rank in (1, 2, 3):
+            for world in (1, 2, 3):
+                for si, (n, m) in enumerate(shapes):
+                    key = f"{name}_r{rank}_w{world}_s{si}"
+                    mats = [derive_rng(77, "sib", name, rank, world, si, w).standard_normal((n, m))
+                            .astype(np.float32).astype(np.float64) for w in range(world)]
+                    comp = make_compressor(name, rank=rank)
+                    comm = Communicator(world)
+                    ctx = CompressionContext(11, param_index=si, step=rank + world)
+                    trip = comp.round_trip(mats, ctx, comm)
+                    for w in range(world):
+                        out[f"{key}_in{w}"] = mats[w]
+                        out[f"{key}_loc{w}"] = trip.locals[w]
+                    out[f"{key}_agg"] = trip.aggregated
+                    if name == "bestapprox":
+                        out[f"{key}_p"], out[f"{key}_q"] = trip.payload.p, trip.payload.q
+                    else:
+                        out[f"{key}_p"], out[f"{key}_q"] = trip.payload.proj, trip.payload.u
+                    out[f"{key}_stats"] = np.array([comm.stats.bits_allreduced, comm.stats.compress_flops,
+                                                    comm.stats.decode_ops])
+                    out[f"{key}_ctx"] = np.array([11, si, rank + world])
+    np.savez_compressed(os.path.join(HERE, "siblings.npz"), **out)
+
+
 if __name__ == "__main__":
     ef_case("r2_w1", rank=2, world=1, steps=3)
     ef_case("r4_w2", rank=4, world=2, steps=3)
     ef_case("r1_w3", rank=1, world=3, steps=3)
     orth_cases()
+    sibling_cases()
     print("wrote", sorted(f for f in os.listdir(HERE) if f.endswith(".npz")))

@@ -77,7 +77,14 @@ def test_compressor_accounting_matches_reference():
         assert ours.payload_bits(n, m) == ref.payload_bits(n, m)
         assert ours.compress_cost(n, m) == ref.compress_cost(n, m)
     assert PowerSGD.linear and PowerSGD.route == "allreduce" and PowerSGD.uses_error_feedback
-    assert set(COMPRESSORS) == {"powersgd"}
+    assert set(COMPRESSORS) == {"powersgd", "bestapprox", "unbiased"}
+    for name, cls in (("bestapprox", O.BestApproximation), ("unbiased", O.UnbiasedRankK)):
+        for r in (1, 2, 5):
+            a, b = make_compressor(name, r), cls(r)
+            assert a.linear and a.route == "allreduce" and a.uses_error_feedback
+            for n, m in [(3, 7), (512, 4608), (64, 27)]:
+                assert a.payload_bits(n, m) == b.payload_bits(n, m)
+                assert a.compress_cost(n, m) == b.compress_cost(n, m)
     with pytest.raises(ContractViolation):
         make_compressor("topk")
     with pytest.raises(ContractViolation):
