@@ -801,18 +801,23 @@ struct GramItem {
   long long gbase;  // first partial slot of this matrix in the Gram workspace
 };
 
-constexpr int K2G_ROWS = 1024;
+constexpr int K2G_ROWS = 128;
 constexpr int K2G_TILE = 64;
 
 __global__ void __launch_bounds__(256)
     k2_gram(const MatDev* __restrict__ mats, const GramItem* __restrict__ items, const float* __restrict__ P,
             int divisor, const double* __restrict__ repl, double* __restrict__ wsg, double* __restrict__ wsT,
             int* __restrict__ counters, long long flag_off, int nflags, int* status) {
-  __shared__ double X[K2G_TILE][2 * PSGD_MAX_RANK + 1];
+  // Gram of P / W over this block's rows (r (r+1) / 2 pairs, float64); the last
+  // block reduces the partials in block order and runs the MGS sequence of
+  // linalg.py:61-90 on coefficient vectors.  The replacement columns R enter
+  // only if a column degenerates (then the cross terms are computed directly).
+  __shared__ double X[K2G_TILE][PSGD_MAX_RANK + 1];
   __shared__ double G[2 * PSGD_MAX_RANK][2 * PSGD_MAX_RANK];
   __shared__ double cvec[2 * PSGD_MAX_RANK];
   __shared__ double Tm[PSGD_MAX_RANK][2 * PSGD_MAX_RANK];
-  __shared__ int s_last;
+  __shared__ double gpart[256];
+  __shared__ int s_last, s_degen;
   pdl_wait();
   {
     int bad = 0;
@@ -825,62 +830,72 @@ __global__ void __launch_bounds__(256)
   const GramItem it = items[blockIdx.x];
   const MatDev md = mats[it.mat];
   const int n = md.n, r = md.r, R2 = 2 * r;
-  const int npairs = R2 * (R2 + 1) / 2;
+  const int npairs = r * (r + 1) / 2;
   const double inv_div = 1.0 / (double)divisor;
   const int t = threadIdx.x;
-  double acc[3] = {0.0, 0.0, 0.0};
-  int pk[3], pl[3];
-  for (int u = 0; u < 3; ++u) {  // pair index -> (k, l), k <= l
-    int p = t + 256 * u, k = 0;
-    pk[u] = pl[u] = -1;
-    if (p < npairs) {
-      while (p >= R2 - k) { p -= R2 - k; ++k; }
-      pk[u] = k;
-      pl[u] = k + p;
-    }
+  int pk = -1, pl = -1;  // pair index -> (k, l), k <= l (npairs <= 136 < 256)
+  if (t < npairs) {
+    int p = t, k = 0;
+    while (p >= r - k) { p -= r - k; ++k; }
+    pk = k;
+    pl = k + p;
   }
+  double acc = 0.0;
   int bad = 0;
   for (int r0 = it.row0; r0 < it.row0 + it.nrows; r0 += K2G_TILE) {
-    for (int idx = t; idx < K2G_TILE * R2; idx += 256) {
-      const int i = idx / R2, k = idx - i * R2, row = r0 + i;
+    for (int idx = t; idx < K2G_TILE * r; idx += 256) {
+      const int i = idx / r, k = idx - i * r, row = r0 + i;
       double v = 0.0;
       if (row < it.row0 + it.nrows) {
-        if (k < r) {
-          const float f = P[md.p_off + (long long)row * r + k];
-          bad |= !finite1(f);
-          v = (double)f * inv_div;
-        } else {
-          v = repl[md.repl_off + (long long)(k - r) * n + row];
-        }
+        const float f = P[md.p_off + (long long)row * r + k];
+        bad |= !finite1(f);
+        v = (double)f * inv_div;
       }
       X[i][k] = v;
     }
     __syncthreads();
-    for (int u = 0; u < 3; ++u)
-      if (pk[u] >= 0)
-        for (int i = 0; i < K2G_TILE; ++i) acc[u] += X[i][pk[u]] * X[i][pl[u]];
+    if (pk >= 0)
+#pragma unroll 8
+      for (int i = 0; i < K2G_TILE; ++i) acc = fma(X[i][pk], X[i][pl], acc);
     __syncthreads();
   }
   if (__syncthreads_or(bad)) {  // linalg.py:35-36
     if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
   }
-  for (int u = 0; u < 3; ++u)
-    if (pk[u] >= 0) wsg[it.gbase + (long long)it.blk * npairs + t + 256 * u] = acc[u];
+  if (pk >= 0) wsg[it.gbase + (long long)it.blk * npairs + t] = acc;
   __threadfence();
   __syncthreads();
   if (t == 0) s_last = atomicAdd(counters + it.gidx, 1) == it.nblk - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int p = t; p < npairs; p += 256) {  // fixed block order
-    double s = 0.0;
-    for (int b = 0; b < it.nblk; ++b) s += __ldcg(wsg + it.gbase + (long long)b * npairs + p);
-    int k = 0, q = p;
-    while (q >= R2 - k) { q -= R2 - k; ++k; }
-    G[k][k + q] = s;
-    G[k + q][k] = s;
+  {  // fixed order: thread groups take blocks q, q + NG, ...; then groups in order
+    const int NG = 256 / npairs;
+    const int p = t % npairs, q = t / npairs;
+    double sacc = 0.0;
+    if (q < NG) {
+      for (int b0 = q; b0 < it.nblk; b0 += 8 * NG) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          x[u] = b0 + u * NG < it.nblk ? __ldcg(wsg + it.gbase + (long long)(b0 + u * NG) * npairs + p) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sacc += x[u];
+      }
+      gpart[q * npairs + p] = sacc;
+    }
+    __syncthreads();
+    if (t < npairs) {
+      double s2 = 0.0;
+      for (int qq = 0; qq < NG; ++qq) s2 += gpart[qq * npairs + t];
+      G[pk][pl] = s2;
+      G[pl][pk] = s2;
+    }
   }
-  if (t == 0) counters[it.gidx] = 0;
+  if (t == 0) {
+    counters[it.gidx] = 0;
+    s_degen = 0;
+  }
   __syncthreads();
   if (t >= 32) return;
   // ---- MGS on coefficient vectors: value(c) = [P/W, R] c ; <a, b> = a^T G b
@@ -896,35 +911,68 @@ __global__ void __launch_bounds__(256)
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
     return s;
   };
-  for (int j = 0; j < r; ++j) {
-    if (lane < R2) cvec[lane] = lane == j ? 1.0 : 0.0;
+  bool full = false;  // G holds the R cross terms
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (lane < R2 && !full)
+      for (int l = r; l < R2; ++l) {  // unknown R terms are never used unless a column degenerates
+        G[lane][l] = 0.0;
+        G[l][lane] = 0.0;
+      }
     __syncwarp();
-    double before = sqrt(fmax(gdot(cvec, cvec), 0.0));
-    double nrm = before;
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 1) {  // degenerate: the seeded replacement column, before := 1
-        if (lane < R2) cvec[lane] = lane == r + j ? 1.0 : 0.0;
-        __syncwarp();
-        before = 1.0;
+    bool need_full = false;
+    for (int j = 0; j < r && !need_full; ++j) {
+      if (lane < R2) cvec[lane] = lane == j ? 1.0 : 0.0;
+      __syncwarp();
+      double before = sqrt(fmax(gdot(cvec, cvec), 0.0));
+      double nrm = before;
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {  // degenerate: the seeded replacement column, before := 1
+          if (!full) {
+            need_full = true;
+            break;
+          }
+          if (lane < R2) cvec[lane] = lane == r + j ? 1.0 : 0.0;
+          __syncwarp();
+          before = 1.0;
+        }
+        for (int i2 = 0; i2 < j; ++i2) {
+          const double c = gdot(Tm[i2], cvec);
+          __syncwarp();
+          if (lane < R2) cvec[lane] -= c * Tm[i2][lane];
+          __syncwarp();
+        }
+        if (j > 0 || pass == 1) nrm = sqrt(fmax(gdot(cvec, cvec), 0.0));
+        if (!(nrm < 1e-12 * (before + 1.0))) break;
+        if (pass == 1 && lane == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
       }
-      for (int i2 = 0; i2 < j; ++i2) {
-        const double c = gdot(Tm[i2], cvec);
-        __syncwarp();
-        if (lane < R2) cvec[lane] -= c * Tm[i2][lane];
-        __syncwarp();
-      }
-      if (j > 0 || pass == 1) nrm = sqrt(fmax(gdot(cvec, cvec), 0.0));
-      if (!(nrm < 1e-12 * (before + 1.0))) break;
-      if (pass == 1 && lane == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
+      if (need_full) break;
+      const double inv = 1.0 / nrm;
+      if (lane < R2) Tm[j][lane] = cvec[lane] * inv;
+      __syncwarp();
     }
-    const double inv = 1.0 / nrm;
-    if (lane < R2) Tm[j][lane] = cvec[lane] * inv;
+    if (!need_full) break;
+    // rare path: cross terms <P_k / W, R_l> and <R_k, R_l> over all rows, then redo
+    for (int k = 0; k < R2; ++k)
+      for (int l = (k < r ? r : k); l < R2; ++l) {
+        double s = 0.0;
+        for (int i = lane; i < n; i += 32) {
+          const double a = k < r ? (double)P[md.p_off + (long long)i * r + k] * inv_div
+                                 : repl[md.repl_off + (long long)(k - r) * n + i];
+          s = fma(a, repl[md.repl_off + (long long)(l - r) * n + i], s);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) {
+          G[k][l] = s;
+          G[l][k] = s;
+        }
+      }
+    full = true;
     __syncwarp();
   }
   for (int x = lane; x < R2 * r; x += 32) wsT[(long long)it.gidx * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK + x] =
       Tm[x % r][x / r];  // row-major [k][j]
 }
-
 __global__ void __launch_bounds__(256)
     k2_apply(const MatDev* __restrict__ mats, const int* __restrict__ gram_list, const int* __restrict__ blk_mat,
              const int* __restrict__ blk_row0, const float* __restrict__ P, int divisor,
@@ -940,11 +988,14 @@ __global__ void __launch_bounds__(256)
   const double* T = wsT + (long long)gidx * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK;
   const double inv_div = 1.0 / (double)divisor;
   double x[2 * PSGD_MAX_RANK];
+  bool use_r = false;  // replacement columns enter only if a column degenerated
+  for (int k = r * r; k < 2 * r * r; ++k) use_r |= T[k] != 0.0;
   for (int k = 0; k < r; ++k) x[k] = (double)P[md.p_off + (long long)i * r + k] * inv_div;
-  for (int k = 0; k < r; ++k) x[r + k] = repl[md.repl_off + (long long)k * n + i];
+  for (int k = 0; k < r; ++k) x[r + k] = use_r ? repl[md.repl_off + (long long)k * n + i] : 0.0;
+  const int kmax = use_r ? 2 * r : r;
   for (int j = 0; j < r; ++j) {
     double s = 0.0;
-    for (int k = 0; k < 2 * r; ++k) s += x[k] * T[k * r + j];
+    for (int k = 0; k < kmax; ++k) s += x[k] * T[k * r + j];
     Phat[md.p_off + (long long)i * r + j] = (float)s;
   }
 }
@@ -1629,25 +1680,36 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
     const bool qal = (head & 3) == 0;
     float4* __restrict__ w4 = reinterpret_cast<float4*>(work + o + head);
     float4* __restrict__ e4 = reinterpret_cast<float4*>(e + o + head);
-    for (int c = gl; c < body4; c += G) {
-      float qv[4][R];
-      load_q4<R, false>(qrow + 4 * c, md.qld, qal, r, qv);
-      float mh[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          float qk = qv[u][k];
-          if (MODE == 1 && divisor != 1) qk = qk / (float)divisor;
-          mh[u] = fmaf(ph[k], qk, mh[u]);
-        }
-      }
+    // 4 float4 per lane per pass: the delta loads are issued together (memory-level parallelism)
+    for (int c0 = gl; c0 < body4; c0 += 4 * G) {
+      float4 d[4];
       if (MODE == 0) {
-        const float4 d = __ldcs(w4 + c);
-        st_stream(e4 + c, make_float4(d.x - mh[0], d.y - mh[1], d.z - mh[2], d.w - mh[3]));
-        if (write_mhat) st_stream(w4 + c, make_float4(mh[0], mh[1], mh[2], mh[3]));
-      } else {
-        st_stream(w4 + c, make_float4(mh[0], mh[1], mh[2], mh[3]));
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          d[v] = c0 + v * G < body4 ? __ldcs(w4 + c0 + v * G) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int c = c0 + v * G;
+        if (c >= body4) break;
+        float qv[4][R];
+        load_q4<R, false>(qrow + 4 * c, md.qld, qal, r, qv);
+        float mh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float qk = qv[u][k];
+            if (MODE == 1 && divisor != 1) qk = qk / (float)divisor;
+            mh[u] = fmaf(ph[k], qk, mh[u]);
+          }
+        }
+        if (MODE == 0) {
+          st_stream(e4 + c, make_float4(d[v].x - mh[0], d[v].y - mh[1], d[v].z - mh[2], d[v].w - mh[3]));
+          if (write_mhat) st_stream(w4 + c, make_float4(mh[0], mh[1], mh[2], mh[3]));
+        } else {
+          st_stream(w4 + c, make_float4(mh[0], mh[1], mh[2], mh[3]));
+        }
       }
     }
   }
@@ -2009,7 +2071,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       pl->wlist.push_back(mi);
       pl->small_list.push_back(mi);
       pl->k2_wregion = std::max(pl->k2_wregion, (int)align4((long long)md.n * md.r));
-    } else if ((long long)md.n * md.r <= K2_SMEM_DOUBLES) {
+    } else if ((long long)md.n * md.r <= K2_SMEM_DOUBLES && md.n <= 1024) {  // taller: Gram space
       pl->clist.push_back(mi);
       pl->small_list.push_back(mi);
       pl->k2_smem = std::max(pl->k2_smem, md.n * md.r * 8);
@@ -2017,7 +2079,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       const int gidx = (int)pl->gram_list.size();
       pl->gram_list.push_back(mi);
       const int nblk = (md.n + K2G_ROWS - 1) / K2G_ROWS;
-      const int npairs = (2 * md.r) * (2 * md.r + 1) / 2;
+      const int npairs = md.r * (md.r + 1) / 2;
       for (int b2 = 0; b2 < nblk; ++b2)
         pl->gram_items.push_back({mi, b2 * K2G_ROWS, std::min(K2G_ROWS, md.n - b2 * K2G_ROWS), b2, nblk, gidx,
                                   pl->wsg_elems});

@@ -646,6 +646,9 @@ __global__ void __launch_bounds__(RT, 1)
     RES_LOG(si - sb0, 0);
     if (dbg != nullptr && t == 0 && si - sb0 < 16)
       dbg[gridDim.x * 8 + (blockIdx.x * 16 + si - sb0) * 4 + 1] = sb.mat * 100000 + sb.c0 * 10 + sb.vec;
+    // the next run (another matrix) maps rows to other owner lanes: every warp must
+    // have published and zeroed this run's accumulators first
+    if (sb.flush && si + 1 < sb1) __syncthreads();
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   RES_T(1);
