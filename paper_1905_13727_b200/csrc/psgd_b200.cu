@@ -116,10 +116,12 @@ struct SplitRow {  // an over-long row whose P is combined from `parts` partials
 struct SlabItem {  // K3 item: column slab [c0, c0 + C) x row chunk `chunk` of `mat` (nchunks == 1: fused)
   long long ws_off;
   int mat, c0, chunk, nchunks, slab, vec, cq_log2, pad;
+  int ksub, pad2;  // tall items: register-slab row chunks per CTA (q accumulated in registers)
 };
 
 struct Group {
   int r, beg, end, smem;
+  int tall;  // K3 groups: items of tall matrices (k3_slab<..., TALL = true>)
 };
 
 __host__ __device__ constexpr int k3_dcap(int r) { return r <= 4 ? 64 : 32; }
@@ -364,7 +366,7 @@ struct WarpReducer {  // one warp, shuffles only
 // delta = g + e ; P[i,:] = sum_j delta[i,j] Q[j,:]   (optimizer.py:120, compressors.py:336)
 
 struct K1Layout {  // dynamic smem: g stages | e stages | Q slots | red | barriers
-  int qslot_floats;
+  int qslot_floats, nq;  // nq = 2 (double-buffered Q) or 1 (one large slot: m r up to ~128 KB)
   int off_q, off_red, off_bar, total;
   int stages, stage_floats;  // chosen per plan: the largest stage that fits beside the Q slots
 };
@@ -539,7 +541,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     if (lane == 0) {
       const uint64_t pol = pol_evict_first();
       const uint64_t polq = pol_evict_last();
-      int cur = -1, mseq = -1;
+      int cur = -1, qseq = -1;  // qseq counts the matrices whose Q is staged
       Chunk1 nx = chunks[cb < ce ? cb : 0];
       MatDev md{};
       for (int k = cb; k < ce; ++k) {
@@ -550,10 +552,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         if (ch.mat != cur) {  // Q of the next matrix into a smem slot (double-buffered)
           md = mats[ch.mat];
           cur = ch.mat;
-          ++mseq;
           if (md.qs) {
-            const int qs = mseq & 1;
-            mbar_wait(&qempty[qs], ((mseq >> 1) & 1) ^ 1);
+            ++qseq;
+            const int qs = qseq % L.nq;
+            mbar_wait(&qempty[qs], ((qseq / L.nq) & 1) ^ 1);
             const uint32_t qb = (uint32_t)((long long)md.r * md.qld * 4);
             mbar_expect_tx(&qfull[qs], qb);
             tma_load(qsl + qs * L.qslot_floats, Q + md.q_off, qb, &qfull[qs], polq);
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     P[bias_off + x] = v;
   }
   const uint64_t keep = pol_evict_last();
-  int cur = -1, mseq = -1, rpar = 0;
+  int cur = -1, qseq = -1, rpar = 0;
   bool cur_qs = false;
   Chunk1 nx = chunks[cb < ce ? cb : 0];
   MatDev md{};
@@ -592,13 +594,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     if (ch.mat != cur) {
       if (cur >= 0 && cur_qs) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&qempty[mseq & 1]);
+        if (lane == 0) mbar_arrive(&qempty[qseq % L.nq]);
       }
       md = mats[ch.mat];
       cur = ch.mat;
-      ++mseq;
       cur_qs = md.qs != 0;
-      if (cur_qs) mbar_wait(&qfull[mseq & 1], (mseq >> 1) & 1);
+      if (cur_qs) {
+        ++qseq;
+        mbar_wait(&qfull[qseq % L.nq], (qseq / L.nq) & 1);
+      }
     }
     mbar_wait(&full[s], ph);
     const float* sg = sgb + s * L.stage_floats;
@@ -610,7 +614,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 #else
     if (cur_qs)
 #endif
-      k1_chunk<RM, true>(ch, md, qsl + (mseq & 1) * L.qslot_floats, sg, se, e != nullptr, work, P, splits,
+      k1_chunk<RM, true>(ch, md, qsl + (qseq % L.nq) * L.qslot_floats, sg, se, e != nullptr, work, P, splits,
                          psplit, split_cnt, rb, keep, bad);
 #ifndef PSGD_K1_NOCOMPUTE
     else
@@ -1012,7 +1016,7 @@ __global__ void __launch_bounds__(256)
 //     last-arriving chunk of the slab sums the partials in chunk order; the EF
 //     pass is K4.
 
-template <int R, bool EXACT>
+template <int R, bool EXACT, bool TALL>
 __global__ void __launch_bounds__(kThreads, 2)
     k3_slab(const MatDev* __restrict__ mats, const SlabItem* __restrict__ items, float* __restrict__ work,
             const float* __restrict__ P, int divisor, const double* __restrict__ repl, float* __restrict__ Phat,
@@ -1026,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ double sred[64];
   const SlabItem it = items[blockIdx.x];
   const int t = threadIdx.x;
-  const bool fused = it.nchunks == 1;
+  const bool fused = !TALL;  // fused: all n rows in this CTA; tall: split rows, q partials
   const MatDev md = mats[it.mat];
   const int r = EXACT ? R : md.r;
   const int n = md.n, m = md.m;
@@ -1041,7 +1045,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int rg = t >> cql;
   const int col = it.c0 + cq * vec;
   const bool colok = col < m;
-  const int rbeg = it.chunk * rows_chunk;
+  const int rbeg = it.chunk * it.ksub * rows_chunk;
   const int nrows = min(n - rbeg, rows_chunk);
   const int ncols = min(C, m - it.c0);
   double* gsd = reinterpret_cast<double*>(k3smem);                  // fused owner: n x r float64
@@ -1196,6 +1200,58 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int k = 0; k < R; ++k)
           if (EXACT || k < r) qp[0][k] = fmaf(d[s], ps[li * r + k], qp[0][k]);
+      }
+    }
+  }
+  // 3b. tall items: the CTA's further row chunks, q accumulated in registers (one
+  //     reduction and one partial per CTA instead of one per 32-64 KB chunk)
+  for (int sub = 1; TALL && !fused && sub < it.ksub; ++sub) {
+    const int rb = rbeg + sub * rows_chunk;
+    const int nr = min(n - rb, rows_chunk);
+    if (nr <= 0) break;
+    __syncthreads();  // every thread is done with ps
+    for (int x = t; x < nr * r; x += kThreads) ps[x] = Phat[md.p_off + (long long)rb * r + x];
+    const long long bs = md.flat_off + (long long)rb * m + col;
+    if (vec == 4) {
+#pragma unroll
+      for (int s2 = 0; s2 < DCAP / 4; ++s2) {
+        const int li = rg + RG * s2;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (colok && li < nr) v = __ldcs(reinterpret_cast<const float4*>(work + bs + (long long)li * m));
+        d[4 * s2 + 0] = v.x; d[4 * s2 + 1] = v.y; d[4 * s2 + 2] = v.z; d[4 * s2 + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < DCAP; ++s2) {
+        const int li = rg + RG * s2;
+        d[s2] = (colok && li < nr) ? __ldcs(work + bs + (long long)li * m) : 0.f;
+      }
+    }
+    __syncthreads();
+    if (vec == 4) {
+#pragma unroll
+      for (int s2 = 0; s2 < DCAP / 4; ++s2) {
+        const int li = rg + RG * s2;
+        if (li < nr) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            if (EXACT || k < r) {
+              const float pk = ps[li * r + k];
+#pragma unroll
+              for (int v = 0; v < 4; ++v) qp[v][k] = fmaf(d[4 * s2 + v], pk, qp[v][k]);
+            }
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < DCAP; ++s2) {
+        const int li = rg + RG * s2;
+        if (li < nr) {
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (EXACT || k < r) qp[0][k] = fmaf(d[s2], ps[li * r + k], qp[0][k]);
+        }
       }
     }
   }
@@ -1996,17 +2052,27 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     const long long bar_b = (2 * K1_STAGES + 4) * 8 + 16;
     const long long min_stage = 2LL * 2 * (K1_CHUNK + 8) * 4;  // 2 stages of the smallest chunk
     const long long cap = std::min<long long>(K1_QSLOT_CAP, ((227LL * 1024 - min_stage - red_b - bar_b - 512) / 8) & ~3LL);
+    // one large slot (up to 128 KB) when some Q does not fit a double-buffered slot:
+    // Q read from smem beats Q read through L1/L2 per element (stress: 4096 x 8)
+    const long long cap1 = std::min<long long>(32768, ((227LL * 1024 - min_stage - red_b - bar_b - 512) / 4) & ~3LL);
+    // measured slower on the stress set (one row per chunk behind a 128 KB slot), so
+    // opt-in only: PSGD_K1_BIGQ=1
+    bool big = false;
+    const char* bq = getenv("PSGD_K1_BIGQ");
+    if (bq && bq[0] == '1')
+      for (auto& md : pl->mats) big |= (long long)md.r * md.qld > cap;
+    L.nq = big ? 1 : 2;
     long long qslot = 4;
     for (auto& md : pl->mats) {
-      md.qs = (long long)md.r * md.qld <= cap ? 1 : 0;
+      md.qs = (long long)md.r * md.qld <= (big ? cap1 : cap) ? 1 : 0;
       if (md.qs) qslot = std::max(qslot, (long long)md.r * md.qld);
     }
     L.qslot_floats = (int)qslot;
     L.stages = 2;
-    const long long room = 227LL * 1024 - 2 * qslot * 4 - red_b - bar_b - 512;
+    const long long room = 227LL * 1024 - L.nq * qslot * 4 - red_b - bar_b - 512;
     L.stage_floats = (int)std::min<long long>(16384 + 8, (room / (2LL * L.stages * 4)) & ~3LL);
     int off = 2 * L.stages * L.stage_floats * 4;
-    L.off_q = off;   off += 2 * L.qslot_floats * 4;
+    L.off_q = off;   off += L.nq * L.qslot_floats * 4;
     L.off_red = off; off += (int)red_b;
     off = (off + 15) & ~15;
     L.off_bar = off; off += (int)bar_b;
@@ -2102,31 +2168,40 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     std::vector<int> rs;
     for (auto& md : pl->mats)
       if (std::find(rs.begin(), rs.end(), md.r) == rs.end()) rs.push_back(md.r);
-    for (int r : rs) {
-      Group gp{r, (int)pl->k3.size(), 0, 0};
+    for (int r : rs) for (int tall = 0; tall < 2; ++tall) {
+      Group gp{r, (int)pl->k3.size(), 0, 0, tall};
       for (int mi = 0; mi < nmat; ++mi) {
         const MatDev& md = pl->mats[mi];
         if (md.r != r) continue;
         const K3Cfg cf = k3_tall_config(md.n, md.m, r);
+        if ((cf.nchunks > 1) != (tall == 1)) continue;
         const int CQ = 1 << cf.cql, C = CQ * cf.vec, RG = kThreads / CQ;
         const int nslab = (md.m + C - 1) / C;
         for (int s = 0; s < nslab; ++s) {
           int slab_id = -1;
           long long wo = 0;
+          // tall: ~PSGD_K3_SUBROWS rows per CTA, q accumulated in registers
+          // (measured: 2048 rows for float4 slabs (stress 4096 x 4096), one register slab for
+          // scalar-column slabs (LSTM, m % 4 != 0) where the extra loop only adds latency)
+          static const int sub_rows = getenv("PSGD_K3_SUBROWS") ? atoi(getenv("PSGD_K3_SUBROWS")) : 2048;
+          const int ksub = (cf.nchunks > 1 && cf.vec == 4)
+                               ? std::max(1, std::min(cf.nchunks, sub_rows / cf.rows_chunk)) : 1;
+          const int nitems = (cf.nchunks + ksub - 1) / ksub;
           if (cf.nchunks > 1) {
             slab_id = pl->n_tall_slabs++;
             wo = pl->wsq_elems;
-            pl->wsq_elems += (long long)cf.nchunks * C * r;
+            pl->wsq_elems += (long long)nitems * C * r;
           }
-          for (int ch = 0; ch < cf.nchunks; ++ch)
-            pl->k3.push_back({wo, mi, s * C, ch, cf.nchunks, slab_id, cf.vec, cf.cql, nslab});
+          for (int ch = 0; ch < nitems; ++ch)
+            pl->k3.push_back({wo, mi, s * C, ch, cf.nchunks > 1 ? nitems : 1, slab_id, cf.vec, cf.cql, nslab,
+                              ksub, 0});
         }
         const int smem = (cf.nchunks == 1 && PSGD_K3_OWNER_GS ? md.n * r * 8 : 0) +
                          (cf.rows_chunk * r + RG * C * r + C * r) * (int)sizeof(float);
         gp.smem = std::max(gp.smem, smem);
       }
       gp.end = (int)pl->k3.size();
-      pl->g3.push_back(gp);
+      if (gp.end > gp.beg) pl->g3.push_back(gp);
     }
   }
   build_row_items(pl->mats, true, pl->k4, pl->g4);
@@ -2374,7 +2449,7 @@ struct RunK3 {
                  bool wait_first, int* status, cudaStream_t st) {
     const int nitems = gp.end - gp.beg;
     if (nitems <= 0) return PSGD_OK;
-    auto kern = k3_slab<R, EXACT>;
+    auto kern = gp.tall ? k3_slab<R, EXACT, true> : k3_slab<R, EXACT, false>;
     if (gp.smem > 48 * 1024)
       PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gp.smem));
     PSGD_CUDA_CHECK(launch_ex(kern, nitems, kThreads, gp.smem, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
