@@ -121,14 +121,14 @@ def run_reference(a):
     specs = catalog_specs(a.workload)
     world = a.gpus
     budget = 150.0
-    times = oracle_steps(specs, a.rank, world, a.steps, budget, warmup=min(a.warmup, 2))
+    times = oracle_steps(specs, a.rank, world, a.steps, budget, warmup=a.warmup)
     ms = 1e3 * statistics.mean(times)
     cores = cpu_threads()
     sample = (f"{len(times)} full steps of {a.workload} r={a.rank} with {world} simulated workers "
               f"(float64 numpy oracle of optimizer.py:110-129, OpenBLAS {cores} threads)")
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms/step", "n_gpus": a.gpus,
-        "steps": len(times), "warmup": min(a.warmup, 2), "ms_per_step": round(ms, 4),
+        "steps": len(times), "warmup": a.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": f"{a.workload} rank {a.rank}, W={world} simulated workers (CPU)",
