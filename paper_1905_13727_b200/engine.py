@@ -54,8 +54,13 @@ class PowerSGDEngine:
     """
 
     def __init__(self, specs, rank, *, workers=1, comm=None, seed=0, device=None,
-                 error_feedback=True):
+                 error_feedback=True, param_indices=None):
         self.specs = list(specs)
+        # the reference's param_index (seeds the warm start): catalog position, or the
+        # caller's global indices when the specs are a subset (e.g. one DDP bucket)
+        self.param_indices = list(range(len(self.specs))) if param_indices is None else list(param_indices)
+        if len(self.param_indices) != len(self.specs):
+            raise ValueError("param_indices must match specs")
         self.rank = int(rank)
         if self.rank < 1:
             raise ContractViolation(f"rank must be >= 1, got {rank}")
@@ -103,7 +108,7 @@ class PowerSGDEngine:
         self.repl = pl.repl_table()
         for k, pi in enumerate(self.mat_index):
             mi = pl.matrices[k]
-            q0 = warm_start_q(self.seed, pi, mi.m, mi.r_eff)
+            q0 = warm_start_q(self.seed, self.param_indices[pi], mi.m, mi.r_eff)
             pl.q_view(self.Q, k).copy_(torch.from_numpy(q0))
         self.step_count = 0
         self._graph = None
