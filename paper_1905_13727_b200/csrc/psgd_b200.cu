@@ -1771,6 +1771,67 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
   }
 }
 
+// K4 column tiles (tall matrices with m % 4 == 0): a warp owns 128 columns x
+// K4T_ROWS rows; its Q block (4 columns x r) sits in registers for the whole
+// tile, so per float4 of delta the warp loads only delta and a broadcast P-hat
+// row (the row pass above re-reads r float4 of Q per float4 of delta).
+constexpr int K4T_ROWS = 64;
+struct TileItem {
+  int mat, row0, nrows, c0;
+};
+
+template <int R, bool EXACT>
+__global__ void __launch_bounds__(kThreads) k4_tile(const MatDev* __restrict__ mats, const TileItem* __restrict__ items,
+                                                    int beg, int end, float* __restrict__ work, float* __restrict__ e,
+                                                    const float* __restrict__ Phat, const float* __restrict__ qsrc,
+                                                    int write_mhat, const int* __restrict__ status) {
+  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
+  const int lane = threadIdx.x & 31;
+  const int wi = beg + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (wi >= end) return;
+  const TileItem it = items[wi];
+  const MatDev md = mats[it.mat];
+  const int r = EXACT ? R : md.r;
+  const int m = md.m;
+  const int col = it.c0 + 4 * lane;
+  const bool ok = col < m;
+  float qv[4][R];
+  if (ok) {
+    load_q4<R, false>(qsrc + md.q_off + col, md.qld, true, r, qv);
+  } else {
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int k = 0; k < R; ++k) qv[v][k] = 0.f;
+  }
+  const float* __restrict__ pr = Phat + md.p_off + (long long)it.row0 * r;
+  const long long base = md.flat_off + (long long)it.row0 * m + col;
+  for (int i0 = 0; i0 < it.nrows; i0 += 8) {
+    float4 d[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      d[u] = (ok && i0 + u < it.nrows) ? __ldcs(reinterpret_cast<const float4*>(work + base + (long long)(i0 + u) * m))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (!ok || i0 + u >= it.nrows) break;
+      float mh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (EXACT || k < r) {
+          const float p = __ldg(pr + (long long)(i0 + u) * r + k);  // one address per warp: broadcast
+#pragma unroll
+          for (int v = 0; v < 4; ++v) mh[v] = fmaf(p, qv[v][k], mh[v]);
+        }
+      }
+      const long long a = base + (long long)(i0 + u) * m;
+      st_stream(reinterpret_cast<float4*>(e + a),
+                make_float4(d[u].x - mh[0], d[u].y - mh[1], d[u].z - mh[2], d[u].w - mh[3]));
+      if (write_mhat) st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
+    }
+  }
+}
+
 // ============================================================================= tree mean
 struct TreeArgs {
   const float* p[PSGD_MAX_TREE];
@@ -1877,6 +1938,9 @@ struct psgd_plan {
   std::vector<int> tall_list, all_list;
   std::vector<RowItem> k4, k5;
   std::vector<Group> g4, g5;
+  std::vector<TileItem> k4t;   // K4 column tiles (tall, m % 4 == 0)
+  std::vector<Group> g4t;
+  TileItem* d_k4t = nullptr;
   int n_tall = 0, n_tall_slabs = 0;
   long long wsq_elems = 0;
   // device
@@ -1916,6 +1980,28 @@ int lanes_log2_for(int m, int max_lg) {
   return lg;
 }
 
+bool k4_tileable(const MatDev& md) {
+  static const bool off = getenv("PSGD_K4_TILE") && getenv("PSGD_K4_TILE")[0] == '0';
+  return !off && md.tall && md.m % 4 == 0 && md.flat_off % 4 == 0 && md.m >= 128;
+}
+
+void build_tile_items(const std::vector<MatDev>& mats, std::vector<TileItem>& items, std::vector<Group>& groups) {
+  std::vector<int> rs;
+  for (auto& md : mats)
+    if (k4_tileable(md) && std::find(rs.begin(), rs.end(), md.r) == rs.end()) rs.push_back(md.r);
+  for (int r : rs) {
+    Group gp{r, (int)items.size(), 0, 0, 0};
+    for (int mi = 0; mi < (int)mats.size(); ++mi) {
+      const MatDev& md = mats[mi];
+      if (md.r != r || !k4_tileable(md)) continue;
+      for (int r0 = 0; r0 < md.n; r0 += K4T_ROWS)
+        for (int c0 = 0; c0 < md.m; c0 += 128) items.push_back({mi, r0, std::min(K4T_ROWS, md.n - r0), c0});
+    }
+    gp.end = (int)items.size();
+    groups.push_back(gp);
+  }
+}
+
 void build_row_items(const std::vector<MatDev>& mats, bool tall_only, std::vector<RowItem>& items,
                      std::vector<Group>& groups) {
   std::vector<int> rs;
@@ -1927,6 +2013,7 @@ void build_row_items(const std::vector<MatDev>& mats, bool tall_only, std::vecto
     for (int mi = 0; mi < (int)mats.size(); ++mi) {
       const MatDev& md = mats[mi];
       if (md.r != r || (tall_only && !md.tall)) continue;
+      if (tall_only && k4_tileable(md)) continue;  // K4 column tiles instead
       const int lg = lanes_log2_for(md.m, 5);
       const int rpp = 32 >> lg;
       int rows = std::max(1, kRowItemElems / md.m);
@@ -2205,6 +2292,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     }
   }
   build_row_items(pl->mats, true, pl->k4, pl->g4);
+  build_tile_items(pl->mats, pl->k4t, pl->g4t);
   build_row_items(pl->mats, false, pl->k5, pl->g5);
 
   // ---- fused W = 1 step eligibility and layout
@@ -2265,6 +2353,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_ksg = take(pl->ks_grp.size() * sizeof(int));
   const size_t o_gbar = take(4 * sizeof(unsigned));
   const size_t o_k4 = take(pl->k4.size() * sizeof(RowItem));
+  const size_t o_k4t = take(pl->k4t.size() * sizeof(TileItem));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
   const size_t o_wsq = take((size_t)std::max(1LL, pl->wsq_elems) * sizeof(float));
@@ -2299,6 +2388,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_ks_grp = reinterpret_cast<int*>(b + o_ksg);
   pl->d_gbar = reinterpret_cast<unsigned*>(b + o_gbar);
   pl->d_k4 = reinterpret_cast<RowItem*>(b + o_k4);
+  pl->d_k4t = reinterpret_cast<TileItem*>(b + o_k4t);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
   pl->d_wsq = reinterpret_cast<float*>(b + o_wsq);
@@ -2329,6 +2419,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_ks_grp, pl->ks_grp.data(), pl->ks_grp.size() * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gbar, 0, 4 * sizeof(unsigned));
   if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
+  if (ce == cudaSuccess) ce = up(pl->d_k4t, pl->k4t.data(), pl->k4t.size() * sizeof(TileItem));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_split_cnt, 0, std::max<size_t>(16, pl->splits.size() * sizeof(int)));
@@ -2378,7 +2469,7 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->launches_orthogonalize = (pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0;
   o->launches_orthogonalize = ((pl->small_list.size() + (pl->nbias > 0)) > 0 ? 1 : 0) +
                               (pl->gram_items.empty() ? 0 : 2);
-  o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4);
+  o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4) + nonempty(pl->g4t);
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
   const bool fused_step = pl->ks_ok && !psgd_force_multi();
@@ -2482,6 +2573,19 @@ struct RunK45Mode {
 
 template <int R, bool EXACT>
 using RunK4 = RunK45Mode<0>::F<R, EXACT>;
+
+template <int R, bool EXACT>
+struct RunK4T {
+  static int run(const psgd_plan* pl, const Group& gp, float* work, float* e, const float* phat, const float* q,
+                 int write_mhat, const int* status, cudaStream_t st) {
+    const int nitems = gp.end - gp.beg;
+    if (nitems <= 0) return PSGD_OK;
+    k4_tile<R, EXACT><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k4t, gp.beg, gp.end, work, e, phat, q,
+                                                               write_mhat, status);
+    PSGD_CUDA_CHECK(cudaGetLastError());
+    return PSGD_OK;
+  }
+};
 template <int R, bool EXACT>
 using RunK5 = RunK45Mode<1>::F<R, EXACT>;
 
@@ -2625,6 +2729,11 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
     rc = dispatch_r<RunK4>(gp.r, pl, (const RowItem*)pl->d_k4, gp, work, e, (const float*)p_hat,
                            (const float*)q_out, 1, (float*)nullptr, pl->world == 1 ? 1 : 0,
                            (const int*)status, st);
+    if (rc) return rc;
+  }
+  for (const Group& gp : pl->g4t) {
+    rc = dispatch_r<RunK4T>(gp.r, pl, gp, work, e, (const float*)p_hat, (const float*)q_out,
+                            pl->world == 1 ? 1 : 0, (const int*)status, st);
     if (rc) return rc;
   }
   return PSGD_OK;
