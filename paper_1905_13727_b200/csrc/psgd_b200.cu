@@ -1832,6 +1832,129 @@ __global__ void __launch_bounds__(kThreads) k4_tile(const MatDev* __restrict__ m
   }
 }
 
+// K1 column tiles for matrices whose Q block cannot be staged in shared memory
+// (m r > the Q slot, e.g. the 4096 x 4096 rank-8 stress set): a warp owns 128
+// columns x K1T_ROWS rows with its Q block (4 columns x r) in registers; per
+// batch of 8 rows it loads g and e (16 float4 in flight per lane), stores delta,
+// and reduce-scatters the 8 x r row partials across the warp (each lane ends up
+// owning V / 32 sums) into a per-column-tile partial buffer; k1_tile_reduce
+// sums the tiles in order into P (optimizer.py:120, compressors.py:336).
+constexpr int K1T_ROWS = 64;
+
+template <int RM>
+__global__ void __launch_bounds__(kThreads) k1_tile(const MatDev* __restrict__ mats, const TileItem* __restrict__ items,
+                                                    int nitems, const long long* __restrict__ part_off,
+                                                    const float* __restrict__ g, const float* __restrict__ e,
+                                                    float* __restrict__ work, const float* __restrict__ Q,
+                                                    float* __restrict__ part) {
+  constexpr int V = 8 * RM;
+  const int lane = threadIdx.x & 31;
+  const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (wi >= nitems) return;
+  const TileItem it = items[wi];
+  const MatDev md = mats[it.mat];
+  const int r = md.r, m = md.m, n = md.n;
+  const int col = it.c0 + 4 * lane;
+  const bool ok = col < m;
+  float qv[4][RM];
+  if (ok) {
+    load_q4<RM, false>(Q + md.q_off + col, md.qld, true, r, qv);
+  } else {
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int k = 0; k < RM; ++k) qv[v][k] = 0.f;
+  }
+  const long long base = md.flat_off + (long long)it.row0 * m + col;
+  float* __restrict__ pt = part + part_off[it.mat] + (long long)(it.c0 >> 7) * n * r;
+  for (int i0 = 0; i0 < it.nrows; i0 += 8) {
+    float4 d[8];
+    {
+      float4 a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] = b[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok && i0 + u < it.nrows) {
+          a[u] = __ldcs(reinterpret_cast<const float4*>(g + base + (long long)(i0 + u) * m));
+          if (e) b[u] = __ldcs(reinterpret_cast<const float4*>(e + base + (long long)(i0 + u) * m));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) d[u] = make_float4(a[u].x + b[u].x, a[u].y + b[u].y, a[u].z + b[u].z, a[u].w + b[u].w);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (ok && i0 + u < it.nrows) reinterpret_cast<float4*>(work + base + (long long)(i0 + u) * m)[0] = d[u];
+    float v[V];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int k = 0; k < RM; ++k) {
+        float s2 = d[u].x * qv[0][k];
+        s2 = fmaf(d[u].y, qv[1][k], s2);
+        s2 = fmaf(d[u].z, qv[2][k], s2);
+        v[u * RM + k] = fmaf(d[u].w, qv[3][k], s2);
+      }
+    int vbase = 0, h = V;  // reduce-scatter over the 32 lanes (fixed order => deterministic)
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      const int o = 16 >> l;
+      if (h > 1) {
+        h >>= 1;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < V / 2; ++i)
+          if (i < h) {
+            const float send = up ? v[i] : v[i + h];
+            const float keep = up ? v[i + h] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        if (up) vbase += h;
+      } else {
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+      }
+    }
+    const bool owner = V >= 32 || (lane & ((32 / V) - 1)) == 0;
+#pragma unroll
+    for (int i = 0; i < (V >= 32 ? V / 32 : 1); ++i) {
+      const int oi = vbase + i, u = oi / RM, k = oi - u * RM;
+      if (owner && k < r && i0 + u < it.nrows) pt[(long long)(it.row0 + i0 + u) * r + k] = v[i];
+    }
+  }
+}
+
+// P = sum over the column tiles (in tile order) of the k1_tile partials; a
+// non-finite sum (a non-finite g or e poisons its row) raises the plan's last flag
+__global__ void __launch_bounds__(256) k1_tile_reduce(const MatDev* __restrict__ mats, const int* __restrict__ list,
+                                                      const long long* __restrict__ part_off,
+                                                      const float* __restrict__ part, float* __restrict__ P,
+                                                      long long flag_slot) {
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  const int mi = list[blockIdx.y];
+  const MatDev md = mats[mi];
+  const long long nr = (long long)md.n * md.r;
+  const int ntiles = (md.m + 127) >> 7;
+  const float* src = part + part_off[mi];
+  bool bad = false;
+  for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < nr; x += (long long)gridDim.x * blockDim.x) {
+    float s2 = 0.f;
+    for (int t0 = 0; t0 < ntiles; t0 += 8) {
+      float y[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) y[u] = t0 + u < ntiles ? __ldcs(src + (long long)(t0 + u) * nr + x) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s2 += y[u];
+    }
+    bad |= !finite1(s2);
+    P[md.p_off + x] = s2;
+  }
+  if (bad) atomicOr(&s_bad, 1);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_bad) P[flag_slot] = 1.f;
+}
+
 // ============================================================================= tree mean
 struct TreeArgs {
   const float* p[PSGD_MAX_TREE];
@@ -1941,6 +2064,15 @@ struct psgd_plan {
   std::vector<TileItem> k4t;   // K4 column tiles (tall, m % 4 == 0)
   std::vector<Group> g4t;
   TileItem* d_k4t = nullptr;
+  // K1 column tiles (matrices whose Q block is not staged): items, matrix list, partials
+  std::vector<TileItem> k1t;
+  std::vector<int> k1t_list;
+  std::vector<long long> k1t_off;  // per matrix (all matrices, -1 unused)
+  long long k1t_part_elems = 0;
+  TileItem* d_k1t = nullptr;
+  int* d_k1t_list = nullptr;
+  long long* d_k1t_off = nullptr;
+  float* d_k1t_part = nullptr;
   int n_tall = 0, n_tall_slabs = 0;
   long long wsq_elems = 0;
   // device
@@ -2168,8 +2300,20 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   // ---- K1 chunks: whole rows, <= stage_floats - 8 floats; 2^lg1 lanes per row so
   // that a pass keeps all 16 consumer warps busy (rows <= 32 lanes need no barrier)
   const int seg = pl->k1l.stage_floats - 8;
+  pl->k1t_off.assign(std::max(1, nmat), 0);
   for (int mi = 0; mi < nmat; ++mi) {
     MatDev& md = pl->mats[mi];
+    static const bool k1t_off_env = getenv("PSGD_K1_TILE") && getenv("PSGD_K1_TILE")[0] == '0';
+    if (!k1t_off_env && !md.qs && md.m % 4 == 0 && md.flat_off % 4 == 0 && md.m >= 128) {
+      // K1 column tiles: Q stays in registers per warp tile (k1_tile + k1_tile_reduce)
+      pl->k1t_list.push_back(mi);
+      pl->k1t_off[mi] = pl->k1t_part_elems;
+      pl->k1t_part_elems += (long long)((md.m + 127) / 128) * md.n * md.r;
+      for (int r0 = 0; r0 < md.n; r0 += K1T_ROWS)
+        for (int c0 = 0; c0 < md.m; c0 += 128) pl->k1t.push_back({mi, r0, std::min(K1T_ROWS, md.n - r0), c0});
+      md.nck = 0;
+      continue;
+    }
     if (md.m <= seg) {
       const int rows_fit = seg / md.m;
       int lg = 2;  // ~4 float4 per lane per row, 4..32 lanes
@@ -2211,7 +2355,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     for (auto& c : pl->k1) w.push_back((double)c.nrows * c.ncols + 2048.0);  // + per-chunk overhead
     pl->k1_beg = balance(w, pl->nsm);
   }
-  pl->nflags = std::max(1, (int)pl->k1_beg.size() - 1);
+  pl->nflags = std::max(1, (int)pl->k1_beg.size() - 1) + (pl->k1t.empty() ? 0 : 1);  // + k1_tile_reduce's slot
   pl->p_bias_off = po;
   pl->flag_off = align4(po + nbias);
   pl->p_elems = pl->flag_off + align4(pl->nflags);
@@ -2354,6 +2498,10 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_gbar = take(4 * sizeof(unsigned));
   const size_t o_k4 = take(pl->k4.size() * sizeof(RowItem));
   const size_t o_k4t = take(pl->k4t.size() * sizeof(TileItem));
+  const size_t o_k1t = take(pl->k1t.size() * sizeof(TileItem));
+  const size_t o_k1tl = take(pl->k1t_list.size() * sizeof(int));
+  const size_t o_k1to = take(pl->k1t_off.size() * sizeof(long long));
+  const size_t o_k1tp = take((size_t)std::max(1LL, pl->k1t_part_elems) * sizeof(float));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
   const size_t o_wsq = take((size_t)std::max(1LL, pl->wsq_elems) * sizeof(float));
@@ -2389,6 +2537,10 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_gbar = reinterpret_cast<unsigned*>(b + o_gbar);
   pl->d_k4 = reinterpret_cast<RowItem*>(b + o_k4);
   pl->d_k4t = reinterpret_cast<TileItem*>(b + o_k4t);
+  pl->d_k1t = reinterpret_cast<TileItem*>(b + o_k1t);
+  pl->d_k1t_list = reinterpret_cast<int*>(b + o_k1tl);
+  pl->d_k1t_off = reinterpret_cast<long long*>(b + o_k1to);
+  pl->d_k1t_part = reinterpret_cast<float*>(b + o_k1tp);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
   pl->d_wsq = reinterpret_cast<float*>(b + o_wsq);
@@ -2420,6 +2572,9 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gbar, 0, 4 * sizeof(unsigned));
   if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = up(pl->d_k4t, pl->k4t.data(), pl->k4t.size() * sizeof(TileItem));
+  if (ce == cudaSuccess) ce = up(pl->d_k1t, pl->k1t.data(), pl->k1t.size() * sizeof(TileItem));
+  if (ce == cudaSuccess) ce = up(pl->d_k1t_list, pl->k1t_list.data(), pl->k1t_list.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_k1t_off, pl->k1t_off.data(), pl->k1t_off.size() * sizeof(long long));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_split_cnt, 0, std::max<size_t>(16, pl->splits.size() * sizeof(int)));
@@ -2465,7 +2620,7 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
     return c;
   };
   const bool any_fused = pl->n_tall < pl->nmat;
-  o->launches_ef_p = (pl->k1.empty() && pl->nbias == 0) ? 0 : 1;
+  o->launches_ef_p = ((pl->k1.empty() && pl->nbias == 0) ? 0 : 1) + (pl->k1t.empty() ? 0 : 2);
   o->launches_orthogonalize = (pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0;
   o->launches_orthogonalize = ((pl->small_list.size() + (pl->nbias > 0)) > 0 ? 1 : 0) +
                               (pl->gram_items.empty() ? 0 : 2);
@@ -2517,9 +2672,31 @@ cudaError_t launch_ex(Kern kern, int grid, int block, size_t smem, cudaStream_t 
 }
 
 template <int RM>
+int run_k1_tiles(const psgd_plan* pl, const float* g, const float* e, float* work, const float* q, float* p,
+                 cudaStream_t st) {
+  if (pl->k1t.empty()) return PSGD_OK;
+  const long long flag_slot = pl->flag_off + pl->nflags - 1;
+  PSGD_CUDA_CHECK(cudaMemsetAsync(p + flag_slot, 0, sizeof(float), st));
+  const int nitems = (int)pl->k1t.size();
+  k1_tile<RM><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k1t, nitems, pl->d_k1t_off, g, e, work, q,
+                                                     pl->d_k1t_part);
+  PSGD_CUDA_CHECK(cudaGetLastError());
+  long long maxnr = 0;
+  for (int mi : pl->k1t_list) maxnr = std::max(maxnr, (long long)pl->mats[mi].n * pl->mats[mi].r);
+  dim3 grid((unsigned)std::min<long long>((maxnr + 255) / 256, 64), (unsigned)pl->k1t_list.size());
+  k1_tile_reduce<<<grid, 256, 0, st>>>(pl->d_mats, pl->d_k1t_list, pl->d_k1t_off, pl->d_k1t_part, p, flag_slot);
+  PSGD_CUDA_CHECK(cudaGetLastError());
+  return PSGD_OK;
+}
+
+template <int RM>
 int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, const float* q, float* p,
            float* phat, const double* repl, const float* bias_g, int* status, cudaStream_t st) {
   const int grid = (int)pl->k1_beg.size() - 1;
+  {
+    const int rc = run_k1_tiles<RM>(pl, g, e, work, q, p, st);
+    if (rc) return rc;
+  }
   if (pl->k1.empty() && pl->nbias == 0) return PSGD_OK;
   auto kern = k1_ef_p<RM>;
   const size_t smem = pl->k1l.total;
