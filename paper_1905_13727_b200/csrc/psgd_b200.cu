@@ -1955,6 +1955,95 @@ __global__ void __launch_bounds__(256) k1_tile_reduce(const MatDev* __restrict__
   if (threadIdx.x == 0 && s_bad) P[flag_slot] = 1.f;
 }
 
+// K3 column tiles for tall matrices with m % 4 == 0: a warp owns 128 columns x
+// K3T_ROWS rows, accumulates q_w = delta^T P-hat for its 4 columns x r in
+// registers (P-hat rows are warp-broadcast loads), and writes one partial per
+// (row block, column); k3_tile_reduce sums the row blocks in order into q
+// (column-major Q layout; compressors.py:339).
+constexpr int K3T_ROWS = 256;
+
+template <int RM>
+__global__ void __launch_bounds__(kThreads) k3_tile(const MatDev* __restrict__ mats, const TileItem* __restrict__ items,
+                                                    int nitems, const long long* __restrict__ part_off,
+                                                    const float* __restrict__ work, const float* __restrict__ Phat,
+                                                    float* __restrict__ part, const int* __restrict__ status) {
+  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
+  const int lane = threadIdx.x & 31;
+  const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (wi >= nitems) return;
+  const TileItem it = items[wi];
+  const MatDev md = mats[it.mat];
+  const int r = md.r, m = md.m;
+  const int col = it.c0 + 4 * lane;
+  const bool ok = col < m;
+  float qp[4][RM];
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int k = 0; k < RM; ++k) qp[v][k] = 0.f;
+  const float* __restrict__ pr = Phat + md.p_off + (long long)it.row0 * r;
+  const long long base = md.flat_off + (long long)it.row0 * m + col;
+  for (int i0 = 0; i0 < it.nrows; i0 += 8) {
+    float4 d[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      d[u] = (ok && i0 + u < it.nrows) ? __ldcs(reinterpret_cast<const float4*>(work + base + (long long)(i0 + u) * m))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (i0 + u >= it.nrows) break;
+      float p[RM];  // the P-hat row: one address per warp (broadcast), float4 when r == RM % 4 == 0
+      if (RM % 4 == 0 && r == RM) {
+#pragma unroll
+        for (int k4 = 0; k4 < RM / 4; ++k4) {
+          const float4 pv = __ldg(reinterpret_cast<const float4*>(pr + (long long)(i0 + u) * r) + k4);
+          p[4 * k4] = pv.x; p[4 * k4 + 1] = pv.y; p[4 * k4 + 2] = pv.z; p[4 * k4 + 3] = pv.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < RM; ++k) p[k] = k < r ? __ldg(pr + (long long)(i0 + u) * r + k) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < RM; ++k) {
+        qp[0][k] = fmaf(d[u].x, p[k], qp[0][k]);
+        qp[1][k] = fmaf(d[u].y, p[k], qp[1][k]);
+        qp[2][k] = fmaf(d[u].z, p[k], qp[2][k]);
+        qp[3][k] = fmaf(d[u].w, p[k], qp[3][k]);
+      }
+    }
+  }
+  if (!ok) return;
+  // partial layout [row block][k][column] (column-major like Q, ld = m)
+  float* pt = part + part_off[it.mat] + (long long)(it.row0 / K3T_ROWS) * r * m;
+#pragma unroll
+  for (int k = 0; k < RM; ++k)
+    if (k < r) *reinterpret_cast<float4*>(pt + (long long)k * m + col) = make_float4(qp[0][k], qp[1][k], qp[2][k], qp[3][k]);
+}
+
+__global__ void __launch_bounds__(256) k3_tile_reduce(const MatDev* __restrict__ mats, const int* __restrict__ list,
+                                                      const long long* __restrict__ part_off,
+                                                      const float* __restrict__ part, float* __restrict__ qout,
+                                                      const int* __restrict__ status) {
+  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
+  const int mi = list[blockIdx.y];
+  const MatDev md = mats[mi];
+  const long long mr = (long long)md.m * md.r;
+  const int nblk = (md.n + K3T_ROWS - 1) / K3T_ROWS;
+  const float* src = part + part_off[mi];
+  for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < mr; x += (long long)gridDim.x * blockDim.x) {
+    float s2 = 0.f;
+    for (int b0 = 0; b0 < nblk; b0 += 8) {
+      float y[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) y[u] = b0 + u < nblk ? __ldcs(src + (long long)(b0 + u) * mr + x) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s2 += y[u];
+    }
+    const long long k = x / md.m, c = x - k * md.m;
+    qout[md.q_off + k * md.qld + c] = s2;
+  }
+}
+
 // ============================================================================= tree mean
 struct TreeArgs {
   const float* p[PSGD_MAX_TREE];
@@ -2073,6 +2162,15 @@ struct psgd_plan {
   int* d_k1t_list = nullptr;
   long long* d_k1t_off = nullptr;
   float* d_k1t_part = nullptr;
+  // K3 column tiles (tall, m % 4 == 0): q partials per 256-row block
+  std::vector<TileItem> k3t;
+  std::vector<int> k3t_list;
+  std::vector<long long> k3t_off;
+  long long k3t_part_elems = 0;
+  TileItem* d_k3t = nullptr;
+  int* d_k3t_list = nullptr;
+  long long* d_k3t_off = nullptr;
+  float* d_k3t_part = nullptr;
   int n_tall = 0, n_tall_slabs = 0;
   long long wsq_elems = 0;
   // device
@@ -2110,6 +2208,11 @@ int lanes_log2_for(int m, int max_lg) {
   int lg = 2;
   while ((1LL << lg) < per && lg < max_lg) ++lg;
   return lg;
+}
+
+bool k3_tileable(const MatDev& md) {
+  static const bool off = getenv("PSGD_K3_TILE") && getenv("PSGD_K3_TILE")[0] == '0';
+  return !off && md.tall && md.m % 4 == 0 && md.flat_off % 4 == 0 && md.m >= 128;
 }
 
 bool k4_tileable(const MatDev& md) {
@@ -2406,6 +2509,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
         if (md.r != r) continue;
         const K3Cfg cf = k3_tall_config(md.n, md.m, r);
         if ((cf.nchunks > 1) != (tall == 1)) continue;
+        if (tall && k3_tileable(md)) continue;  // K3 column tiles instead
         const int CQ = 1 << cf.cql, C = CQ * cf.vec, RG = kThreads / CQ;
         const int nslab = (md.m + C - 1) / C;
         for (int s = 0; s < nslab; ++s) {
@@ -2437,6 +2541,16 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   }
   build_row_items(pl->mats, true, pl->k4, pl->g4);
   build_tile_items(pl->mats, pl->k4t, pl->g4t);
+  pl->k3t_off.assign(std::max(1, nmat), 0);
+  for (int mi = 0; mi < nmat; ++mi) {
+    const MatDev& md = pl->mats[mi];
+    if (!k3_tileable(md)) continue;
+    pl->k3t_list.push_back(mi);
+    pl->k3t_off[mi] = pl->k3t_part_elems;
+    pl->k3t_part_elems += (long long)((md.n + K3T_ROWS - 1) / K3T_ROWS) * md.m * md.r;
+    for (int r0 = 0; r0 < md.n; r0 += K3T_ROWS)
+      for (int c0 = 0; c0 < md.m; c0 += 128) pl->k3t.push_back({mi, r0, std::min(K3T_ROWS, md.n - r0), c0});
+  }
   build_row_items(pl->mats, false, pl->k5, pl->g5);
 
   // ---- fused W = 1 step eligibility and layout
@@ -2502,6 +2616,10 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_k1tl = take(pl->k1t_list.size() * sizeof(int));
   const size_t o_k1to = take(pl->k1t_off.size() * sizeof(long long));
   const size_t o_k1tp = take((size_t)std::max(1LL, pl->k1t_part_elems) * sizeof(float));
+  const size_t o_k3t = take(pl->k3t.size() * sizeof(TileItem));
+  const size_t o_k3tl = take(pl->k3t_list.size() * sizeof(int));
+  const size_t o_k3to = take(pl->k3t_off.size() * sizeof(long long));
+  const size_t o_k3tp = take((size_t)std::max(1LL, pl->k3t_part_elems) * sizeof(float));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
   const size_t o_wsq = take((size_t)std::max(1LL, pl->wsq_elems) * sizeof(float));
@@ -2541,6 +2659,10 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_k1t_list = reinterpret_cast<int*>(b + o_k1tl);
   pl->d_k1t_off = reinterpret_cast<long long*>(b + o_k1to);
   pl->d_k1t_part = reinterpret_cast<float*>(b + o_k1tp);
+  pl->d_k3t = reinterpret_cast<TileItem*>(b + o_k3t);
+  pl->d_k3t_list = reinterpret_cast<int*>(b + o_k3tl);
+  pl->d_k3t_off = reinterpret_cast<long long*>(b + o_k3to);
+  pl->d_k3t_part = reinterpret_cast<float*>(b + o_k3tp);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
   pl->d_wsq = reinterpret_cast<float*>(b + o_wsq);
@@ -2575,6 +2697,9 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_k1t, pl->k1t.data(), pl->k1t.size() * sizeof(TileItem));
   if (ce == cudaSuccess) ce = up(pl->d_k1t_list, pl->k1t_list.data(), pl->k1t_list.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_k1t_off, pl->k1t_off.data(), pl->k1t_off.size() * sizeof(long long));
+  if (ce == cudaSuccess) ce = up(pl->d_k3t, pl->k3t.data(), pl->k3t.size() * sizeof(TileItem));
+  if (ce == cudaSuccess) ce = up(pl->d_k3t_list, pl->k3t_list.data(), pl->k3t_list.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_k3t_off, pl->k3t_off.data(), pl->k3t_off.size() * sizeof(long long));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_split_cnt, 0, std::max<size_t>(16, pl->splits.size() * sizeof(int)));
@@ -2624,7 +2749,8 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->launches_orthogonalize = (pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0;
   o->launches_orthogonalize = ((pl->small_list.size() + (pl->nbias > 0)) > 0 ? 1 : 0) +
                               (pl->gram_items.empty() ? 0 : 2);
-  o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4) + nonempty(pl->g4t);
+  o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4) + nonempty(pl->g4t) +
+                     (pl->k3t.empty() ? 0 : 2);
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
   const bool fused_step = pl->ks_ok && !psgd_force_multi();
@@ -2901,6 +3027,23 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
     first = false;
     if (rc) return rc;
     bias_done = true;
+  }
+  if (!pl->k3t.empty()) {  // K3 column tiles (tall, m % 4 == 0), then the in-order block reduction
+    const int nitems = (int)pl->k3t.size();
+    switch (pl->rmax) {
+      case 1: k3_tile<1><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
+      case 2: k3_tile<2><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
+      case 4: k3_tile<4><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
+      case 8: k3_tile<8><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
+      default: k3_tile<16><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
+    }
+    PSGD_CUDA_CHECK(cudaGetLastError());
+    long long maxmr = 0;
+    for (int mi : pl->k3t_list) maxmr = std::max(maxmr, (long long)pl->mats[mi].m * pl->mats[mi].r);
+    dim3 grid((unsigned)std::min<long long>((maxmr + 255) / 256, 64), (unsigned)pl->k3t_list.size());
+    k3_tile_reduce<<<grid, 256, 0, st>>>(pl->d_mats, pl->d_k3t_list, pl->d_k3t_off, pl->d_k3t_part, q_out,
+                                         (const int*)status);
+    PSGD_CUDA_CHECK(cudaGetLastError());
   }
   for (const Group& gp : pl->g4) {
     rc = dispatch_r<RunK4>(gp.r, pl, (const RowItem*)pl->d_k4, gp, work, e, (const float*)p_hat,
