@@ -58,7 +58,7 @@ constexpr int kGsThreads = 1024;
 constexpr int kFusedNMax = 512;    // K3 fused path holds all rows of a slab
 constexpr int K1_STAGES = 3;       // max stages (the plan picks 2 or 3 and the stage size)
 constexpr int K1_CHUNK = 4608;     // floats of g (and of e) per chunk at the smallest stage
-constexpr int K1_QSLOT_CAP = 12288;  // floats of Q per smem slot (2 slots)
+constexpr int K1_QSLOT_CAP = 18432;  // floats of Q per smem slot (2 slots): 4 x 4608 (ResNet-18 r = 4)
 constexpr int K1_RED_ROWS = 16;
 constexpr int K1_STAGE_FLOATS = K1_CHUNK + 8;  // + misalignment slack of a chunk
 constexpr int K3_STAGES = 2;
@@ -2373,7 +2373,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     const long long red_b = 2LL * (K1_RED_ROWS * kConsWarps * pl->rmax + pl->rmax) * 4;
     const long long bar_b = (2 * K1_STAGES + 4) * 8 + 16;
     const long long min_stage = 2LL * 2 * (K1_CHUNK + 8) * 4;  // 2 stages of the smallest chunk
-    const long long cap = std::min<long long>(K1_QSLOT_CAP, ((227LL * 1024 - min_stage - red_b - bar_b - 512) / 8) & ~3LL);
+    static const long long qcap = getenv("PSGD_K1_QCAP") ? atoll(getenv("PSGD_K1_QCAP")) : K1_QSLOT_CAP;
+    const long long cap = std::min<long long>(qcap, ((227LL * 1024 - min_stage - red_b - bar_b - 512) / 8) & ~3LL);
     // one large slot (up to 128 KB) when some Q does not fit a double-buffered slot:
     // Q read from smem beats Q read through L1/L2 per element (stress: 4096 x 8)
     const long long cap1 = std::min<long long>(32768, ((227LL * 1024 - min_stage - red_b - bar_b - 512) / 4) & ~3LL);
