@@ -78,6 +78,18 @@ def sizes(specs, rank):
     return N, snr, smr, nb
 
 
+def use_all_host_threads():
+    """The CPU arms use every host core (torchrun exports OMP_NUM_THREADS=1)."""
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    try:
+        from threadpoolctl import threadpool_limits
+        import numpy  # noqa: F401  (load the BLAS the limit applies to)
+        threadpool_limits(limits=n, user_api="blas")
+    except Exception:
+        pass
+    return n
+
+
 def cpu_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -120,6 +132,7 @@ def run_reference(a):
         return 0
     specs = catalog_specs(a.workload)
     world = a.gpus
+    use_all_host_threads()
     budget = 150.0
     times = oracle_steps(specs, a.rank, world, a.steps, budget, warmup=a.warmup)
     ms = 1e3 * statistics.mean(times)
@@ -203,10 +216,14 @@ def run_ours(a):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != a.gpus:
         print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    if os.environ.get("PSGD_BENCH_BACKEND") == "gloo":  # test only: ranks may share a GPU
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # PSGD_BENCH_BACKEND=gloo exercises this path with several ranks on one GPU (test only)
+        backend = os.environ.get("PSGD_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     comm = DistributedCommunicator() if world > 1 else None
     specs = catalog_specs(a.workload)
     N, snr, smr, nbias = sizes(specs, a.rank)
@@ -380,6 +397,7 @@ def run_ours(a):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
+        use_all_host_threads()
         times = oracle_steps(specs, a.rank, 1, 1000, a.cpu_seconds, warmup=1)
         cores = cpu_threads()
         cpu = {"value": round(1e3 * statistics.median(times), 3), "unit": "ms/step", "cores": cores,
