@@ -332,38 +332,10 @@ def run_ours(a):
         nccl_us = 1e3 * e0.elapsed_time(e1) / 100
 
     # ---------------- e2e: host gradients in, M-hat + bias mean out, every step
-    g_host = torch.empty(eng.g[0].numel(), dtype=torch.float32, pin_memory=True)
-    g_host.copy_(eng.g[0].cpu())
-    b_host = torch.empty(eng.bias_g[0].numel(), dtype=torch.float32, pin_memory=True)
-    b_host.copy_(eng.bias_g[0].cpu())
-    m_host = torch.empty(eng.work[0].numel(), dtype=torch.float32, pin_memory=True)
-    bo_host = torch.empty(eng.bias_out.numel(), dtype=torch.float32, pin_memory=True)
-    st_host = torch.empty(1, dtype=torch.int32, pin_memory=True)
-    ke = max(3, min(a.steps, 20))
-    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
-    e_e = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
-    barrier()
-    for k in range(ke):
-        if flush is not None:
-            flush.zero_()
-        e_s[k].record(stream)
-        eng.g[0].copy_(g_host, non_blocking=True)
-        eng.bias_g[0].copy_(b_host, non_blocking=True)
-        eng.run()
-        m_host.copy_(eng.work[0], non_blocking=True)
-        bo_host.copy_(eng.bias_out, non_blocking=True)
-        st_host.copy_(eng.status, non_blocking=True)
-        e_e[k].record(stream)
-    barrier()
-    if int(st_host.item()) != 0:
-        raise RuntimeError(f"e2e step reported status {int(st_host.item())}")
-    e2e_local = statistics.mean(s.elapsed_time(e) for s, e in zip(e_s, e_e))
-    t = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t[0])
-    h2d = 4 * (g_host.numel() + b_host.numel())
-    d2h = 4 * (m_host.numel() + bo_host.numel() + st_host.numel())
+    if world == 1 and N * 4 < (2 << 30):  # the public host-pipelined API (pipeline.py)
+        e2e_ms, h2d, d2h = e2e_pipelined(specs, a, dev, flush, barrier, stream)
+    else:
+        e2e_ms, h2d, d2h = e2e_serial(eng, a, world, dev, flush, barrier, stream, dist)
 
     # ---------------- roofline (measured peaks)
     peaks = {}
@@ -438,6 +410,70 @@ def run_ours(a):
         dist.destroy_process_group()
     return 0
 
+
+
+def e2e_serial(eng, a, world, dev, flush, barrier, stream, dist):
+    """host gradients in (pinned), step, M-hat + bias mean out, on one stream"""
+    import statistics
+    import torch
+    g_host = torch.empty(eng.g[0].numel(), dtype=torch.float32, pin_memory=True)
+    g_host.copy_(eng.g[0].cpu())
+    b_host = torch.empty(eng.bias_g[0].numel(), dtype=torch.float32, pin_memory=True)
+    b_host.copy_(eng.bias_g[0].cpu())
+    m_host = torch.empty(eng.work[0].numel(), dtype=torch.float32, pin_memory=True)
+    bo_host = torch.empty(eng.bias_out.numel(), dtype=torch.float32, pin_memory=True)
+    st_host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+    ke = max(3, min(a.steps, 20))
+    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
+    e_e = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
+    barrier()
+    for k in range(ke):
+        if flush is not None:
+            flush.zero_()
+        e_s[k].record(stream)
+        eng.g[0].copy_(g_host, non_blocking=True)
+        eng.bias_g[0].copy_(b_host, non_blocking=True)
+        eng.run()
+        m_host.copy_(eng.work[0], non_blocking=True)
+        bo_host.copy_(eng.bias_out, non_blocking=True)
+        st_host.copy_(eng.status, non_blocking=True)
+        e_e[k].record(stream)
+    barrier()
+    if int(st_host.item()) != 0:
+        raise RuntimeError(f"e2e step reported status {int(st_host.item())}")
+    e2e_local = statistics.mean(s.elapsed_time(e) for s, e in zip(e_s, e_e))
+    t = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t[0])
+    h2d = 4 * (g_host.numel() + b_host.numel())
+    d2h = 4 * (m_host.numel() + bo_host.numel() + st_host.numel())
+    return e2e_ms, h2d, d2h
+
+
+def e2e_pipelined(specs, a, dev, flush, barrier, stream):
+    """HostPipelinedEngine: per parameter group, H2D || compression || D2H on three streams"""
+    import statistics
+    import torch
+    from paper_1905_13727_b200.pipeline import HostPipelinedEngine
+    pipe = HostPipelinedEngine(specs, a.rank, groups=int(os.environ.get("PSGD_E2E_GROUPS", "4")), seed=0, device=dev)
+    for t in pipe.g_host + pipe.bias_host:
+        t.normal_()
+    for _ in range(3):
+        pipe.step()
+    barrier()
+    ke = max(3, min(a.steps, 20))
+    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
+    e_e = [torch.cuda.Event(enable_timing=True) for _ in range(ke)]
+    for k in range(ke):
+        if flush is not None:
+            flush.zero_()
+        e_s[k].record(stream)
+        pipe.step()
+        e_e[k].record(stream)
+    barrier()
+    pipe.check()
+    return statistics.mean(s.elapsed_time(e) for s, e in zip(e_s, e_e)), pipe.h2d_bytes, pipe.d2h_bytes
 
 def main():
     a = parse_args()
