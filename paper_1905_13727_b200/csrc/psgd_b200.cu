@@ -2044,6 +2044,101 @@ __global__ void __launch_bounds__(256) k3_tile_reduce(const MatDev* __restrict__
   }
 }
 
+// K4 column tiles for m % 4 == 2 (LSTM, m = 650): consecutive rows alternate
+// between two 16-byte alignment classes, so even-aligned rows use float4 columns
+// c0 + 4l.. and odd-aligned rows c0 + 2 + 4l..; each lane keeps both Q blocks in
+// registers.  Columns 0, 1 of odd-aligned rows (tile 0, lane 0) and the last two
+// columns of even-aligned rows (last tile) are scalar.
+template <int R, bool EXACT>
+__global__ void __launch_bounds__(kThreads) k4_tile2(const MatDev* __restrict__ mats, const TileItem* __restrict__ items,
+                                                     int beg, int end, float* __restrict__ work, float* __restrict__ e,
+                                                     const float* __restrict__ Phat, const float* __restrict__ qsrc,
+                                                     int write_mhat, const int* __restrict__ status) {
+  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
+  const int lane = threadIdx.x & 31;
+  const int wi = beg + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (wi >= end) return;
+  const TileItem it = items[wi];
+  const MatDev md = mats[it.mat];
+  const int r = EXACT ? R : md.r;
+  const int m = md.m;
+  const float* Qm = qsrc + md.q_off;
+  auto qcol = [&](int c, int k) { return (c < m && (EXACT || k < r)) ? __ldg(Qm + (long long)k * md.qld + c) : 0.f; };
+  const int ce = it.c0 + 4 * lane, co = it.c0 + 2 + 4 * lane;  // first column of the lane's float4, per class
+  float qe[4][R], qo[4][R], qx[2][R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      qe[v][k] = qcol(ce + v, k);
+      qo[v][k] = qcol(co + v, k);
+    }
+    qx[0][k] = qcol(0, k);
+    qx[1][k] = qcol(1, k);
+  }
+  const bool lead = it.c0 == 0 && lane == 0;  // scalar columns 0, 1 of odd-aligned rows
+  const float* __restrict__ pr = Phat + md.p_off + (long long)it.row0 * r;
+  for (int i0 = 0; i0 < it.nrows; i0 += 8) {
+    float4 d[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      d[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i0 + u < it.nrows) {
+        const long long o = md.flat_off + (long long)(it.row0 + i0 + u) * m;
+        const int c = (o & 3) ? co : ce;
+        if (c + 3 < m) d[u] = __ldcs(reinterpret_cast<const float4*>(work + o + c));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (i0 + u >= it.nrows) break;
+      const long long o = md.flat_off + (long long)(it.row0 + i0 + u) * m;
+      const bool odd = (o & 3) != 0;
+      const int c = odd ? co : ce;
+      float p[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) p[k] = (EXACT || k < r) ? __ldg(pr + (long long)(i0 + u) * r + k) : 0.f;
+      if (c + 3 < m) {
+        float mh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) mh[v] = fmaf(p[k], odd ? qo[v][k] : qe[v][k], mh[v]);
+        st_stream(reinterpret_cast<float4*>(e + o + c),
+                  make_float4(d[u].x - mh[0], d[u].y - mh[1], d[u].z - mh[2], d[u].w - mh[3]));
+        if (write_mhat) st_stream(reinterpret_cast<float4*>(work + o + c), make_float4(mh[0], mh[1], mh[2], mh[3]));
+      } else if (!odd && c < m) {  // last two columns of an even-aligned row
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          float mh = 0.f;
+#pragma unroll
+          for (int k = 0; k < R; ++k) mh = fmaf(p[k], qe[v][k], mh);
+          const float dv = work[o + c + v];
+          st_stream(e + o + c + v, dv - mh);
+          if (write_mhat) st_stream(work + o + c + v, mh);
+        }
+      }
+      if (odd && lead) {  // columns 0, 1 of an odd-aligned row
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          float mh = 0.f;
+#pragma unroll
+          for (int k = 0; k < R; ++k) mh = fmaf(p[k], qx[v][k], mh);
+          const float dv = work[o + v];
+          st_stream(e + o + v, dv - mh);
+          if (write_mhat) st_stream(work + o + v, mh);
+        }
+      }
+    }
+  }
+}
+
+template <int R, bool EXACT>
+struct RunK4T2 {
+  static int run(const psgd_plan* pl, const Group& gp, float* work, float* e, const float* phat, const float* q,
+                 int write_mhat, const int* status, cudaStream_t st);
+};
+
 // ============================================================================= tree mean
 struct TreeArgs {
   const float* p[PSGD_MAX_TREE];
@@ -2151,7 +2246,7 @@ struct psgd_plan {
   std::vector<RowItem> k4, k5;
   std::vector<Group> g4, g5;
   std::vector<TileItem> k4t;   // K4 column tiles (tall, m % 4 == 0)
-  std::vector<Group> g4t;
+  std::vector<Group> g4t, g4t2;
   TileItem* d_k4t = nullptr;
   // K1 column tiles (matrices whose Q block is not staged): items, matrix list, partials
   std::vector<TileItem> k1t;
@@ -2220,6 +2315,11 @@ bool k4_tileable(const MatDev& md) {
   return !off && md.tall && md.m % 4 == 0 && md.flat_off % 4 == 0 && md.m >= 128;
 }
 
+bool k4_tileable2(const MatDev& md) {  // two alignment classes (k4_tile2)
+  static const bool off = getenv("PSGD_K4_TILE2") && getenv("PSGD_K4_TILE2")[0] == '0';
+  return !off && md.tall && md.m % 4 == 2 && md.flat_off % 4 == 0 && md.m >= 128;
+}
+
 void build_tile_items(const std::vector<MatDev>& mats, std::vector<TileItem>& items, std::vector<Group>& groups) {
   std::vector<int> rs;
   for (auto& md : mats)
@@ -2248,7 +2348,7 @@ void build_row_items(const std::vector<MatDev>& mats, bool tall_only, std::vecto
     for (int mi = 0; mi < (int)mats.size(); ++mi) {
       const MatDev& md = mats[mi];
       if (md.r != r || (tall_only && !md.tall)) continue;
-      if (tall_only && k4_tileable(md)) continue;  // K4 column tiles instead
+      if (tall_only && (k4_tileable(md) || k4_tileable2(md))) continue;  // K4 column tiles instead
       const int lg = lanes_log2_for(md.m, 5);
       const int rpp = 32 >> lg;
       int rows = std::max(1, kRowItemElems / md.m);
@@ -2542,6 +2642,22 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   }
   build_row_items(pl->mats, true, pl->k4, pl->g4);
   build_tile_items(pl->mats, pl->k4t, pl->g4t);
+  {  // k4_tile2 items go after the k4_tile items in the same array, in their own groups
+    std::vector<int> rs;
+    for (auto& md : pl->mats)
+      if (k4_tileable2(md) && std::find(rs.begin(), rs.end(), md.r) == rs.end()) rs.push_back(md.r);
+    for (int r : rs) {
+      Group gp{r, (int)pl->k4t.size(), 0, 0, 0};
+      for (int mi = 0; mi < nmat; ++mi) {
+        const MatDev& md = pl->mats[mi];
+        if (md.r != r || !k4_tileable2(md)) continue;
+        for (int r0 = 0; r0 < md.n; r0 += K4T_ROWS)
+          for (int c0 = 0; c0 < md.m; c0 += 128) pl->k4t.push_back({mi, r0, std::min(K4T_ROWS, md.n - r0), c0});
+      }
+      gp.end = (int)pl->k4t.size();
+      pl->g4t2.push_back(gp);
+    }
+  }
   pl->k3t_off.assign(std::max(1, nmat), 0);
   for (int mi = 0; mi < nmat; ++mi) {
     const MatDev& md = pl->mats[mi];
@@ -2751,6 +2867,7 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->launches_orthogonalize = ((pl->small_list.size() + (pl->nbias > 0)) > 0 ? 1 : 0) +
                               (pl->gram_items.empty() ? 0 : 2);
   o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4) + nonempty(pl->g4t) +
+                     nonempty(pl->g4t2) +
                      (pl->k3t.empty() ? 0 : 2);
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
@@ -2877,6 +2994,17 @@ struct RunK45Mode {
 
 template <int R, bool EXACT>
 using RunK4 = RunK45Mode<0>::F<R, EXACT>;
+
+template <int R, bool EXACT>
+int RunK4T2<R, EXACT>::run(const psgd_plan* pl, const Group& gp, float* work, float* e, const float* phat,
+                           const float* q, int write_mhat, const int* status, cudaStream_t st) {
+  const int nitems = gp.end - gp.beg;
+  if (nitems <= 0) return PSGD_OK;
+  k4_tile2<R, EXACT><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k4t, gp.beg, gp.end, work, e, phat, q,
+                                                              write_mhat, status);
+  PSGD_CUDA_CHECK(cudaGetLastError());
+  return PSGD_OK;
+}
 
 template <int R, bool EXACT>
 struct RunK4T {
@@ -3055,6 +3183,11 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
   for (const Group& gp : pl->g4t) {
     rc = dispatch_r<RunK4T>(gp.r, pl, gp, work, e, (const float*)p_hat, (const float*)q_out,
                             pl->world == 1 ? 1 : 0, (const int*)status, st);
+    if (rc) return rc;
+  }
+  for (const Group& gp : pl->g4t2) {
+    rc = dispatch_r<RunK4T2>(gp.r, pl, gp, work, e, (const float*)p_hat, (const float*)q_out,
+                             pl->world == 1 ? 1 : 0, (const int*)status, st);
     if (rc) return rc;
   }
   return PSGD_OK;

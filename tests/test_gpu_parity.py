@@ -125,8 +125,8 @@ def test_odd_shapes_and_rank_clamps():
     specs = [ParamSpec("a", (8, 6)), ParamSpec("b", (16, 3, 2, 2)), ParamSpec("bias", (10,)),
              ParamSpec("c", (3, 20)), ParamSpec("d", (513, 7)), ParamSpec("e", (5, 1)),
              ParamSpec("f", (700, 33)), ParamSpec("g", (1, 9)), ParamSpec("h", (1030, 1030)),
-             ParamSpec("t", (900, 132)), ParamSpec("u", (96, 2056)),
-             ParamSpec("bias2", (3,))]  # t: K4 column tiles (last tile 4 cols); u: K1 column tiles at r >= 8
+             ParamSpec("t", (900, 132)), ParamSpec("u", (96, 2056)), ParamSpec("v", (700, 130)),
+             ParamSpec("bias2", (3,))]  # t: K4 column tiles (last tile 4 cols); u: K1 column tiles at r >= 8; v: K4 two-alignment tiles
     for rank, world in [(1, 1), (3, 1), (8, 2), (12, 1), (16, 3)]:
         errs, _ = run_synced_step(specs, rank, world)
         assert max(errs.values()) <= TOL, (rank, world, errs)
