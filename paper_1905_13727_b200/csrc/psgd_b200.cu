@@ -58,7 +58,8 @@ constexpr int kGsThreads = 1024;
 constexpr int kFusedNMax = 512;    // K3 fused path holds all rows of a slab
 constexpr int K1_STAGES = 3;       // max stages (the plan picks 2 or 3 and the stage size)
 constexpr int K1_CHUNK = 4608;     // floats of g (and of e) per chunk at the smallest stage
-constexpr int K1_QSLOT_CAP = 18432;  // floats of Q per smem slot (2 slots): 4 x 4608 (ResNet-18 r = 4)
+constexpr int K1_QSLOT_CAP = 12288;  // floats of Q per smem slot (2 slots)
+constexpr int K1_QBIG_CAP = 18432;   // one large slot up to this (ResNet-18 r = 4: 4 x 4608); beyond: column tiles
 constexpr int K1_RED_ROWS = 16;
 constexpr int K1_STAGE_FLOATS = K1_CHUNK + 8;  // + misalignment slack of a chunk
 constexpr int K3_STAGES = 2;
@@ -2477,13 +2478,17 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     const long long cap = std::min<long long>(qcap, ((227LL * 1024 - min_stage - red_b - bar_b - 512) / 8) & ~3LL);
     // one large slot (up to 128 KB) when some Q does not fit a double-buffered slot:
     // Q read from smem beats Q read through L1/L2 per element (stress: 4096 x 8)
-    const long long cap1 = std::min<long long>(32768, ((227LL * 1024 - min_stage - red_b - bar_b - 512) / 4) & ~3LL);
-    // measured slower on the stress set (one row per chunk behind a 128 KB slot), so
-    // opt-in only: PSGD_K1_BIGQ=1
-    bool big = false;
+    const long long cap1 = std::min<long long>(K1_QBIG_CAP, ((227LL * 1024 - min_stage - red_b - bar_b - 512) / 4) & ~3LL);
+    // one large Q slot when a Q block exceeds the double-buffered slot but not 18432
+    // floats (ResNet-18 r = 4: 90 vs 95 us); larger blocks (stress) go to the K1 column
+    // tiles, which beat a single 128 KB slot there (9.9 vs 22 ms).  PSGD_K1_BIGQ=0/1 forces.
     const char* bq = getenv("PSGD_K1_BIGQ");
-    if (bq && bq[0] == '1')
-      for (auto& md : pl->mats) big |= (long long)md.r * md.qld > cap;
+    bool big = false;
+    for (auto& md : pl->mats) {
+      const long long qb = (long long)md.r * md.qld;
+      big |= qb > cap && qb <= K1_QBIG_CAP;
+    }
+    if (bq) big = bq[0] == '1';
     L.nq = big ? 1 : 2;
     long long qslot = 4;
     for (auto& md : pl->mats) {
