@@ -706,7 +706,7 @@ constexpr int K2_THREADS = 256;
 // items: [warp blocks | CTA blocks | bias blocks].  A warp block orthogonalises
 // up to 8 small matrices, one per warp, reductions by shuffles only; a CTA
 // block one medium matrix with 8 warps and a __syncthreads per reduction.
-__global__ void __launch_bounds__(K2_THREADS)
+__global__ void __launch_bounds__(K2_THREADS, 1)
     k2_gs(const MatDev* __restrict__ mats, const int* __restrict__ wlist, int nw_items, int nwblocks,
           const int* __restrict__ clist, int nc_items, int wregion, const float* __restrict__ P,
           float* __restrict__ Phat, int divisor, const double* __restrict__ repl, float* __restrict__ bias_out,
