@@ -2869,8 +2869,12 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   const bool any_fused = pl->n_tall < pl->nmat;
   o->launches_ef_p = ((pl->k1.empty() && pl->nbias == 0) ? 0 : 1) + (pl->k1t.empty() ? 0 : 2);
   o->launches_orthogonalize = (pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0;
-  o->launches_orthogonalize = ((pl->small_list.size() + (pl->nbias > 0)) > 0 ? 1 : 0) +
-                              (pl->gram_items.empty() ? 0 : 2);
+  {  // same rule as psgd_q_ef: k2_gs runs for small matrices, or for the bias unless K3 takes it
+    const bool tall_only = pl->world == 1;
+    const bool small = (tall_only ? pl->wlist_t.size() + pl->clist_t.size() : pl->wlist.size() + pl->clist.size()) > 0;
+    const bool bias_in_k3 = !small && !pl->gram_items.empty() && !pl->g3.empty();
+    o->launches_orthogonalize = ((small || (pl->nbias > 0 && !bias_in_k3)) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 2);
+  }
   o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4) + nonempty(pl->g4t) +
                      nonempty(pl->g4t2) +
                      (pl->k3t.empty() ? 0 : 2);
@@ -3147,11 +3151,16 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
 #else
   // K2: P-hat of the matrices K1 did not orthogonalise (all of them when W > 1) + bias mean
   const bool k2 = pl->need_k2 || pl->world > 1 || divisor != 1;
+  // every matrix in Gram space (k2_gram checks the non-finite flags) and a K3 slab launch
+  // follows: that launch writes the bias mean, so k2_gs is not launched for the bias alone
+  const bool tall_only = pl->world == 1 && divisor == 1;
+  const bool k2_small = (tall_only ? pl->wlist_t.size() + pl->clist_t.size() : pl->wlist.size() + pl->clist.size()) > 0;
+  const bool bias_in_k3 = k2 && !k2_small && !pl->gram_items.empty() && !pl->g3.empty();
   if (k2) {
-    rc = launch_k2(pl, pl->world == 1 && divisor == 1, true, p, p_hat, divisor, repl, bias_out, (int*)status, st);
+    rc = launch_k2(pl, tall_only, !bias_in_k3, p, p_hat, divisor, repl, bias_out, (int*)status, st);
     if (rc) return rc;
   }
-  bool bias_done = k2;
+  bool bias_done = k2 && !bias_in_k3;
 #endif
   bool first = true;
   for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab
