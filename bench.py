@@ -90,6 +90,55 @@ def use_all_host_threads():
     return n
 
 
+def workload_name(workload, rank, world):
+    """config.workload: the same string for both arms (ours and --impl reference)."""
+    return f"{workload} rank {rank}, W={world}"
+
+
+def host_info():
+    """lscpu model, numpy and BLAS versions (state the CPU the baseline ran on)."""
+    import numpy as np
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        for info in threadpool_info():
+            if info.get("user_api") == "blas":
+                blas = f"{info.get('internal_api')} {info.get('version')}"
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "numpy": np.__version__, "blas": blas}
+
+
+def cpu_baseline_leg(specs, rank, world, budget_s, workload):
+    """The float64 oracle port timed on the host: all BLAS threads, then 1 thread."""
+    use_all_host_threads()
+    times = oracle_steps(specs, rank, world, 1000, budget_s, warmup=1)
+    cores = cpu_threads()
+    one = None
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1, user_api="blas"):
+            t1 = oracle_steps(specs, rank, world, 1000, max(2.0, budget_s / 3), warmup=1)
+        one = round(1e3 * statistics.median(t1), 3)
+    except Exception:
+        pass
+    return {"value": round(1e3 * statistics.median(times), 3), "unit": "ms/step", "cores": cores,
+            "kind": "port", "value_1_thread": one,
+            "sample": f"{len(times)} full {workload} r={rank} W={world} steps (median), float64 numpy "
+                      f"oracle of optimizer.py:110-129 on {cores} OpenBLAS threads, ~{budget_s:.0f}s",
+            **host_info()}
+
+
 def cpu_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -144,10 +193,10 @@ def run_reference(a):
         "steps": len(times), "warmup": a.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{a.workload} rank {a.rank}, W={world} simulated workers (CPU)",
-                   "rank": a.rank, "world": world},
+        "config": {"workload": workload_name(a.workload, a.rank, world),
+                   "detail": f"{world} simulated workers on the host CPU", "rank": a.rank, "world": world},
         "cpu_baseline": {"value": round(ms, 4), "unit": "ms/step", "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, **host_info()},
         "e2e": {"value": round(ms, 4), "unit": "ms/step", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -231,8 +280,9 @@ def run_ours(a):
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
     eng.g[0].normal_(generator=gen)
     eng.bias_g[0].normal_(generator=gen)
-    use_graph = world == 1 and not a.no_graph
-    if use_graph:
+    # (gloo, a test-only transport, runs on the host and cannot be captured)
+    use_graph = not a.no_graph and not (world > 1 and os.environ.get("PSGD_BENCH_BACKEND") == "gloo")
+    if use_graph:  # at N > 1 the graph holds the two NCCL all-reduces too
         eng.capture()
     flush = None if a.no_flush else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -267,11 +317,20 @@ def run_ours(a):
     barrier()
     clk = clocks.stop()
     per = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    # back-to-back steps (no flush between them): the L2 keeps part of the previous step
+    bb0, bb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    bb0.record(stream)
+    for _ in range(a.steps):
+        eng.run()
+    bb1.record(stream)
+    barrier()
+    ms_b2b = bb0.elapsed_time(bb1) / a.steps
     ms_local = statistics.mean(per)
-    t = torch.tensor([ms_local, statistics.median(per)], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms_local, statistics.median(per), ms_b2b], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, ms_median = float(t[0]), float(t[1])
+    ms, ms_median, ms_b2b = float(t[0]), float(t[1]), float(t[2])
     eng.check()
     info = eng.plan.info
     launches_per_step = (info.launches_step_single if world == 1 else
@@ -291,7 +350,7 @@ def run_ours(a):
         eng.status.zero_()
         ev[0].record(stream)
         _lib.check(lib.psgd_ef_p(h, ptr(eng.g[0]), ptr(eng.e[0]), ptr(eng.work[0]), ptr(eng.Q), ptr(eng.P[0]),
-                                 ptr(eng.Phat), ptr(eng.repl), ptr(eng.bias_g[0]), ptr(eng.status), sp), "ef_p")
+                                 ptr(eng.bias_g[0]), ptr(eng.status), sp), "ef_p")
         ev[1].record(stream)
         if world > 1:
             comm.all_reduce_sum_(eng.P[0])
@@ -363,19 +422,18 @@ def run_ours(a):
     except Exception:
         pass
     b_alg = 24 * N + 20 * snr + 16 * smr
-    t_roof_us = b_alg / (hbm * 1e9) * 1e6
-    if world > 1:
-        t_roof_us += 2 * (world - 1) / world * 4 * (snr + nbias + smr) / 900e9 * 1e6
+    t_hbm_us = b_alg / (hbm * 1e9) * 1e6
+    # ring all-reduce bytes per GPU per step over NVLink 5 (900 GB/s per direction)
+    nvl_bytes = 2 * (world - 1) / world * 4 * (snr + nbias + smr) if world > 1 else 0.0
+    t_nvl_us = nvl_bytes / 900e9 * 1e6
+    t_roof_us = t_hbm_us + t_nvl_us
 
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu:
-        use_all_host_threads()
-        times = oracle_steps(specs, a.rank, 1, 1000, a.cpu_seconds, warmup=1)
-        cores = cpu_threads()
-        cpu = {"value": round(1e3 * statistics.median(times), 3), "unit": "ms/step", "cores": cores,
-               "kind": "port",
-               "sample": f"{len(times)} full {a.workload} r={a.rank} W=1 steps (median), float64 numpy "
-                         f"oracle of optimizer.py:110-129 on {cores} OpenBLAS threads, ~{a.cpu_seconds:.0f}s"}
+    if rank == 0 and not a.no_cpu:  # N > 1: rank 0 times the W = N simulated-worker oracle
+        cpu = cpu_baseline_leg(specs, a.rank, world, a.cpu_seconds if world == 1 else a.cpu_seconds / 2,
+                               a.workload)
+    if world > 1:
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -384,17 +442,23 @@ def run_ours(a):
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: seeded N(0,1) fp32 gradients of the catalog shapes, resident in HBM",
             "impl": "ours",
-            "config": {"workload": f"{a.workload} rank {a.rank}, one worker per GPU "
-                                   + ("(configs[1], no collective)" if world == 1 else "(configs[2], NCCL AR of packed P, q)"),
+            "config": {"workload": workload_name(a.workload, a.rank, world),
+                       "detail": "one worker per GPU " + ("(configs[1], no collective)" if world == 1
+                                                          else "(configs[2], NCCL all-reduce of packed P and q, "
+                                                               "captured in the CUDA graph)"),
                        "rank": a.rank, "world": world, "matrix_elems": N, "bias_elems": nbias,
                        "l2": "flushed (256 MiB write) before every timed step" if flush is not None else "not flushed",
-                       "cuda_graph": use_graph, "median_ms": round(ms_median, 5)},
+                       "cuda_graph": use_graph, "median_ms": round(ms_median, 5),
+                       "back_to_back_ms": round(ms_b2b, 5)},
             "roofline": {"bound": "hbm", "kernel": "k1_ef_p (psgd_ef_p)", "achieved": round(achieved, 1),
                          "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                          "algorithmic_bytes": dom_bytes, "peak_source": peak_src,
                          "traffic_source": "profiles/ncu_summary.json (ncu --set full, one launch)"},
-            "step_roofline": {"algorithmic_bytes": b_alg, "t_roof_us": round(t_roof_us, 2),
-                              "t_measured_us": round(ms * 1e3, 2), "frac": round(t_roof_us / (ms * 1e3), 4)},
+            "step_roofline": {"algorithmic_bytes": b_alg, "t_hbm_us": round(t_hbm_us, 2),
+                              "nvlink_bytes_per_gpu": round(nvl_bytes), "t_nvlink_us": round(t_nvl_us, 3),
+                              "t_roof_us": round(t_roof_us, 2), "t_measured_us": round(ms * 1e3, 2),
+                              "frac": round(t_roof_us / (ms * 1e3), 4),
+                              "frac_back_to_back": round(t_roof_us / (ms_b2b * 1e3), 4)},
             "kernels_ms": {k: round(v, 5) for k, v in kern_ms.items()},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/step", "h2d_bytes_per_step": h2d,

@@ -43,10 +43,11 @@ extern "C" {
 /* device status word bits (int32, caller-owned; psgd_ef_p resets it each step) */
 #define PSGD_STATUS_NONFINITE_GRAD  1  /* optimizer.py:72-76 NonFiniteGradient */
 #define PSGD_STATUS_NONFINITE_P     2  /* linalg.py:35-36 via orthogonalize(as_matrix) */
-#define PSGD_STATUS_REPLACEMENT     4  /* linalg.py:82-88 needed a 2nd replacement draw */
+#define PSGD_STATUS_REPLACEMENT     4  /* linalg.py:82-88 needed more replacement draws than the table holds */
 
 #define PSGD_MAX_RANK   16
 #define PSGD_MAX_TREE   64
+#define PSGD_REPL_ATTEMPTS 3  /* replacement draws per column held on the device (linalg.py:82-88 attempt 0..2) */
 
 typedef struct psgd_plan psgd_plan;
 
@@ -55,7 +56,7 @@ typedef struct {
     int64_t p_elems;      /* length of the packed P buffer: sum n*r_eff (aligned) + bias tail + flags */
     int64_t p_bias_off;   /* offset of the bias tail inside the P buffer */
     int64_t q_elems;      /* length of the packed Q buffers: sum r_eff * q_ld */
-    int64_t repl_elems;   /* doubles in the degenerate-column replacement table */
+    int64_t repl_elems;   /* doubles in the degenerate-column replacement table (PSGD_REPL_ATTEMPTS draws per column) */
     int64_t nbias;        /* bias scalars carried uncompressed */
     int32_t nmat;
     int32_t rank;
@@ -67,19 +68,20 @@ typedef struct {
     int32_t launches_orthogonalize;
     int32_t launches_q_ef;
     int32_t launches_decompress;
-    int32_t launches_step_single; /* psgd_step_single: 1 when the fused single-kernel step applies */
-    int32_t fused_step;           /* psgd_step_single runs one cooperative kernel: 2 = k_resident (delta on chip), 1 = k_step_w1 */
+    int32_t launches_step_single; /* kernel launches issued by one psgd_step_single call */
+    int32_t pad;
 } psgd_plan_info;
 
 typedef struct {
     int64_t flat_off;     /* element offset of the n x m row-major matrix in g / e / work */
     int64_t p_off;        /* element offset of its n x r_eff P block */
     int64_t q_off;        /* element offset of its Q block: column-major, (j, k) at q_off + k * q_ld + j */
-    int64_t repl_off;     /* double offset of its r_eff replacement columns (column-major, n each) */
+    int64_t repl_off;     /* double offset of its replacement table: column j, attempt a (linalg.py:54-58)
+                             at repl_off + (a * repl_cols + j) * n; shared by every matrix with the same n */
     int32_t n, m, r_eff;
     int32_t tall;         /* 1: n > fused limit, q via split-n partials + separate EF pass */
     int32_t q_ld;         /* column stride of the Q block (m rounded up to a multiple of 4) */
-    int32_t pad;
+    int32_t repl_cols;    /* columns per attempt in its replacement table (max r_eff over matrices with this n) */
 } psgd_matrix_info;
 
 /* Plan: shapes -> packed layout, per-kernel work lists, plan-owned scratch.
@@ -98,15 +100,10 @@ int psgd_plan_matrix(const psgd_plan* plan, int32_t i, psgd_matrix_info* out);
  * g, e: flat_elems (e may be NULL: error feedback off, optimizer.py:118-119).
  * work: out delta.  q: warm-start Q (q_elems).  p: out P (p_elems; the bias
  * tail receives bias_g, the flag tail one non-finite flag per CTA, so the P
- * all-reduce carries them to every worker).  status: reset to 0; raised to
- * PSGD_STATUS_NONFINITE_GRAD by the last CTA when any flag is set.
- * World-1 plans also orthogonalise (compressors.py:338, linalg.py:61-90) every
- * matrix with n <= 512 and r_eff <= 4 as soon as its last chunk is done,
- * writing P-hat to p_hat (seeded replacement columns from repl); p_hat and
- * repl may be NULL when the plan's world > 1. */
+ * all-reduce carries them to every worker; K2 raises PSGD_STATUS_NONFINITE_GRAD
+ * from them).  status: reset to 0 by every call. */
 int psgd_ef_p(const psgd_plan* plan, const float* g, const float* e, float* work,
-              const float* q, float* p, float* p_hat, const double* repl, const float* bias_g,
-              int32_t* status, void* stream);
+              const float* q, float* p, const float* bias_g, int32_t* status, void* stream);
 
 /* K2 — standalone Gram-Schmidt: replaces compressors.py:337-338 after the sum,
  * P = P_sum / divisor (comm.py:97-98; divisor 1 = the W=1 copy), then
@@ -117,6 +114,13 @@ int psgd_ef_p(const psgd_plan* plan, const float* g, const float* e, float* work
  * serves linalg.orthogonalize and callers that want P-hat alone. */
 int psgd_orthogonalize(const psgd_plan* plan, const float* p, int32_t divisor, const double* repl,
                        float* p_hat, float* bias_out, int32_t* status, void* stream);
+
+/* linalg.orthogonalize (linalg.py:61-90) on float64 input, computed in float64
+ * exactly as the reference (no fp32 rounding of the input): P-hat of the plan's
+ * matrix i (n x r_eff, row-major doubles) with the seeded replacement loop
+ * (linalg.py:82-88) drawing from `repl`.  p and p_hat may alias. */
+int psgd_orthogonalize_f64(const psgd_plan* plan, int32_t i, const double* p, const double* repl,
+                           double* p_hat, int32_t* status, void* stream);
 
 /* K3 (+ tall-matrix kernels) — replaces compressors.py:338 (P-hat = GS(P / W)),
  * :339 (q_w = delta^T P-hat), :376-378 (locals = P-hat q_w^T) and
@@ -154,18 +158,6 @@ int psgd_tree_mean(const float* const* bufs, int32_t nbuf, int64_t count, float*
 int psgd_momentum_step(const psgd_plan* plan, float* params, float* mom, const float* update,
                        float* bias_params, float* bias_mom, const float* bias_update, float lr,
                        float momentum, const int32_t* status, void* stream);
-
-/* Diagnostics: with PSGD_RES_TIMING=1 set when the plan was created, copies 8
- * globaltimer stamps per CTA of the last resident step (start, end of phase 1,
- * end of the reductions / Gram-Schmidt, after the grid barrier, end); returns
- * the number of values copied (0 when the plan has no resident step). */
-int psgd_debug_resident_times(const psgd_plan* plan, int64_t* out, int64_t cap);
-
-/* Host-only check of the on-chip-resident step's partition for a catalog (no GPU
- * needed): returns 1 and stats = {CTAs, slabs, max/avg CTA load, max slots used,
- * slot capacity}, or 0 and the reason in `why`. */
-int psgd_resident_dryrun(int32_t nmat, const int64_t* n, const int64_t* m, int32_t rank, int32_t nsm,
-                         double* stats, char* why, int32_t why_cap);
 
 const char* psgd_last_error(void);
 int32_t psgd_version(void);

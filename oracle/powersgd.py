@@ -429,21 +429,35 @@ def momentum_update(params, buffers, updates, lr, momentum):
 # --------------------------------------------------------------------------- desk problem (known-answer pin)
 
 class LeastSquares:
-    """problems.py:53-116 (noise 0, no target spectrum) with the CLI defaults
-    of problems.py:173-178 (n=24, m=32, 256 samples).  Only used to replay the
-    reference's GOLDEN_TRAIN_CSV (pkg/tests/test_cli.py:10-17)."""
+    """problems.py:53-116 (noise 0) with the CLI defaults of problems.py:173-178
+    (n=24, m=32, 256 samples).  `target_spectrum` is the conditioned instance of
+    problems.py:78-86 (seeded orthonormal bases with exactly those singular
+    values, mean-centred inputs, zero initial parameters) used by the reference's
+    linearity check (verify.py:99-143).  Used to replay GOLDEN_TRAIN_CSV
+    (pkg/tests/test_cli.py:10-17) and the linearity acceptance run."""
 
-    def __init__(self, seed, n=24, m=32, n_samples=256):
+    def __init__(self, seed, n=24, m=32, n_samples=256, target_spectrum=None):
         rng = derive_rng(seed, "data")
-        self.inputs = rng.standard_normal((n_samples, m))
-        w_true = rng.standard_normal((n, m)) / np.sqrt(m)
+        inputs = rng.standard_normal((n_samples, m))
+        if target_spectrum is not None:                      # problems.py:78-86
+            sig = tuple(float(x) for x in target_spectrum)
+            inputs = inputs - inputs.mean(axis=0)
+            u = np.linalg.qr(rng.standard_normal((n, n)))[0][:, :len(sig)]
+            v = np.linalg.qr(rng.standard_normal((m, m)))[0][:, :len(sig)]
+            w_true = (u * sig) @ v.T
+        else:
+            w_true = rng.standard_normal((n, m)) / np.sqrt(m)
         c_true = rng.standard_normal(n) * 0.5
-        self.targets = self.inputs @ w_true.T + c_true
+        self.inputs = inputs
+        self.targets = inputs @ w_true.T + c_true
         self.specs = [ParamSpec("weight", (n, m)), ParamSpec("bias", (n,))]
         self.seed = seed
         self.n_samples = n_samples
+        self.target_spectrum = target_spectrum
 
-    def init_params(self):                      # problems.py:28-34
+    def init_params(self):                      # problems.py:28-34, :88-91
+        if self.target_spectrum is not None:
+            return [np.zeros(s.shape) for s in self.specs]
         rng = derive_rng(self.seed, "param_init")
         return [rng.standard_normal(s.shape) / np.sqrt(s.shape[-1] if not s.is_bias else 1)
                 for s in self.specs]
@@ -463,6 +477,20 @@ class LeastSquares:
     def worker_gradients(self, params, w, world):   # problems.py:36-50
         per = self.n_samples // world
         return self.gradients(params, slice(w * per, (w + 1) * per))
+
+
+def train_params(prob, steps, workers, seed, rank=2, lr=0.01, momentum=0.9):
+    """train.py:78-139 for powersgd on `prob`: the final parameters."""
+    comp = PowerSGD(rank)
+    comm = Communicator(workers)
+    params = prob.init_params()
+    bufs = [np.zeros_like(p) for p in params]
+    ws = [WorkerState(w) for w in range(workers)]
+    for t in range(steps):
+        grads = [prob.worker_gradients(params, w, workers) for w in range(workers)]
+        updates, _ = ef_step(ws, grads, prob.specs, comp, comm, seed, t)
+        momentum_update(params, bufs, updates, lr, momentum)
+    return params
 
 
 def train_losses(steps, workers, seed, rank=2, lr=0.01, momentum=0.9):

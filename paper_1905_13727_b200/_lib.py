@@ -22,12 +22,13 @@ STATUS_REPLACEMENT = 4
 
 MAX_RANK = 16
 MAX_TREE = 64
+REPL_ATTEMPTS = 3  # PSGD_REPL_ATTEMPTS: replacement draws per column held on the device
 
 # every symbol include/psgd_b200.h declares (tests check the export table)
 EXPORTS = (
     "psgd_plan_create", "psgd_plan_destroy", "psgd_plan_get_info", "psgd_plan_matrix",
-    "psgd_ef_p", "psgd_orthogonalize", "psgd_q_ef", "psgd_decompress", "psgd_step_single",
-    "psgd_tree_mean", "psgd_momentum_step", "psgd_debug_resident_times", "psgd_resident_dryrun", "psgd_last_error", "psgd_version",
+    "psgd_ef_p", "psgd_orthogonalize", "psgd_orthogonalize_f64", "psgd_q_ef", "psgd_decompress", "psgd_step_single",
+    "psgd_tree_mean", "psgd_momentum_step", "psgd_last_error", "psgd_version",
 )
 
 
@@ -40,7 +41,7 @@ class PlanInfo(ctypes.Structure):
         ("n_tall", ctypes.c_int32), ("items_k1", ctypes.c_int64), ("items_k3", ctypes.c_int64),
         ("launches_ef_p", ctypes.c_int32), ("launches_orthogonalize", ctypes.c_int32),
         ("launches_q_ef", ctypes.c_int32), ("launches_decompress", ctypes.c_int32),
-        ("launches_step_single", ctypes.c_int32), ("fused_step", ctypes.c_int32),
+        ("launches_step_single", ctypes.c_int32), ("pad", ctypes.c_int32),
     ]
 
 
@@ -49,7 +50,7 @@ class MatrixInfo(ctypes.Structure):
         ("flat_off", ctypes.c_int64), ("p_off", ctypes.c_int64), ("q_off", ctypes.c_int64),
         ("repl_off", ctypes.c_int64), ("n", ctypes.c_int32), ("m", ctypes.c_int32),
         ("r_eff", ctypes.c_int32), ("tall", ctypes.c_int32), ("q_ld", ctypes.c_int32),
-        ("pad", ctypes.c_int32),
+        ("repl_cols", ctypes.c_int32),
     ]
 
 
@@ -63,16 +64,14 @@ _SIGNATURES = {
     "psgd_plan_destroy": (_I32, [_P]),
     "psgd_plan_get_info": (_I32, [_P, ctypes.POINTER(PlanInfo)]),
     "psgd_plan_matrix": (_I32, [_P, _I32, ctypes.POINTER(MatrixInfo)]),
-    "psgd_ef_p": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "psgd_ef_p": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psgd_orthogonalize": (_I32, [_P, _P, _I32, _P, _P, _P, _P, _P]),
+    "psgd_orthogonalize_f64": (_I32, [_P, _I32, _P, _P, _P, _P, _P]),
     "psgd_q_ef": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "psgd_decompress": (_I32, [_P, _P, _P, _I32, _P, _P, _P, _P]),
     "psgd_step_single": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psgd_tree_mean": (_I32, [ctypes.POINTER(_P), _I32, _I64, _P, _P]),
     "psgd_momentum_step": (_I32, [_P, _P, _P, _P, _P, _P, _P, ctypes.c_float, ctypes.c_float, _P, _P]),
-    "psgd_debug_resident_times": (_I32, [_P, ctypes.POINTER(_I64), _I64]),
-    "psgd_resident_dryrun": (_I32, [_I32, ctypes.POINTER(_I64), ctypes.POINTER(_I64), _I32, _I32,
-                                    ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, _I32]),
     "psgd_last_error": (ctypes.c_char_p, []),
     "psgd_version": (_I32, []),
 }

@@ -9,8 +9,8 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("psgd_b200.cu", "psgd_resident.cu")]
-HEADERS = [os.path.join(CSRC, f) for f in ("common.cuh", "resident.h")]
+SOURCES = [os.path.join(CSRC, "psgd_b200.cu")]
+HEADERS = [os.path.join(CSRC, "common.cuh")]
 LIB = os.path.join(HERE, "libpsgd_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 

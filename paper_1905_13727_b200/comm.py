@@ -117,9 +117,11 @@ class DistributedCommunicator:
         if self.world_size > 1:
             self.stats.bits_allreduced += payload_bits
 
-    def all_reduce_sum_(self, t):
+    def all_reduce_sum_(self, t, force=False):
+        """In-place sum over the ranks; `force` issues the collective even for a
+        one-rank group (exercises the NCCL path on a single GPU)."""
         import torch.distributed as dist
-        if self.world_size > 1:
+        if self.world_size > 1 or force:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 

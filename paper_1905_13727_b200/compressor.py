@@ -230,8 +230,8 @@ class PowerSGD(Compressor):
                 pl.matrix_view(g, 0).copy_(d)
                 w = torch.empty(pl.flat_elems, **f32)
                 p = torch.zeros(pl.p_elems, **f32)
-                _lib.check(lib.psgd_ef_p(h, ptr(g), None, ptr(w), ptr(q_in), ptr(p), ptr(phat), ptr(repl), None,
-                                         ptr(status), sp), "psgd_ef_p")
+                _lib.check(lib.psgd_ef_p(h, ptr(g), None, ptr(w), ptr(q_in), ptr(p), None, ptr(status), sp),
+                           "psgd_ef_p")
                 works.append(w)
                 ps.append(p)
             if dist:                      # :337
@@ -280,7 +280,7 @@ class PowerSGD(Compressor):
         if st & (_lib.STATUS_NONFINITE_GRAD | _lib.STATUS_NONFINITE_P):
             raise ContractViolation("orthogonalize input contains non-finite entries")
         if st & _lib.STATUS_REPLACEMENT:
-            raise RuntimeError("Gram-Schmidt needed more than one replacement draw")
+            raise RuntimeError(f"Gram-Schmidt needed more than {_lib.REPL_ATTEMPTS} replacement draws for a column")
         q_new = pl.q_view(qbar, 0).contiguous()
         self.q_memory[ctx.param_index] = q_new           # :373
         comm.stats.decode_ops += 2 * n * m * r           # :374
@@ -354,8 +354,8 @@ class _Rounds:
         ps = []
         for w in self.works:
             p = torch.zeros(pl.p_elems, **self.f32)
-            _lib.check(lib.psgd_ef_p(pl.handle, ptr(w), None, ptr(self.scratch), ptr(q_in), ptr(p), ptr(self.phat),
-                                     ptr(self.repl), None, ptr(self.status), sp), "psgd_ef_p")
+            _lib.check(lib.psgd_ef_p(pl.handle, ptr(w), None, ptr(self.scratch), ptr(q_in), ptr(p), None,
+                                     ptr(self.status), sp), "psgd_ef_p")
             ps.append(p)
         return ps
 
@@ -399,7 +399,7 @@ class _Rounds:
         if st & (_lib.STATUS_NONFINITE_GRAD | _lib.STATUS_NONFINITE_P):
             raise ContractViolation("orthogonalize input contains non-finite entries")
         if st & _lib.STATUS_REPLACEMENT:
-            raise RuntimeError("Gram-Schmidt needed more than one replacement draw")
+            raise RuntimeError(f"Gram-Schmidt needed more than {_lib.REPL_ATTEMPTS} replacement draws for a column")
 
 
 class BestApproximation(Compressor):

@@ -15,7 +15,7 @@ __device__ __forceinline__ bool finite1(float x) {
 // Same sequence, threshold and replacement rule as mgs_inplace (linalg.py:61-90).
 template <int RPL, int R, class T = float>
 __device__ __forceinline__ void warp_mgs_reg(const T* __restrict__ P, int n, double inv_div,
-                                             const double* __restrict__ repl, float* __restrict__ out,
+                                             const double* __restrict__ repl, int rcols, float* __restrict__ out,
                                              int* status) {
   const int lane = threadIdx.x & 31;
   double x[R][RPL];
@@ -46,8 +46,8 @@ __device__ __forceinline__ void warp_mgs_reg(const T* __restrict__ P, int n, dou
     for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
     double before = sqrt(wsum(s));
     double nrm = before;
-    for (int attempt = 0;; ++attempt) {
-      if (attempt == 1 || j > 0) {
+    for (int attempt = 0;; ++attempt) {  // attempt a > 0: after the a-th replacement draw
+      if (attempt > 0 || j > 0) {
 #pragma unroll
         for (int i2 = 0; i2 < j; ++i2) {
           double d = 0.0;
@@ -62,15 +62,16 @@ __device__ __forceinline__ void warp_mgs_reg(const T* __restrict__ P, int n, dou
         for (int k = 0; k < RPL; ++k) s = fma(x[j][k], x[j][k], s);
         nrm = sqrt(wsum(s));
       }
-      if (!(nrm < 1e-12 * (before + 1.0))) break;
-      if (attempt == 1) {  // the table holds attempt 0 only
+      if (!(nrm < 1e-12 * (before + 1.0))) break;  // linalg.py:82-88
+      if (attempt == PSGD_REPL_ATTEMPTS) {  // the table holds attempts 0 .. PSGD_REPL_ATTEMPTS - 1
         if (lane == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
         break;
       }
+      const double* rv = repl + ((long long)attempt * rcols + j) * n;
 #pragma unroll
       for (int k = 0; k < RPL; ++k) {
         const int i = lane + 32 * k;
-        x[j][k] = i < n ? repl[(long long)j * n + i] : 0.0;
+        x[j][k] = i < n ? rv[i] : 0.0;
       }
       before = 1.0;
     }
@@ -89,28 +90,28 @@ __device__ __forceinline__ void warp_mgs_reg(const T* __restrict__ P, int n, dou
 
 template <int R, class T = float>
 __device__ __forceinline__ bool warp_mgs_dispatch_r(int rpl_log2, const T* P, int n, double inv_div,
-                                                    const double* repl, float* out, int* status) {
+                                                    const double* repl, int rcols, float* out, int* status) {
   switch (rpl_log2) {
-    case 0: warp_mgs_reg<1, R, T>(P, n, inv_div, repl, out, status); return true;
-    case 1: warp_mgs_reg<2, R, T>(P, n, inv_div, repl, out, status); return true;
-    case 2: warp_mgs_reg<4, R, T>(P, n, inv_div, repl, out, status); return true;
-    case 3: warp_mgs_reg<8, R, T>(P, n, inv_div, repl, out, status); return true;
-    case 4: warp_mgs_reg<16, R, T>(P, n, inv_div, repl, out, status); return true;
+    case 0: warp_mgs_reg<1, R, T>(P, n, inv_div, repl, rcols, out, status); return true;
+    case 1: warp_mgs_reg<2, R, T>(P, n, inv_div, repl, rcols, out, status); return true;
+    case 2: warp_mgs_reg<4, R, T>(P, n, inv_div, repl, rcols, out, status); return true;
+    case 3: warp_mgs_reg<8, R, T>(P, n, inv_div, repl, rcols, out, status); return true;
+    case 4: warp_mgs_reg<16, R, T>(P, n, inv_div, repl, rcols, out, status); return true;
     default: return false;
   }
 }
 
 // P-hat of one matrix by one warp when n <= 512 and r <= 4; false otherwise
 __device__ __forceinline__ bool warp_mgs(const float* P, int n, int r, double inv_div, const double* repl,
-                                         float* out, int* status) {
+                                         int rcols, float* out, int* status) {
   if (n > 512 || r > 4) return false;
   int l = 0;
   while ((32 << l) < n) ++l;
   switch (r) {
-    case 1: return warp_mgs_dispatch_r<1>(l, P, n, inv_div, repl, out, status);
-    case 2: return warp_mgs_dispatch_r<2>(l, P, n, inv_div, repl, out, status);
-    case 3: return warp_mgs_dispatch_r<3>(l, P, n, inv_div, repl, out, status);
-    default: return warp_mgs_dispatch_r<4>(l, P, n, inv_div, repl, out, status);
+    case 1: return warp_mgs_dispatch_r<1>(l, P, n, inv_div, repl, rcols, out, status);
+    case 2: return warp_mgs_dispatch_r<2>(l, P, n, inv_div, repl, rcols, out, status);
+    case 3: return warp_mgs_dispatch_r<3>(l, P, n, inv_div, repl, rcols, out, status);
+    default: return warp_mgs_dispatch_r<4>(l, P, n, inv_div, repl, rcols, out, status);
   }
 }
 

@@ -30,13 +30,13 @@
 
 #include "../../include/psgd_b200.h"
 #include "common.cuh"
-#include "resident.h"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <cmath>
 #include <cstdint>
@@ -72,18 +72,6 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
-bool psgd_force_multi() {
-  // The fused single-kernel step (k_step_w1) is correct but measured slower than
-  // the three-kernel step on B200 (GS latency and per-CTA imbalance sit on its
-  // critical path).  PSGD_FUSED_STEP=1 opts in for A/B measurement.
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("PSGD_FUSED_STEP");
-    v = (s && s[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 #define PSGD_CUDA_CHECK(expr)                                                        \
   do {                                                                               \
     cudaError_t _e = (expr);                                                         \
@@ -95,8 +83,9 @@ struct MatDev {
   long long flat_off, p_off, q_off, repl_off;
   int n, m, r, tall;
   int lg1, qs;  // lg1: log2 lanes per row in K1 (2..9); qs: Q staged in smem by K1
-  int nck, gs1;  // nck: K1 chunks of the matrix; gs1: orthogonalised by K1 (W = 1, n <= 512, r <= 4)
-  int qld, pad3;  // Q is column-major: element (j, k) at q_off + k * qld + j, qld = align4(m)
+  int nck, pad1;  // nck: K1 chunks of the matrix
+  int qld, rcols;  // Q is column-major: element (j, k) at q_off + k * qld + j, qld = align4(m);
+                  // rcols: columns per attempt of the replacement table at repl_off (shared by equal n)
 };
 
 struct RowItem {   // K4 / K5 warp item: rows [row0, row0 + nrows) of `mat`, 2^lg lanes per row
@@ -172,26 +161,11 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
       : "memory");
 }
-// 2-D tiled tensor copy global -> shared (TMA, SASS UTMALDG)
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
-                                            uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar)), "l"(pol)
-      : "memory");
-}
 #ifndef PSGD_STORE_HINT
 #define PSGD_STORE_HINT 1
 #endif
 #ifndef PSGD_PDL
 #define PSGD_PDL 1
-#endif
-#ifndef PSGD_K1_GS
-#define PSGD_K1_GS 0  // 1: at W = 1 the last K1 CTA orthogonalises (measured slower: register pressure)
-#endif
-#ifndef PSGD_K3_OWNER_GS
-#define PSGD_K3_OWNER_GS 0  // 1: fused matrices orthogonalised inside K3 (measured slower)
 #endif
 __device__ __forceinline__ void st_hint(float4* p, float4 v, uint64_t pol) {
 #if !PSGD_STORE_HINT
@@ -253,12 +227,14 @@ __device__ __forceinline__ void load_q4(const float* __restrict__ q, int ld, boo
 }
 
 // ----------------------------------------------------------------------------- Gram-Schmidt
-// linalg.py:61-90: in-order MODIFIED Gram-Schmidt on x (n x r row-major,
-// float64, smem or global); thread `tid` of `nth` owns rows tid + k*nth, so
-// only the reductions need barriers.  Degenerate columns (norm <
-// 1e-12 (before + 1), linalg.py:15,82) are replaced by the attempt-0 seeded
-// column from `repl` (column-major, n per column); a second degenerate draw
-// sets PSGD_STATUS_REPLACEMENT.
+// linalg.py:61-90: in-order MODIFIED Gram-Schmidt on x (n x r, float64, smem
+// or global); thread `tid` of `nth` owns rows tid + k*nth, so only the
+// reductions need barriers.  A degenerate column (norm < 1e-12 (before + 1),
+// linalg.py:15,82) is replaced by the seeded column of attempt 0, 1, ... from
+// `repl` (column j of attempt a at repl[(a * rcols + j) * n], linalg.py:54-58),
+// re-projected, and tested again, exactly as the reference's while loop; a
+// column still degenerate after PSGD_REPL_ATTEMPTS draws raises
+// PSGD_STATUS_REPLACEMENT (the host turns it into an error).
 
 struct BlockReducer {  // all threads of the CTA, __syncthreads
   double* red;         // >= 32 doubles
@@ -271,24 +247,6 @@ struct BlockReducer {  // all threads of the CTA, __syncthreads
     double t = 0.0;
     for (int w = 0; w < nw; ++w) t += red[w];
     __syncthreads();
-    return t;
-  }
-};
-
-struct ConsumerReducer {  // the consumer threads of a TMA CTA, named barrier 1
-  double* red;            // 2 x kConsWarps doubles (double-buffered by call parity)
-  int* parity;
-  __device__ double sum(double v) const {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* buf = red + kConsWarps * (*parity & 1);
-    ++*parity;
-    if (lane == 0) buf[warp] = v;
-    bar_consumers();
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < kConsWarps; ++w) t += buf[w];
     return t;
   }
 };
@@ -319,10 +277,9 @@ __device__ __forceinline__ void col_scale(double* y, double c, int n, int rs, in
 }
 
 template <class Red>
-__device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ repl, int tid, int nth,
-                            const Red& red, int* status, int rs = -1, int cs = 1) {
-  // element (i, j) lives at x[i * rs + j * cs]; default row-major n x r
-  if (rs < 0) rs = r;
+__device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ repl, int rcols, int tid, int nth,
+                            const Red& red, int* status, int rs, int cs) {
+  // element (i, j) lives at x[i * rs + j * cs]
   for (int j = 0; j < r; ++j) {
     double* xj = x + j * cs;
     double before = sqrt(red.sum(col_dot(xj, xj, n, rs, tid, nth)));
@@ -335,13 +292,13 @@ __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ 
       }
       nrm = sqrt(red.sum(col_dot(xj, xj, n, rs, tid, nth)));
     }
-    int attempt = 0;
-    while (nrm < 1e-12 * (before + 1.0)) {
-      if (attempt > 0) {
+    for (int attempt = 0; nrm < 1e-12 * (before + 1.0); ++attempt) {  // linalg.py:82-88
+      if (attempt >= PSGD_REPL_ATTEMPTS) {
         if (tid == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
         break;
       }
-      for (int i = tid; i < n; i += nth) xj[i * rs] = repl[(long long)j * n + i];
+      const double* rv = repl + ((long long)attempt * rcols + j) * n;
+      for (int i = tid; i < n; i += nth) xj[i * rs] = rv[i];
       before = 1.0;
       for (int i2 = 0; i2 < j; ++i2) {
         const double* xi = x + i2 * cs;
@@ -349,7 +306,6 @@ __device__ void mgs_inplace(double* x, int n, int r, const double* __restrict__ 
         col_axpy(xj, c, xi, n, rs, tid, nth);
       }
       nrm = sqrt(red.sum(col_dot(xj, xj, n, rs, tid, nth)));
-      ++attempt;
     }
     col_scale(xj, 1.0 / nrm, n, rs, tid, nth);  // one fp64 divide; scale by the reciprocal
   }
@@ -505,10 +461,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const float* __restrict__ g, const float* __restrict__ e, float* __restrict__ work,
             const float* __restrict__ Q, float* __restrict__ P, float* __restrict__ psplit,
             int* __restrict__ split_cnt, const float* __restrict__ bias_g, long long nbias,
-            long long bias_off, long long flag_off, int nflags, const double* __restrict__ repl,
-            float* __restrict__ Phat, int nmat, int k1_tail, int* __restrict__ k1_done, int* status) {
+            long long bias_off, long long flag_off, int* status) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ int s_gs;
   float* sgb = reinterpret_cast<float*>(smem_raw);
   float* seb = sgb + L.stages * L.stage_floats;
   float* qsl = reinterpret_cast<float*>(smem_raw + L.off_q);
@@ -629,30 +583,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   }
   if (bad) atomicOr(sflag, 1);
   bar_consumers();
-  if (t == 0) P[flag_off + blockIdx.x] = *sflag ? 1.f : 0.f;  // rides in the P all-reduce
-  if (!k1_tail) return;  // K2 raises the status from the flags and orthogonalises
-  // The last CTA to finish (every thread's P / delta writes fenced first)
-  // raises the status from all flags and, at W = 1, orthogonalises every
-  // eligible matrix, one warp each (compressors.py:338, linalg.py:61-90).
-  __threadfence();
-  bar_consumers();
-  if (t == 0) s_gs = atomicAdd(k1_done, 1) == (int)gridDim.x - 1;
-  bar_consumers();
-  if (!s_gs) return;
-  __threadfence();
-  if (t == 0) {
-    int any = 0;
-    for (int x = 0; x < nflags; ++x) any |= __ldcg(P + flag_off + x) != 0.f;
-    if (any) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
-    s_gs = any;
-    *k1_done = 0;
-  }
-  bar_consumers();
-  if (s_gs || Phat == nullptr) return;  // non-finite: the next kernels mutate nothing
-  for (int mi = warp; mi < nmat; mi += kConsWarps) {
-    const MatDev mdx = mats[mi];
-    if (mdx.gs1) warp_mgs(P + mdx.p_off, mdx.n, mdx.r, 1.0, repl + mdx.repl_off, Phat + mdx.p_off, status);
-  }
+  if (t == 0) P[flag_off + blockIdx.x] = *sflag ? 1.f : 0.f;  // rides in the P all-reduce (K2 reads it)
 }
 
 // ============================================================================= K2
@@ -743,7 +674,7 @@ __global__ void __launch_bounds__(K2_THREADS, 1)
     if (item >= nw_items) return;
     const MatDev md = mats[wlist[item]];
     const int n = md.n, r = md.r;
-    if (warp_mgs(P + md.p_off, n, r, inv_div, repl + md.repl_off, Phat + md.p_off, status)) return;
+    if (warp_mgs(P + md.p_off, n, r, inv_div, repl + md.repl_off, md.rcols, Phat + md.p_off, status)) return;
     double* x = k2smem + warp * wregion;  // column-major: lanes hit consecutive banks
     int bad = 0;
 #pragma unroll 8
@@ -758,7 +689,7 @@ __global__ void __launch_bounds__(K2_THREADS, 1)
       return;
     }
     __syncwarp();
-    mgs_inplace(x, n, r, repl + md.repl_off, lane, 32, WarpReducer{}, status, 1, n);
+    mgs_inplace(x, n, r, repl + md.repl_off, md.rcols, lane, 32, WarpReducer{}, status, 1, n);
     __syncwarp();
     for (int idx = lane; idx < n * r; idx += 32) {
       const int i = idx / r, j = idx - i * r;
@@ -783,7 +714,7 @@ __global__ void __launch_bounds__(K2_THREADS, 1)
   }
   int par = 0;
   SyncReducer sr{red, &par};
-  mgs_inplace(x, n, r, repl + md.repl_off, threadIdx.x, blockDim.x, sr, status, 1, n);
+  mgs_inplace(x, n, r, repl + md.repl_off, md.rcols, threadIdx.x, blockDim.x, sr, status, 1, n);
   __syncthreads();  // rows were thread-owned above; the copy-out mapping differs
   for (int idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
     const int i = idx / r, j = idx - i * r;
@@ -791,15 +722,25 @@ __global__ void __launch_bounds__(K2_THREADS, 1)
   }
 }
 
-// ---- K2 for very tall matrices (n * r beyond the smem budget, e.g. the LSTM
-// encoder 28869 x 650): modified Gram-Schmidt carried out in Gram space.
-// Pass 1 (k2_gram, many CTAs): partial Gram matrices of [P / W, R] (R: the
-// attempt-0 replacement columns, linalg.py:54-58), reduced in block order by
-// the last-arriving CTA, whose warp 0 then runs the reference's MGS sequence
-// (linalg.py:61-90, same projections, same degeneracy test and replacement
-// rule) on coefficient vectors, producing T (2r x r) with P-hat = [P / W, R] T.
-// Pass 2 (k2_apply): P-hat rows.  Exactly dependent fp32 columns are resolved
-// to ~1e-8 relative here instead of ~1e-16 ("tall GS").
+// ---- K2 for very tall matrices (n * r beyond the smem budget: LSTM, stress).
+// Modified Gram-Schmidt in Gram space, re-orthogonalised (CholeskyQR2 form),
+// with the reference's direct MGS as the fallback for columns Gram space cannot
+// resolve:
+// pass 1 (k2_gram<1>, one CTA per 128-row block): float64 Gram partials of
+//   X = P / W; the last-arriving block of a matrix sums them in block order and
+//   warp 0 runs the reference's MGS sequence (linalg.py:61-90: same
+//   projections, same order) on coefficient vectors, giving T1 (r x r, upper
+//   triangular) with X T1 orthonormal in exact arithmetic.  The Gram matrix
+//   squares the condition number, so any column whose residual after
+//   projection is below kGramTrust x its norm before projection — this
+//   includes every column the reference would call degenerate (linalg.py:82)
+//   — makes the block run the reference's direct MGS on X itself (float64, the
+//   seeded replacement loop of linalg.py:82-88, global scratch) and write
+//   P-hat; the later passes skip that matrix.
+// pass 2 (k2_gram<2>, only when pass 1 saw a residual ratio below kGramRefine):
+//   Gram partials of Y = X T1 computed from the rows, T2 from MGS on them and
+//   T = T1 T2 (orthogonality ~1e-16 instead of ~1e-16 kappa^2).
+// apply (k2_apply): P-hat = X T.
 
 struct GramItem {
   int mat, row0, nrows, blk, nblk, gidx;
@@ -808,36 +749,48 @@ struct GramItem {
 
 constexpr int K2G_ROWS = 128;
 constexpr int K2G_TILE = 64;
+constexpr int K2G_TS = PSGD_MAX_RANK * PSGD_MAX_RANK + 8;  // doubles per matrix in wsT: T, then flags
+constexpr int K2G_DIRECT = PSGD_MAX_RANK * PSGD_MAX_RANK;  // flag: P-hat written by the direct fallback
+constexpr int K2G_REFINE = K2G_DIRECT + 1;                 // flag: pass 2 needed
+constexpr double kGramTrust = 1e-5;
+constexpr double kGramRefine = 1e-2;
 
+template <int PASS>
 __global__ void __launch_bounds__(256)
     k2_gram(const MatDev* __restrict__ mats, const GramItem* __restrict__ items, const float* __restrict__ P,
             int divisor, const double* __restrict__ repl, double* __restrict__ wsg, double* __restrict__ wsT,
-            int* __restrict__ counters, long long flag_off, int nflags, int* status) {
-  // Gram of P / W over this block's rows (r (r+1) / 2 pairs, float64); the last
-  // block reduces the partials in block order and runs the MGS sequence of
-  // linalg.py:61-90 on coefficient vectors.  The replacement columns R enter
-  // only if a column degenerates (then the cross terms are computed directly).
+            int* __restrict__ counters, long long flag_off, int nflags, double* __restrict__ scratch,
+            float* __restrict__ Phat, int* status) {
   __shared__ double X[K2G_TILE][PSGD_MAX_RANK + 1];
-  __shared__ double G[2 * PSGD_MAX_RANK][2 * PSGD_MAX_RANK];
-  __shared__ double cvec[2 * PSGD_MAX_RANK];
-  __shared__ double Tm[PSGD_MAX_RANK][2 * PSGD_MAX_RANK];
+  __shared__ double G[PSGD_MAX_RANK][PSGD_MAX_RANK + 1];
+  __shared__ double T1s[PSGD_MAX_RANK * PSGD_MAX_RANK];
+  __shared__ double cvec[PSGD_MAX_RANK];
+  __shared__ double Tm[PSGD_MAX_RANK][PSGD_MAX_RANK];  // Tm[j]: coefficient vector of output column j
   __shared__ double gpart[256];
-  __shared__ int s_last, s_degen;
+  __shared__ double red[64];
+  __shared__ int s_last, s_direct, s_refine;
   pdl_wait();
-  {
-    int bad = 0;
+  if (PASS == 1) {
+    int bad = 0;  // a non-finite gradient on any worker (flags ride in P): mutate nothing
     for (int x = threadIdx.x; x < nflags; x += blockDim.x) bad |= P[flag_off + x] != 0.f;
     if (__syncthreads_or(bad)) {
       if (threadIdx.x == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
       return;
     }
+  } else if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) {
+    return;
   }
   const GramItem it = items[blockIdx.x];
   const MatDev md = mats[it.mat];
-  const int n = md.n, r = md.r, R2 = 2 * r;
+  const int n = md.n, r = md.r;
   const int npairs = r * (r + 1) / 2;
   const double inv_div = 1.0 / (double)divisor;
   const int t = threadIdx.x;
+  double* Tg = wsT + (long long)it.gidx * K2G_TS;
+  if (PASS == 2) {
+    if (Tg[K2G_DIRECT] != 0.0 || Tg[K2G_REFINE] == 0.0) return;  // same for every block of the matrix
+    for (int x = t; x < r * r; x += 256) T1s[x] = Tg[x];
+  }
   int pk = -1, pl = -1;  // pair index -> (k, l), k <= l (npairs <= 136 < 256)
   if (t < npairs) {
     int p = t, k = 0;
@@ -848,23 +801,35 @@ __global__ void __launch_bounds__(256)
   double acc = 0.0;
   int bad = 0;
   for (int r0 = it.row0; r0 < it.row0 + it.nrows; r0 += K2G_TILE) {
-    for (int idx = t; idx < K2G_TILE * r; idx += 256) {
-      const int i = idx / r, k = idx - i * r, row = r0 + i;
-      double v = 0.0;
-      if (row < it.row0 + it.nrows) {
-        const float f = P[md.p_off + (long long)row * r + k];
-        bad |= !finite1(f);
-        v = (double)f * inv_div;
+    __syncthreads();  // X (and T1s on the first tile) ready / free
+    if (PASS == 1) {
+      for (int idx = t; idx < K2G_TILE * r; idx += 256) {
+        const int i = idx / r, k = idx - i * r, row = r0 + i;
+        double v = 0.0;
+        if (row < it.row0 + it.nrows) {
+          const float f = P[md.p_off + (long long)row * r + k];
+          bad |= !finite1(f);
+          v = (double)f * inv_div;
+        }
+        X[i][k] = v;
       }
-      X[i][k] = v;
+    } else {  // Y = X T1, row by row
+      for (int idx = t; idx < K2G_TILE * r; idx += 256) {
+        const int i = idx / r, k = idx - i * r, row = r0 + i;
+        double v = 0.0;
+        if (row < it.row0 + it.nrows) {
+          const float* pr = P + md.p_off + (long long)row * r;
+          for (int l = 0; l <= k; ++l) v = fma((double)pr[l] * inv_div, T1s[l * r + k], v);
+        }
+        X[i][k] = v;
+      }
     }
     __syncthreads();
     if (pk >= 0)
 #pragma unroll 8
       for (int i = 0; i < K2G_TILE; ++i) acc = fma(X[i][pk], X[i][pl], acc);
-    __syncthreads();
   }
-  if (__syncthreads_or(bad)) {  // linalg.py:35-36
+  if (PASS == 1 && __syncthreads_or(bad)) {  // linalg.py:35-36
     if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
   }
   if (pk >= 0) wsg[it.gbase + (long long)it.blk * npairs + t] = acc;
@@ -874,6 +839,8 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  if (t == 0) counters[it.gidx] = 0;
+  if (ld_acquire(status) & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;  // block-uniform
   {  // fixed order: thread groups take blocks q, q + NG, ...; then groups in order
     const int NG = 256 / npairs;
     const int p = t % npairs, q = t / npairs;
@@ -896,112 +863,139 @@ __global__ void __launch_bounds__(256)
       G[pk][pl] = s2;
       G[pl][pk] = s2;
     }
-  }
-  if (t == 0) {
-    counters[it.gidx] = 0;
-    s_degen = 0;
+    if (t == 0) {
+      s_direct = 0;
+      s_refine = 0;
+    }
   }
   __syncthreads();
-  if (t >= 32) return;
-  // ---- MGS on coefficient vectors: value(c) = [P/W, R] c ; <a, b> = a^T G b
-  const int lane = t;
-  auto gdot = [&](const double* a, const double* b) {  // warp-parallel a^T G b
-    double s = 0.0;
-    if (lane < R2) {
-      double gb = 0.0;
-      for (int l = 0; l < R2; ++l) gb += G[lane][l] * b[l];
-      s = a[lane] * gb;
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    return s;
-  };
-  bool full = false;  // G holds the R cross terms
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    if (lane < R2 && !full)
-      for (int l = r; l < R2; ++l) {  // unknown R terms are never used unless a column degenerates
-        G[lane][l] = 0.0;
-        G[l][lane] = 0.0;
+  if (t < 32) {  // ---- MGS on coefficient vectors: value(c) = X c ; <a, b> = a^T G b
+    const int lane = t;
+    auto gdot = [&](const double* a, const double* b) {  // warp-parallel a^T G b
+      double s = 0.0;
+      if (lane < r) {
+        double gb = 0.0;
+        for (int l = 0; l < r; ++l) gb = fma(G[lane][l], b[l], gb);
+        s = a[lane] * gb;
       }
-    __syncwarp();
-    bool need_full = false;
-    for (int j = 0; j < r && !need_full; ++j) {
-      if (lane < R2) cvec[lane] = lane == j ? 1.0 : 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      return s;
+    };
+    bool direct = false, refine = false;
+    for (int j = 0; j < r && !direct; ++j) {
+      if (lane < r) cvec[lane] = lane == j ? 1.0 : 0.0;
       __syncwarp();
-      double before = sqrt(fmax(gdot(cvec, cvec), 0.0));
+      const double before = sqrt(fmax(G[j][j], 0.0));
       double nrm = before;
-      for (int pass = 0; pass < 2; ++pass) {
-        if (pass == 1) {  // degenerate: the seeded replacement column, before := 1
-          if (!full) {
-            need_full = true;
-            break;
-          }
-          if (lane < R2) cvec[lane] = lane == r + j ? 1.0 : 0.0;
-          __syncwarp();
-          before = 1.0;
-        }
-        for (int i2 = 0; i2 < j; ++i2) {
-          const double c = gdot(Tm[i2], cvec);
-          __syncwarp();
-          if (lane < R2) cvec[lane] -= c * Tm[i2][lane];
-          __syncwarp();
-        }
-        if (j > 0 || pass == 1) nrm = sqrt(fmax(gdot(cvec, cvec), 0.0));
-        if (!(nrm < 1e-12 * (before + 1.0))) break;
-        if (pass == 1 && lane == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
+      for (int i2 = 0; i2 < j; ++i2) {
+        const double c = gdot(Tm[i2], cvec);
+        __syncwarp();
+        if (lane < r) cvec[lane] -= c * Tm[i2][lane];
+        __syncwarp();
       }
-      if (need_full) break;
+      if (j > 0) nrm = sqrt(fmax(gdot(cvec, cvec), 0.0));
+      if (PASS == 1 && (nrm < 1e-12 * (before + 1.0) || nrm < kGramTrust * before)) {
+        direct = true;  // degenerate (linalg.py:82) or beyond what Gram space resolves
+        break;
+      }
+      refine |= nrm < kGramRefine * before;
       const double inv = 1.0 / nrm;
-      if (lane < R2) Tm[j][lane] = cvec[lane] * inv;
+      if (lane < r) Tm[j][lane] = cvec[lane] * inv;
       __syncwarp();
     }
-    if (!need_full) break;
-    // rare path: cross terms <P_k / W, R_l> and <R_k, R_l> over all rows, then redo
-    for (int k = 0; k < R2; ++k)
-      for (int l = (k < r ? r : k); l < R2; ++l) {
-        double s = 0.0;
-        for (int i = lane; i < n; i += 32) {
-          const double a = k < r ? (double)P[md.p_off + (long long)i * r + k] * inv_div
-                                 : repl[md.repl_off + (long long)(k - r) * n + i];
-          s = fma(a, repl[md.repl_off + (long long)(l - r) * n + i], s);
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (lane == 0) {
-          G[k][l] = s;
-          G[l][k] = s;
-        }
-      }
-    full = true;
-    __syncwarp();
+    if (lane == 0) {
+      s_direct = direct;
+      s_refine = refine;
+    }
   }
-  for (int x = lane; x < R2 * r; x += 32) wsT[(long long)it.gidx * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK + x] =
-      Tm[x % r][x / r];  // row-major [k][j]
+  __syncthreads();
+  if (PASS == 1 && s_direct) {  // the reference's direct MGS on X (column-major scratch)
+    double* x = scratch + md.p_off;
+    for (int idx = t; idx < n * r; idx += 256) {
+      const int i = idx / r, j = idx - i * r;
+      x[(long long)j * n + i] = (double)P[md.p_off + idx] * inv_div;
+    }
+    __syncthreads();
+    int par = 0;
+    SyncReducer sr{red, &par};
+    mgs_inplace(x, n, r, repl + md.repl_off, md.rcols, t, 256, sr, status, 1, n);
+    __syncthreads();
+    for (int idx = t; idx < n * r; idx += 256) {
+      const int i = idx / r, j = idx - i * r;
+      Phat[md.p_off + idx] = (float)x[(long long)j * n + i];
+    }
+    if (t == 0) Tg[K2G_DIRECT] = 1.0;
+    return;
+  }
+  for (int x = t; x < r * r; x += 256) {  // T row-major [k][j]: P-hat column j = sum_k X[:, k] T[k][j]
+    const int k = x / r, j = x - k * r;
+    double v;
+    if (PASS == 1) {
+      v = Tm[j][k];
+    } else {  // T = T1 T2
+      v = 0.0;
+      for (int l = 0; l < r; ++l) v = fma(T1s[k * r + l], Tm[j][l], v);
+    }
+    Tg[x] = v;
+  }
+  if (PASS == 1 && t == 0) {
+    Tg[K2G_DIRECT] = 0.0;
+    Tg[K2G_REFINE] = s_refine ? 1.0 : 0.0;
+  }
 }
+
 __global__ void __launch_bounds__(256)
     k2_apply(const MatDev* __restrict__ mats, const int* __restrict__ gram_list, const int* __restrict__ blk_mat,
              const int* __restrict__ blk_row0, const float* __restrict__ P, int divisor,
-             const double* __restrict__ repl, const double* __restrict__ wsT, float* __restrict__ Phat,
-             const int* status) {
+             const double* __restrict__ wsT, float* __restrict__ Phat, const int* status) {
   pdl_wait();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
   const int gidx = blk_mat[blockIdx.x];
+  const double* T = wsT + (long long)gidx * K2G_TS;
+  if (T[K2G_DIRECT] != 0.0) return;  // orthogonalised directly by k2_gram<1>
   const MatDev md = mats[gram_list[gidx]];
   const int n = md.n, r = md.r;
   const int i = blk_row0[blockIdx.x] + threadIdx.x;
   if (i >= n) return;
-  const double* T = wsT + (long long)gidx * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK;
   const double inv_div = 1.0 / (double)divisor;
-  double x[2 * PSGD_MAX_RANK];
-  bool use_r = false;  // replacement columns enter only if a column degenerated
-  for (int k = r * r; k < 2 * r * r; ++k) use_r |= T[k] != 0.0;
+  double x[PSGD_MAX_RANK];
   for (int k = 0; k < r; ++k) x[k] = (double)P[md.p_off + (long long)i * r + k] * inv_div;
-  for (int k = 0; k < r; ++k) x[r + k] = use_r ? repl[md.repl_off + (long long)k * n + i] : 0.0;
-  const int kmax = use_r ? 2 * r : r;
   for (int j = 0; j < r; ++j) {
     double s = 0.0;
-    for (int k = 0; k < kmax; ++k) s += x[k] * T[k * r + j];
+    for (int k = 0; k <= j; ++k) s = fma(x[k], T[k * r + j], s);  // T is upper triangular
     Phat[md.p_off + (long long)i * r + j] = (float)s;
+  }
+}
+
+// linalg.orthogonalize on float64 input (linalg.py:61-90 as the reference runs
+// it, no fp32 rounding): one CTA, the matrix column-major in float64 scratch,
+// the reference's MGS with the seeded replacement loop.
+__global__ void __launch_bounds__(1024)
+    k2_gs_f64(const MatDev* __restrict__ mats, int mi, const double* __restrict__ P, const double* __restrict__ repl,
+              double* __restrict__ scratch, double* __restrict__ Phat, int* status) {
+  __shared__ double red[64];
+  const MatDev md = mats[mi];
+  const int n = md.n, r = md.r, t = threadIdx.x, nth = blockDim.x;
+  double* x = scratch + md.p_off;
+  int bad = 0;
+  for (int idx = t; idx < n * r; idx += nth) {
+    const double v = P[idx];
+    bad |= !isfinite(v);
+    const int i = idx / r, j = idx - i * r;
+    x[(long long)j * n + i] = v;
+  }
+  if (__syncthreads_or(bad)) {  // linalg.py:35-36 (ContractViolation)
+    if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
+    return;
+  }
+  int par = 0;
+  SyncReducer sr{red, &par};
+  mgs_inplace(x, n, r, repl + md.repl_off, md.rcols, t, nth, sr, status, 1, n);
+  __syncthreads();
+  for (int idx = t; idx < n * r; idx += nth) {
+    const int i = idx / r, j = idx - i * r;
+    Phat[idx] = x[(long long)j * n + i];
   }
 }
 
@@ -1022,13 +1016,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     k3_slab(const MatDev* __restrict__ mats, const SlabItem* __restrict__ items, float* __restrict__ work,
             const float* __restrict__ P, int divisor, const double* __restrict__ repl, float* __restrict__ Phat,
             float* __restrict__ qout, float* __restrict__ e, float* __restrict__ wsq, int* __restrict__ counters,
-            int* __restrict__ gs_flag, int* __restrict__ gs_done, float* __restrict__ bias_out, long long nbias,
-            long long bias_off, long long flag_off, int nflags, int write_mhat, int wait_first,
+            float* __restrict__ bias_out, long long nbias,
+            long long bias_off, long long flag_off, int nflags, int write_mhat,
             int* status) {
   constexpr int DCAP = k3_dcap(R);
   extern __shared__ __align__(16) unsigned char k3smem[];
   __shared__ int s_flag;
-  __shared__ double sred[64];
   const SlabItem it = items[blockIdx.x];
   const int t = threadIdx.x;
   const bool fused = !TALL;  // fused: all n rows in this CTA; tall: split rows, q partials
@@ -1049,25 +1042,10 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int rbeg = it.chunk * it.ksub * rows_chunk;
   const int nrows = min(n - rbeg, rows_chunk);
   const int ncols = min(C, m - it.c0);
-  double* gsd = reinterpret_cast<double*>(k3smem);                  // fused owner: n x r float64
-  float* ps = reinterpret_cast<float*>(gsd + (fused && PSGD_K3_OWNER_GS ? n * r : 0));  // nrows x r
+  float* ps = reinterpret_cast<float*>(k3smem);                      // nrows x r
   float* red = ps + rows_chunk * r;                                   // RG x C x r
   float* qs = red + RG * C * r;                                       // C x r
 
-#if PSGD_K3_OWNER_GS
-  pdl_wait();  // K3 follows K1 directly: delta / P must be complete before any load
-  if (fused) {  // a non-finite gradient on any worker (flags ride in P): mutate nothing
-    int bad = 0;
-    for (int x = t; x < nflags; x += kThreads) bad |= P[flag_off + x] != 0.f;
-    if (__syncthreads_or(bad)) {
-      if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
-      return;
-    }
-  } else if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) {
-    return;
-  }
-#endif
-  if (wait_first) pdl_wait();  // K3 follows K1 directly: delta must be complete before any load
   // 1. every load of the slab in flight at once
   float d[DCAP];
   const long long base = md.flat_off + (long long)rbeg * m + col;
@@ -1086,12 +1064,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       d[s] = (colok && li < nrows) ? __ldcs(work + base + (long long)li * m) : 0.f;
     }
   }
-#if !PSGD_K3_OWNER_GS
   // K3 follows K2, which started only after K1 completed: delta was final when
   // the loads above were issued.  Now wait for K2's P-hat and status.
   pdl_wait();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;  // mutate nothing
-#endif
   if (blockIdx.x < 64 && nbias > 0) {  // bias mean (optimizer.py:111-113), first CTAs of the launch
     bool bad = false;
     const long long nb = min(64, (int)gridDim.x);
@@ -1106,68 +1082,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   //    P / W (linalg.py:61-90, float64) while its loads fly and publishes it;
   //    the other slabs of the matrix (dispatched after it) wait for the flag.
   //    Tall: from K2.
-  if (fused && PSGD_K3_OWNER_GS) {
-    int state;
-    if (it.c0 == 0 && n <= 512 && r <= 4) {  // register warp MGS by warp 0
-      if (t == 0) s_flag = 0;
-      __syncthreads();
-      if (t < 32) {
-        const int before = *status;
-        warp_mgs(P + md.p_off, n, r, 1.0 / (double)divisor, repl + md.repl_off, Phat + md.p_off, status);
-        __threadfence();
-        if (t == 0 && (ld_acquire(status) & PSGD_STATUS_NONFINITE_P) && !(before & PSGD_STATUS_NONFINITE_P))
-          s_flag = 2;
-      }
-      __syncthreads();
-      state = s_flag == 2 ? 2 : 1;
-      if (state == 1)
-        for (int x = t; x < nrows * r; x += kThreads) ps[x] = __ldcg(Phat + md.p_off + (long long)rbeg * r + x);
-      __syncthreads();
-      if (t == 0) st_release(gs_flag + it.mat, state);
-    } else if (it.c0 == 0) {
-      const double inv_div = 1.0 / (double)divisor;
-      int bad = 0;
-      for (int idx = t; idx < n * r; idx += kThreads) {
-        const float v = P[md.p_off + idx];
-        bad |= !finite1(v);
-        const int i = idx / r, j = idx - i * r;
-        gsd[j * n + i] = (double)v * inv_div;  // column-major: conflict-free
-      }
-      state = __syncthreads_or(bad) ? 2 : 1;
-      if (state == 1) {
-        int par = 0;
-        SyncReducer sr{sred, &par};
-        mgs_inplace(gsd, n, r, repl + md.repl_off, t, kThreads, sr, status, 1, n);
-        __syncthreads();
-        for (int idx = t; idx < n * r; idx += kThreads) {
-          const int i = idx / r, j = idx - i * r;
-          const float v = (float)gsd[j * n + i];
-          ps[idx] = v;
-          Phat[md.p_off + idx] = v;
-        }
-        __threadfence();
-      } else if (t == 0) {
-        atomicOr(status, PSGD_STATUS_NONFINITE_P);  // linalg.py:35-36
-      }
-      __syncthreads();
-      if (t == 0) st_release(gs_flag + it.mat, state);
-    } else {
-      if (t == 0) {
-        int v;
-        while ((v = ld_acquire(gs_flag + it.mat)) == 0) __nanosleep(100);
-        s_flag = v;
-      }
-      __syncthreads();
-      state = s_flag;
-      if (state == 1)
-        for (int x = t; x < nrows * r; x += kThreads) ps[x] = __ldcg(Phat + md.p_off + (long long)rbeg * r + x);
-    }
-    if (t == 0 && atomicAdd(gs_done + it.mat, 1) == it.pad - 1) {  // last reader resets (self-cleaning)
-      gs_flag[it.mat] = 0;
-      gs_done[it.mat] = 0;
-    }
-    if (state != 1) return;
-  } else {
+  {  // P-hat rows of this chunk (from K2)
     const float* src = Phat + md.p_off + (long long)rbeg * r;
     for (int x = t; x < nrows * r; x += kThreads) ps[x] = src[x];
   }
@@ -1270,7 +1185,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   __syncthreads();
   float* __restrict__ qdst = qout + md.q_off + it.c0;  // column-major: (c, k) at k * qld + c
-  if (!fused) {  // partial of a tall slab; the last chunk combines in chunk order
+  if constexpr (TALL) {  // partial of a tall slab; the last chunk combines in chunk order
     float* part = wsq + it.ws_off;
     for (int o = t; o < ncols * r; o += kThreads) part[(long long)it.chunk * C * r + o] = qs[o];
     __threadfence();
@@ -1288,7 +1203,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (t == 0) counters[it.slab] = 0;
     }
     return;
-  }
+  } else {
   for (int o = t; o < ncols * r; o += kThreads) {
     const int k = o / ncols, cc = o - k * ncols;
     qdst[(long long)k * md.qld + cc] = qs[cc * r + k];
@@ -1336,337 +1251,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
   }
-}
-
-// ============================================================================= fused W=1 step
-// One persistent cooperative kernel per step (1 CTA per SM, 512 threads) when
-// the plan allows it (W = 1; every matrix has n <= rows a K3 CTA holds,
-// n <= 512, one r_eff <= 4): K1 phase (TMA ring, thread 0 refills) -> grid
-// barrier -> GS phase (one warp per matrix, register MGS) + bias mean -> grid
-// barrier -> K3 phase (two 256-thread register-slab groups per CTA).  Saves the
-// two kernel boundaries and K2's launch of the three-kernel step.
-
-__device__ __forceinline__ void bar_group(int gi) {
-  asm volatile("bar.sync %0, 256;" ::"r"(2 + gi) : "memory");
-}
-
-__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    while ((unsigned)ld_acquire(reinterpret_cast<const int*>(ctr)) < target) __nanosleep(32);
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-constexpr int KS_QSLOTS = 3;
-
-struct KsLayout {  // dynamic smem of the fused step
-  int qslot_floats;
-  int off_q, off_red, off_bar, total;
-  int stages, stage_floats;
-};
-
-// one register slab (all rows x C cols) by a 256-thread group: q, e, M-hat (W = 1)
-template <int R>
-__device__ __forceinline__ void ks_slab(const SlabItem& it, const MatDev& md, float* __restrict__ work,
-                                        float* __restrict__ Q, float* __restrict__ e, float* smem, int gtid,
-                                        int gi) {
-  constexpr int DCAP = k3_dcap(R);
-  const int n = md.n, m = md.m, r = R;
-  const int vec = it.vec, cql = it.cq_log2;
-  const int CQ = 1 << cql, C = CQ * vec, RG = kThreads >> cql;
-  const int cq = gtid & (CQ - 1), rg = gtid >> cql;
-  const int col = it.c0 + cq * vec;
-  const bool colok = col < m;
-  const int ncols = min(C, m - it.c0);
-  float* ps = smem;                  // n x r
-  float* red = ps + kFusedNMax * r;  // RG x C x r
-  float* qs = red + RG * C * r;      // C x r
-  float d[DCAP];
-  const long long base = md.flat_off + col;
-  if (vec == 4) {
-#pragma unroll
-    for (int s = 0; s < DCAP / 4; ++s) {
-      const int li = rg + RG * s;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (colok && li < n) v = __ldcs(reinterpret_cast<const float4*>(work + base + (long long)li * m));
-      d[4 * s + 0] = v.x; d[4 * s + 1] = v.y; d[4 * s + 2] = v.z; d[4 * s + 3] = v.w;
-    }
-  } else {
-#pragma unroll
-    for (int s = 0; s < DCAP; ++s) {
-      const int li = rg + RG * s;
-      d[s] = (colok && li < n) ? __ldcs(work + base + (long long)li * m) : 0.f;
-    }
-  }
-  float qp[4][R];
-#pragma unroll
-  for (int v = 0; v < 4; ++v)
-#pragma unroll
-    for (int k = 0; k < R; ++k) qp[v][k] = 0.f;
-  if (vec == 4) {
-#pragma unroll
-    for (int s = 0; s < DCAP / 4; ++s) {
-      const int li = rg + RG * s;
-      if (li < n) {
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-          const float pk = ps[li * r + k];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) qp[v][k] = fmaf(d[4 * s + v], pk, qp[v][k]);
-        }
-      }
-    }
-  } else {
-#pragma unroll
-    for (int s = 0; s < DCAP; ++s) {
-      const int li = rg + RG * s;
-      if (li < n)
-#pragma unroll
-        for (int k = 0; k < R; ++k) qp[0][k] = fmaf(d[s], ps[li * r + k], qp[0][k]);
-    }
-  }
-#pragma unroll
-  for (int v = 0; v < 4; ++v)
-#pragma unroll
-    for (int k = 0; k < R; ++k)
-      if (v < vec) red[(rg * C + cq * vec + v) * r + k] = qp[v][k];
-  bar_group(gi);
-  for (int o = gtid; o < C * r; o += kThreads) {
-    float s = 0.f;
-    for (int gidx = 0; gidx < RG; ++gidx) s += red[gidx * C * r + o];
-    qs[o] = s;
-  }
-  bar_group(gi);
-  {
-    float* qdst = Q + md.q_off + it.c0;  // W = 1: q_w is the next warm start (column-major)
-    for (int o = gtid; o < ncols * r; o += kThreads) {
-      const int k = o / ncols, cc = o - k * ncols;
-      qdst[(long long)k * md.qld + cc] = qs[cc * r + k];
-    }
-  }
-  float qv[4][R];
-#pragma unroll
-  for (int v = 0; v < 4; ++v)
-#pragma unroll
-    for (int k = 0; k < R; ++k) qv[v][k] = v < vec ? qs[(cq * vec + v) * r + k] : 0.f;
-  if (colok) {
-    if (vec == 4) {
-#pragma unroll
-      for (int s = 0; s < DCAP / 4; ++s) {
-        const int li = rg + RG * s;
-        if (li < n) {
-          float mh[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int k = 0; k < R; ++k) {
-            const float pk = ps[li * r + k];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) mh[v] = fmaf(pk, qv[v][k], mh[v]);
-          }
-          const long long a = base + (long long)li * m;
-          st_stream(reinterpret_cast<float4*>(e + a), make_float4(d[4 * s] - mh[0], d[4 * s + 1] - mh[1],
-                                                                  d[4 * s + 2] - mh[2], d[4 * s + 3] - mh[3]));
-          st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
-        }
-      }
-    } else {
-#pragma unroll
-      for (int s = 0; s < DCAP; ++s) {
-        const int li = rg + RG * s;
-        if (li < n) {
-          float mh = 0.f;
-#pragma unroll
-          for (int k = 0; k < R; ++k) mh = fmaf(ps[li * r + k], qv[0][k], mh);
-          const long long a = base + (long long)li * m;
-          st_stream(e + a, d[s] - mh);
-          st_stream(work + a, mh);
-        }
-      }
-    }
-  }
-  bar_group(gi);  // ps / red / qs free for the group's next slab
-}
-
-template <int R>
-__global__ void __launch_bounds__(kCons, 1)
-    k_step_w1(const MatDev* __restrict__ mats, int nmat, const Chunk1* __restrict__ chunks,
-              const int* __restrict__ k1_beg, const SplitRow* __restrict__ splits, KsLayout L,
-              const SlabItem* __restrict__ slabs, int nslabs, const float* __restrict__ g,
-              float* __restrict__ e, float* __restrict__ work, float* __restrict__ Q, float* __restrict__ P,
-              float* __restrict__ Phat, const double* __restrict__ repl, float* __restrict__ psplit,
-              int* __restrict__ split_cnt, const float* __restrict__ bias_g, float* __restrict__ bias_out,
-              long long nbias, long long bias_off, long long flag_off, unsigned* __restrict__ gbar,
-              int* __restrict__ status) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* sgb = reinterpret_cast<float*>(smem_raw);
-  float* seb = sgb + L.stages * L.stage_floats;
-  float* qsl = reinterpret_cast<float*>(smem_raw + L.off_q);
-  float* red = reinterpret_cast<float*>(smem_raw + L.off_red);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
-  uint64_t* qfull = full + L.stages;
-  __shared__ int s_flag;
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int cb = k1_beg[blockIdx.x], ce = k1_beg[blockIdx.x + 1];
-  const unsigned grid = gridDim.x;
-#ifdef PSGD_KS_TIMING
-  unsigned long long tm[6];
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm[0]));
-#define KS_T(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm[i]))
-#else
-#define KS_T(i)
-#endif
-
-  // ------------------------------------------------ phase 1: delta = g + e, P = delta Q
-  if (t == 0) {
-    for (int s = 0; s < L.stages; ++s) mbar_init(&full[s], 1);
-    for (int s = 0; s < KS_QSLOTS; ++s) mbar_init(&qfull[s], 1);
-    s_flag = 0;
-    fence_mbar_init();
-    if (blockIdx.x == 0) *status = 0;
-  }
-  __syncthreads();
-  // thread 0 is the producer: chunk k goes to stage k % S; a new matrix's Q to slot mseq % 3
-  int p_cur = -1, p_qseq = -1;
-  const uint64_t pol = pol_evict_first(), polq = pol_evict_last();
-  auto issue = [&](int k) {
-    const Chunk1 ch = chunks[k];
-    const MatDev md = mats[ch.mat];
-    if (ch.mat != p_cur) {
-      p_cur = ch.mat;
-      if (md.qs) {
-        const int qsi = ++p_qseq % KS_QSLOTS;
-        const uint32_t qb = (uint32_t)((long long)md.r * md.qld * 4);
-        mbar_expect_tx(&qfull[qsi], qb);
-        tma_load(qsl + qsi * L.qslot_floats, Q + md.q_off, qb, &qfull[qsi], polq);
-      }
-    }
-    const int s = (k - cb) % L.stages;
-    const long long a4 = ch.off & ~3LL;
-    const long long span = (long long)(ch.nrows - 1) * md.m + ch.ncols;
-    const uint32_t bytes = (uint32_t)((((ch.off + span + 3) & ~3LL) - a4) * 4);
-    mbar_expect_tx(&full[s], 2 * bytes);
-    tma_load(sgb + s * L.stage_floats, g + a4, bytes, &full[s], pol);
-    tma_load(seb + s * L.stage_floats, e + a4, bytes, &full[s], pol);
-  };
-  if (t == 0)
-    for (int k = cb; k < min(ce, cb + L.stages); ++k) issue(k);
-  bool bad = false;
-  for (long long x = (long long)blockIdx.x * kCons + t; x < nbias; x += (long long)grid * kCons) {
-    const float v = bias_g[x];
-    bad |= !finite1(v);
-    P[bias_off + x] = v;
-  }
-  {
-    const uint64_t keep = pol_evict_last();
-    int cur = -1, mseq = -1, rpar = 0;
-    MatDev md{};
-    for (int k = cb; k < ce; ++k) {
-      const int s = (k - cb) % L.stages;
-      const uint32_t ph = ((k - cb) / L.stages) & 1;
-      const Chunk1 ch = chunks[k];
-      if (ch.mat != cur) {
-        md = mats[ch.mat];
-        cur = ch.mat;
-        if (md.qs) {
-          ++mseq;  // counts Q-slot uses only
-          mbar_wait(&qfull[mseq % KS_QSLOTS], (mseq / KS_QSLOTS) & 1);
-        }
-      }
-      mbar_wait(&full[s], ph);
-      float* rb = red + (rpar & 1) * (K1_RED_ROWS * kConsWarps * R + R);
-      if ((1 << md.lg1) > 32) ++rpar;
-      if (md.qs)
-        k1_chunk<R, true>(ch, md, qsl + (mseq % KS_QSLOTS) * L.qslot_floats, sgb + s * L.stage_floats,
-                          seb + s * L.stage_floats, true, work, P, splits, psplit, split_cnt, rb, keep, bad);
-      else
-        k1_chunk<R, false>(ch, md, Q + md.q_off, sgb + s * L.stage_floats, seb + s * L.stage_floats, true,
-                           work, P, splits, psplit, split_cnt, rb, keep, bad);
-      __syncthreads();  // stage s (and, three matrices back, its Q slot) is free
-      if (t == 0 && k + L.stages < ce) issue(k + L.stages);
-    }
-  }
-  if (bad) atomicOr(&s_flag, 1);
-  __syncthreads();
-  if (t == 0) P[flag_off + blockIdx.x] = s_flag ? 1.f : 0.f;
-  KS_T(1);
-  grid_sync(gbar, grid);
-  KS_T(2);
-
-  // ------------------------------------------------ phase 2+3: per-slab-group GS, q, e, M-hat
-  // No second grid barrier: each 256-thread group takes slabs from a global
-  // counter (dynamic balance) and orthogonalises a slab's matrix itself when it
-  // is new to the group (float64 MGS in smem, while the slab's loads fly).
-  int any = 0;
-  for (unsigned x = t; x < grid; x += kCons) any |= __ldcg(P + flag_off + x) != 0.f;
-  const bool poisoned = __syncthreads_or(any) != 0;
-  KS_T(3);
-  KS_T(4);
-  if (poisoned) {
-    if (blockIdx.x == 0 && t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);  // mutate nothing
-  } else {
-    for (long long x2 = (long long)blockIdx.x * kCons + t; x2 < nbias; x2 += (long long)grid * kCons)
-      bias_out[x2] = __ldcg(P + bias_off + x2);
-    const int gi = warp >> 3, gtid = t & 255;
-    float* gsm = reinterpret_cast<float*>(smem_raw) + gi * (L.off_q / 8);              // ps | red | qs
-    double* gsd = reinterpret_cast<double*>(smem_raw + L.off_q) + gi * (L.qslot_floats * KS_QSLOTS / 4);
-    __shared__ int s_k[2];
-    __shared__ double gred[2][2][8];
-    int cached = -1, gpar = 0;
-    bool skip = false;
-    MatDev md{};
-    for (;;) {
-      if (gtid == 0) s_k[gi] = (int)atomicAdd(gbar + 3, 1u);
-      bar_group(gi);
-      const int k = s_k[gi];
-      if (k >= nslabs) break;
-      const SlabItem it = slabs[k];
-      if (it.mat != cached) {
-        md = mats[it.mat];
-        cached = it.mat;
-        // P / 1 -> float64 column-major; MGS with group reductions (linalg.py:61-90)
-        const int n = md.n, r = md.r;
-        int pbad = 0;
-        for (int idx = gtid; idx < n * r; idx += kThreads) {
-          const float v = __ldcg(P + md.p_off + idx);
-          pbad |= !finite1(v);
-          const int i = idx / r, j = idx - i * r;
-          gsd[j * n + i] = (double)v;
-        }
-        GroupReducer grd{&gred[gi][0][0], &gpar, gi};
-        skip = grd.sum(pbad ? 1.0 : 0.0) != 0.0;
-        if (skip) {
-          if (gtid == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);  // linalg.py:35-36
-        } else {
-          mgs_inplace(gsd, n, r, repl + md.repl_off, gtid, kThreads, grd, status, 1, n);
-          bar_group(gi);
-          for (int idx = gtid; idx < n * r; idx += kThreads) {
-            const int i = idx / r, j = idx - i * r;
-            const float v = (float)gsd[j * n + i];
-            gsm[idx] = v;  // ps of the group
-            if (it.c0 == 0) Phat[md.p_off + idx] = v;
-          }
-        }
-        bar_group(gi);
-      }
-      if (!skip) ks_slab<R>(it, md, work, Q, e, gsm, gtid, gi);
-    }
-  }
-  __syncthreads();
-  KS_T(5);
-#ifdef PSGD_KS_TIMING
-  if (t == 0)
-    printf("ks blk %d: p1 %.1f  bar1 %.1f  p2 %.1f  bar2 %.1f  p3 %.1f us\n", blockIdx.x, (tm[1] - tm[0]) * 1e-3,
-           (tm[2] - tm[1]) * 1e-3, (tm[3] - tm[2]) * 1e-3, (tm[4] - tm[3]) * 1e-3, (tm[5] - tm[4]) * 1e-3);
-#endif
-  if (t == 0 && atomicAdd(gbar + 2, 1u) == grid - 1) {  // last CTA out resets the barriers
-    gbar[0] = 0;
-    gbar[1] = 0;
-    gbar[2] = 0;
-    gbar[3] = 0;
-  }
+  }  // !TALL
 }
 
 // K4 / K5 row streaming.  MODE 0 (K4): e = delta - P-hat q^T (+ M-hat in place
@@ -2168,7 +1753,11 @@ __global__ void k_tree_mean(TreeArgs a, int nbuf, long long count, float* __rest
 __global__ void __launch_bounds__(256) k_momentum(float* __restrict__ x, float* __restrict__ mom,
                                                   const float* __restrict__ u, long long n4, float lr,
                                                   float momentum, float* __restrict__ bx, float* __restrict__ bm,
-                                                  const float* __restrict__ bu, long long nb) {
+                                                  const float* __restrict__ bu, long long nb,
+                                                  const int* __restrict__ status) {
+  // a failed step (non-finite gradient / P) leaves x and m untouched, like the
+  // reference, which raises before optimizer.py:131-134 runs
+  if (status && (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P))) return;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     const float4 uu = __ldcs(reinterpret_cast<const float4*>(u) + i);
@@ -2226,13 +1815,6 @@ struct psgd_plan {
   long long psplit_elems = 0;
   // K3 fused
   int k2_smem = 0;
-  // fused single-kernel W = 1 step (k_step_w1)
-  bool ks_ok = false;
-  int ks_r = 0;
-  KsLayout ksl{};
-  std::vector<int> ks_grp;
-  int* d_ks_grp = nullptr;
-  unsigned* d_gbar = nullptr;
   std::vector<int> small_list, gram_list;   // K2 in smem / in Gram space
   std::vector<int> wlist, clist;             // K2 small: warp items / CTA items
   int k2_wregion = 0, k2_wblocks = 0;
@@ -2283,16 +1865,11 @@ struct psgd_plan {
   int *d_apply_mat = nullptr, *d_apply_row0 = nullptr;
   double *d_wsg = nullptr, *d_wsT = nullptr;
   int *d_gs_flag = nullptr, *d_gs_done = nullptr, *d_gs_cnt = nullptr, *d_k1_done = nullptr;
-  bool need_k2 = true;  // false: K1 orthogonalises every matrix (W = 1, n <= 512, r <= 4)
-  std::vector<int> wlist_t, clist_t;        // K2 restricted to tall matrices
   int* d_gram_cnt = nullptr;
   RowItem *d_k4 = nullptr, *d_k5 = nullptr;
-  double* d_gsws = nullptr;
+  double* d_gsws = nullptr;  // float64 scratch in the P layout (direct MGS fallback of k2_gram)
   float* d_wsq = nullptr;
   int* d_counters = nullptr;
-  // on-chip-resident W = 1 step (psgd_resident.cu); nullptr when not eligible
-  psgd::ResPlan* res = nullptr;
-  std::string res_why;
 };
 
 namespace {
@@ -2449,16 +2026,13 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     md.tall = k3_tall_config(md.n, md.m, md.r).nchunks > 1;
     md.lg1 = 5;  // set with the K1 chunk geometry below
     md.qs = 0;  // decided below, once the K1 smem budget is known
-    md.gs1 = (PSGD_K1_GS && world == 1 && md.n <= 512 && md.r <= 4) ? 1 : 0;
     md.flat_off = fo;
     md.p_off = po;
     md.q_off = qo;
     md.qld = (int)align4(md.m);
-    md.repl_off = ro;
     fo = align4(fo + (long long)md.n * md.m);
     po = align4(po + (long long)md.n * md.r);
     qo += (long long)md.r * md.qld;
-    ro += (long long)md.n * md.r;
     pl->n_tall += md.tall;
     pl->rmax = std::max(pl->rmax, rmax_of(md.r));
     pl->all_list.push_back(i);
@@ -2466,6 +2040,19 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     pl->mats.push_back(md);
   }
   pl->flat_elems = std::max(4LL, fo);
+  {  // replacement columns depend on (n, j, attempt) only (linalg.py:54-58): one table per distinct n
+    std::map<int, int> cols;
+    for (auto& md : pl->mats) cols[md.n] = std::max(cols[md.n], md.r);
+    std::map<int, long long> off;
+    for (auto& kv : cols) {
+      off[kv.first] = ro;
+      ro += (long long)PSGD_REPL_ATTEMPTS * kv.second * kv.first;
+    }
+    for (auto& md : pl->mats) {
+      md.repl_off = off[md.n];
+      md.rcols = cols[md.n];
+    }
+  }
 
   // ---- K1 smem layout: Q slots for the matrices whose r x q_ld block fits, then
   // the largest 2-stage ring of g / e chunks that fits beside them (227 KB)
@@ -2596,12 +2183,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       }
     }
   }
-  for (int mi : pl->wlist)
-    if (!pl->mats[mi].gs1) pl->wlist_t.push_back(mi);
-  for (int mi : pl->clist)
-    if (!pl->mats[mi].gs1) pl->clist_t.push_back(mi);
   pl->k2_wblocks = ((int)pl->wlist.size() + K2_THREADS / 32 - 1) / (K2_THREADS / 32);
-  pl->need_k2 = !pl->wlist_t.empty() || !pl->clist_t.empty() || !pl->gram_items.empty();
   pl->k2_smem = std::max(pl->k2_smem, pl->k2_wregion * (K2_THREADS / 32) * 8);
   // ---- K3 slabs, grouped by r (one launch per group): fused slabs hold all rows
   {
@@ -2637,8 +2219,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
             pl->k3.push_back({wo, mi, s * C, ch, cf.nchunks > 1 ? nitems : 1, slab_id, cf.vec, cf.cql, nslab,
                               ksub, 0});
         }
-        const int smem = (cf.nchunks == 1 && PSGD_K3_OWNER_GS ? md.n * r * 8 : 0) +
-                         (cf.rows_chunk * r + RG * C * r + C * r) * (int)sizeof(float);
+        const int smem = (cf.rows_chunk * r + RG * C * r + C * r) * (int)sizeof(float);
         gp.smem = std::max(gp.smem, smem);
       }
       gp.end = (int)pl->k3.size();
@@ -2675,35 +2256,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   }
   build_row_items(pl->mats, false, pl->k5, pl->g5);
 
-  // ---- fused W = 1 step eligibility and layout
-  {
-    bool ok = world == 1 && nmat > 0 && pl->n_tall == 0 && pl->g3.size() == 1;
-    const int r0 = nmat > 0 ? pl->mats[0].r : 0;
-    for (auto& md : pl->mats) ok = ok && md.r == r0 && md.n <= 512 && md.qs;
-    ok = ok && r0 >= 1 && r0 <= 4 && (int)pl->k1_beg.size() - 1 <= pl->nsm;
-    KsLayout& L = pl->ksl;
-    L.qslot_floats = pl->k1l.qslot_floats;
-    L.stages = pl->k1l.stages;
-    L.stage_floats = pl->k1l.stage_floats;
-    int off = 2 * L.stages * L.stage_floats * 4;
-    L.off_q = off;   off += KS_QSLOTS * L.qslot_floats * 4;
-    L.off_red = off; off += 2 * (K1_RED_ROWS * kConsWarps * std::max(r0, 1) + std::max(r0, 1)) * 4;
-    off = (off + 15) & ~15;
-    L.off_bar = off; off += (L.stages + KS_QSLOTS) * 8 + 16;
-    L.total = off;
-    ok = ok && L.total <= 227 * 1024;
-    // each 256-thread group needs (512 + 1024 + 1024) * r floats of the stage area half
-    ok = ok && (512 + 2048) * r0 * 4 <= L.off_q / 2;
-    if (ok) {
-      const int groups = 2 * ((int)pl->k1_beg.size() - 1);
-      std::vector<double> w;
-      for (auto& it : pl->k3) w.push_back((double)pl->mats[it.mat].n * (it.vec << it.cq_log2) + 256.0);
-      pl->ks_grp = balance(w, groups);
-      while ((int)pl->ks_grp.size() < groups + 1) pl->ks_grp.push_back((int)pl->k3.size());
-    }
-    pl->ks_ok = ok;
-    pl->ks_r = r0;
-  }
   // ---- device block
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t off = 0;
@@ -2721,17 +2273,15 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_k3 = take(pl->k3.size() * sizeof(SlabItem));
   const size_t o_tl = take(pl->tall_list.size() * sizeof(int));
   const size_t o_al = take(pl->all_list.size() * sizeof(int));
-  const size_t o_sl = take((pl->wlist.size() + pl->clist.size() + pl->wlist_t.size() + pl->clist_t.size()) * sizeof(int));
+  const size_t o_sl = take((pl->wlist.size() + pl->clist.size()) * sizeof(int));
   const size_t o_gl = take(pl->gram_list.size() * sizeof(int));
   const size_t o_gi = take(pl->gram_items.size() * sizeof(GramItem));
   const size_t o_am = take(pl->apply_mat.size() * sizeof(int));
   const size_t o_ar = take(pl->apply_row0.size() * sizeof(int));
   const size_t o_wg = take((size_t)std::max(1LL, pl->wsg_elems) * sizeof(double));
-  const size_t o_wt = take(std::max<size_t>(1, pl->gram_list.size()) * 2 * PSGD_MAX_RANK * PSGD_MAX_RANK * sizeof(double));
+  const size_t o_wt = take(std::max<size_t>(1, pl->gram_list.size()) * K2G_TS * sizeof(double));
   const size_t o_gc = take(std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
   const size_t o_gf = take((size_t)std::max(1, nmat) * 3 * sizeof(int) + 16);
-  const size_t o_ksg = take(pl->ks_grp.size() * sizeof(int));
-  const size_t o_gbar = take(4 * sizeof(unsigned));
   const size_t o_k4 = take(pl->k4.size() * sizeof(RowItem));
   const size_t o_k4t = take(pl->k4t.size() * sizeof(TileItem));
   const size_t o_k1t = take(pl->k1t.size() * sizeof(TileItem));
@@ -2773,8 +2323,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_gs_done = pl->d_gs_flag + std::max(1, nmat);
   pl->d_gs_cnt = pl->d_gs_done + std::max(1, nmat);
   pl->d_k1_done = pl->d_gs_cnt + std::max(1, nmat);
-  pl->d_ks_grp = reinterpret_cast<int*>(b + o_ksg);
-  pl->d_gbar = reinterpret_cast<unsigned*>(b + o_gbar);
   pl->d_k4 = reinterpret_cast<RowItem*>(b + o_k4);
   pl->d_k4t = reinterpret_cast<TileItem*>(b + o_k4t);
   pl->d_k1t = reinterpret_cast<TileItem*>(b + o_k1t);
@@ -2802,8 +2350,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   {
     std::vector<int> wc(pl->wlist);
     wc.insert(wc.end(), pl->clist.begin(), pl->clist.end());
-    wc.insert(wc.end(), pl->wlist_t.begin(), pl->wlist_t.end());
-    wc.insert(wc.end(), pl->clist_t.begin(), pl->clist_t.end());
     if (ce == cudaSuccess) ce = up(pl->d_small_list, wc.data(), wc.size() * sizeof(int));
   }
   if (ce == cudaSuccess) ce = up(pl->d_gram_list, pl->gram_list.data(), pl->gram_list.size() * sizeof(int));
@@ -2812,8 +2358,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_apply_row0, pl->apply_row0.data(), pl->apply_row0.size() * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gram_cnt, 0, std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gs_flag, 0, (size_t)std::max(1, nmat) * 3 * sizeof(int) + 16);
-  if (ce == cudaSuccess) ce = up(pl->d_ks_grp, pl->ks_grp.data(), pl->ks_grp.size() * sizeof(int));
-  if (ce == cudaSuccess) ce = cudaMemset(pl->d_gbar, 0, 4 * sizeof(unsigned));
   if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = up(pl->d_k4t, pl->k4t.data(), pl->k4t.size() * sizeof(TileItem));
   if (ce == cudaSuccess) ce = up(pl->d_k1t, pl->k1t.data(), pl->k1t.size() * sizeof(TileItem));
@@ -2830,11 +2374,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     delete pl;
     return fail(PSGD_ECUDA, std::string("plan upload: ") + cudaGetErrorString(ce));
   }
-  if (world == 1) {  // delta held in TMEM + smem across the step when it fits (ResNet-18 class)
-    std::vector<psgd::ResMatIn> rin;
-    for (auto& md : pl->mats) rin.push_back({md.flat_off, md.p_off, md.q_off, md.repl_off, md.n, md.m, md.r, md.qld});
-    pl->res = psgd::res_plan_create(rin.data(), nmat, nbias, pl->nsm, &pl->res_why);
-  }
   *out = pl;
   return PSGD_OK;
 }
@@ -2842,7 +2381,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
 int psgd_plan_destroy(psgd_plan* plan) {
   if (!plan) return PSGD_OK;
   if (plan->dev_block) cudaFree(plan->dev_block);
-  psgd::res_plan_destroy(plan->res);
   delete plan;
   return PSGD_OK;
 }
@@ -2870,19 +2408,16 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->launches_ef_p = ((pl->k1.empty() && pl->nbias == 0) ? 0 : 1) + (pl->k1t.empty() ? 0 : 2);
   o->launches_orthogonalize = (pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0;
   {  // same rule as psgd_q_ef: k2_gs runs for small matrices, or for the bias unless K3 takes it
-    const bool tall_only = pl->world == 1;
-    const bool small = (tall_only ? pl->wlist_t.size() + pl->clist_t.size() : pl->wlist.size() + pl->clist.size()) > 0;
+    const bool small = pl->wlist.size() + pl->clist.size() > 0;
     const bool bias_in_k3 = !small && !pl->gram_items.empty() && !pl->g3.empty();
-    o->launches_orthogonalize = ((small || (pl->nbias > 0 && !bias_in_k3)) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 2);
+    o->launches_orthogonalize = ((small || (pl->nbias > 0 && !bias_in_k3)) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 3);
   }
   o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4) + nonempty(pl->g4t) +
                      nonempty(pl->g4t2) +
                      (pl->k3t.empty() ? 0 : 2);
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
-  const bool fused_step = pl->ks_ok && !psgd_force_multi();
-  o->launches_step_single = (pl->res || fused_step) ? 1 : o->launches_ef_p + o->launches_q_ef;
-  o->fused_step = pl->res ? 2 : fused_step ? 1 : 0;
+  o->launches_step_single = o->launches_ef_p + o->launches_q_ef;
   return PSGD_OK;
 }
 
@@ -2894,6 +2429,7 @@ int psgd_plan_matrix(const psgd_plan* pl, int32_t i, psgd_matrix_info* o) {
   o->p_off = md.p_off;
   o->q_off = md.q_off;
   o->repl_off = md.repl_off;
+  o->repl_cols = md.rcols;
   o->n = md.n;
   o->m = md.m;
   o->r_eff = md.r;
@@ -2944,13 +2480,16 @@ int run_k1_tiles(const psgd_plan* pl, const float* g, const float* e, float* wor
 
 template <int RM>
 int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, const float* q, float* p,
-           float* phat, const double* repl, const float* bias_g, int* status, cudaStream_t st) {
+           const float* bias_g, int* status, cudaStream_t st) {
   const int grid = (int)pl->k1_beg.size() - 1;
   {
     const int rc = run_k1_tiles<RM>(pl, g, e, work, q, p, st);
     if (rc) return rc;
   }
-  if (pl->k1.empty() && pl->nbias == 0) return PSGD_OK;
+  if (pl->k1.empty() && pl->nbias == 0) {  // k1_ef_p (block 0) resets the status word; here nothing else does
+    PSGD_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int), st));
+    return PSGD_OK;
+  }
   auto kern = k1_ef_p<RM>;
   const size_t smem = pl->k1l.total;
   PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -2958,8 +2497,7 @@ int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, con
                             (const MatDev*)pl->d_mats, (const Chunk1*)pl->d_k1, (const int*)pl->d_k1_beg,
                             (const SplitRow*)pl->d_splits, pl->k1l, g, e, work, q, p, pl->d_psplit,
                             pl->d_split_cnt, bias_g, (long long)pl->nbias, (long long)pl->p_bias_off,
-                            (long long)pl->flag_off, pl->nflags, repl, phat, pl->nmat, pl->need_k2 ? 0 : 1,
-                            pl->d_k1_done, status));
+                            (long long)pl->flag_off, status));
   return PSGD_OK;
 }
 
@@ -2967,7 +2505,7 @@ template <int R, bool EXACT>
 struct RunK3 {
   static int run(const psgd_plan* pl, const Group& gp, float* work, const float* p, int divisor,
                  const double* repl, float* phat, float* qout, float* e, float* bias_out, long long nbias,
-                 bool wait_first, int* status, cudaStream_t st) {
+                 int* status, cudaStream_t st) {
     const int nitems = gp.end - gp.beg;
     if (nitems <= 0) return PSGD_OK;
     auto kern = gp.tall ? k3_slab<R, EXACT, true> : k3_slab<R, EXACT, false>;
@@ -2975,9 +2513,9 @@ struct RunK3 {
       PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gp.smem));
     PSGD_CUDA_CHECK(launch_ex(kern, nitems, kThreads, gp.smem, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
                               (const SlabItem*)(pl->d_k3 + gp.beg), work, p, divisor, repl, phat, qout, e,
-                              pl->d_wsq, pl->d_counters, pl->d_gs_flag, pl->d_gs_done, bias_out, nbias,
+                              pl->d_wsq, pl->d_counters, bias_out, nbias,
                               (long long)pl->p_bias_off, (long long)pl->flag_off, pl->nflags,
-                              pl->world == 1 ? 1 : 0, wait_first ? 1 : 0, status));
+                              pl->world == 1 ? 1 : 0, status));
     return PSGD_OK;
   }
 };
@@ -3036,11 +2574,11 @@ bool check_dev(const psgd_plan* pl) {
   return dev == pl->device;
 }
 
-int launch_k2(const psgd_plan* pl, bool tall_only, bool with_bias, const float* p, float* phat, int divisor,
+int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, int divisor,
               const double* repl, float* bias_out, int* status, cudaStream_t st) {
-  const int nw = (int)(tall_only ? pl->wlist_t.size() : pl->wlist.size());
-  const int nci = (int)(tall_only ? pl->clist_t.size() : pl->clist.size());
-  const int* wl = pl->d_small_list + (tall_only ? pl->wlist.size() + pl->clist.size() : 0);
+  const int nw = (int)pl->wlist.size();
+  const int nci = (int)pl->clist.size();
+  const int* wl = pl->d_small_list;
   const int* cl = wl + nw;
   const int nwb = (nw + K2_THREADS / 32 - 1) / (K2_THREADS / 32);
   const int bias_blocks =
@@ -3056,72 +2594,35 @@ int launch_k2(const psgd_plan* pl, bool tall_only, bool with_bias, const float* 
                               status));
   }
   if (!pl->gram_items.empty()) {
-    PSGD_CUDA_CHECK(launch_ex(k2_gram, (int)pl->gram_items.size(), 256, 0, st, false, (const MatDev*)pl->d_mats,
-                              (const GramItem*)pl->d_gram_items, p, divisor, repl, pl->d_wsg, pl->d_wsT,
-                              pl->d_gram_cnt, (long long)pl->flag_off, pl->nflags, status));
+    for (int pass = 1; pass <= 2; ++pass)  // pass 2 (re-orthogonalisation) exits at once unless pass 1 asks for it
+      PSGD_CUDA_CHECK(launch_ex(pass == 1 ? k2_gram<1> : k2_gram<2>, (int)pl->gram_items.size(), 256, 0, st, false,
+                                (const MatDev*)pl->d_mats, (const GramItem*)pl->d_gram_items, p, divisor, repl,
+                                pl->d_wsg, pl->d_wsT, pl->d_gram_cnt, (long long)pl->flag_off, pl->nflags,
+                                pl->d_gsws, phat, status));
     PSGD_CUDA_CHECK(launch_ex(k2_apply, (int)pl->apply_mat.size(), 256, 0, st, false, (const MatDev*)pl->d_mats,
                               (const int*)pl->d_gram_list, (const int*)pl->d_apply_mat,
-                              (const int*)pl->d_apply_row0, p, divisor, repl, (const double*)pl->d_wsT, phat,
+                              (const int*)pl->d_apply_row0, p, divisor, (const double*)pl->d_wsT, phat,
                               (const int*)status));
   }
   return PSGD_OK;
 }
-
-template <int R>
-int run_ks_r(const psgd_plan* pl, const float* g, float* e, float* work, float* q, float* p, float* p_hat,
-             const float* bias_g, const double* repl, float* bias_out, int* status, cudaStream_t st) {
-  auto kern = k_step_w1<R>;
-  const int grid = (int)pl->k1_beg.size() - 1;
-  PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->ksl.total));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kCons);
-  cfg.dynamicSmemBytes = pl->ksl.total;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: grid barriers are safe
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  PSGD_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (const MatDev*)pl->d_mats, pl->nmat, (const Chunk1*)pl->d_k1,
-                                     (const int*)pl->d_k1_beg, (const SplitRow*)pl->d_splits, pl->ksl,
-                                     (const SlabItem*)pl->d_k3, (int)pl->k3.size(), g, e, work, q, p,
-                                     p_hat, repl, pl->d_psplit, pl->d_split_cnt, bias_g, bias_out,
-                                     (long long)pl->nbias, (long long)pl->p_bias_off, (long long)pl->flag_off,
-                                     pl->d_gbar, status));
-  return PSGD_OK;
-}
-
-int run_ks(const psgd_plan* pl, const float* g, float* e, float* work, float* q, float* p, float* p_hat,
-           const float* bias_g, const double* repl, float* bias_out, int* status, cudaStream_t st) {
-  switch (pl->ks_r) {
-    case 1: return run_ks_r<1>(pl, g, e, work, q, p, p_hat, bias_g, repl, bias_out, status, st);
-    case 2: return run_ks_r<2>(pl, g, e, work, q, p, p_hat, bias_g, repl, bias_out, status, st);
-    case 3: return run_ks_r<3>(pl, g, e, work, q, p, p_hat, bias_g, repl, bias_out, status, st);
-    default: return run_ks_r<4>(pl, g, e, work, q, p, p_hat, bias_g, repl, bias_out, status, st);
-  }
-}
-
-
 
 }  // namespace
 
 extern "C" {
 
 int psgd_ef_p(const psgd_plan* pl, const float* g, const float* e, float* work, const float* q,
-              float* p, float* p_hat, const double* repl, const float* bias_g, int32_t* status, void* stream) {
+              float* p, const float* bias_g, int32_t* status, void* stream) {
   if (!pl || !status || !p || (pl->nmat > 0 && (!g || !work || !q)) || (pl->nbias > 0 && !bias_g))
     return fail(PSGD_EINVAL, "psgd_ef_p: NULL argument");
-  if (pl->world == 1 && pl->nmat > 0 && (!p_hat || !repl))
-    return fail(PSGD_EINVAL, "psgd_ef_p: a world-1 plan orthogonalises in K1 and needs p_hat and repl");
   if (!check_dev(pl)) return fail(PSGD_EINVAL, "psgd_ef_p: plan belongs to another device");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (pl->rmax) {
-    case 1: return run_k1<1>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
-    case 2: return run_k1<2>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
-    case 4: return run_k1<4>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
-    case 8: return run_k1<8>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
-    default: return run_k1<16>(pl, g, e, work, q, p, p_hat, repl, bias_g, (int*)status, st);
+    case 1: return run_k1<1>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+    case 2: return run_k1<2>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+    case 4: return run_k1<4>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+    case 8: return run_k1<8>(pl, g, e, work, q, p, bias_g, (int*)status, st);
+    default: return run_k1<16>(pl, g, e, work, q, p, bias_g, (int*)status, st);
   }
 }
 
@@ -3130,8 +2631,20 @@ int psgd_orthogonalize(const psgd_plan* pl, const float* p, int32_t divisor, con
   if (!pl || !p || !p_hat || !status || divisor < 1 || (pl->nmat > 0 && !repl) ||
       (pl->nbias > 0 && !bias_out))
     return fail(PSGD_EINVAL, "psgd_orthogonalize: bad argument");
-  return launch_k2(pl, false, true, p, p_hat, divisor, repl, bias_out, (int*)status,
+  return launch_k2(pl, true, p, p_hat, divisor, repl, bias_out, (int*)status,
                    static_cast<cudaStream_t>(stream));
+}
+
+int psgd_orthogonalize_f64(const psgd_plan* pl, int32_t i, const double* p, const double* repl, double* p_hat,
+                           int32_t* status, void* stream) {
+  if (!pl || !p || !p_hat || !repl || !status || i < 0 || i >= pl->nmat)
+    return fail(PSGD_EINVAL, "psgd_orthogonalize_f64: bad argument");
+  const MatDev& md = pl->mats[i];
+  const int nth = (int)std::min<long long>(1024, std::max<long long>(32, ((long long)md.n + 31) / 32 * 32));
+  k2_gs_f64<<<1, nth, 0, static_cast<cudaStream_t>(stream)>>>(pl->d_mats, i, p, repl, pl->d_gsws, p_hat,
+                                                              (int*)status);
+  PSGD_CUDA_CHECK(cudaGetLastError());
+  return PSGD_OK;
 }
 
 int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor, const double* repl,
@@ -3141,33 +2654,20 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
     return fail(PSGD_EINVAL, "psgd_q_ef: bad argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int rc = PSGD_OK;
-#if PSGD_K3_OWNER_GS
-  const bool any_fused = pl->n_tall < pl->nmat;
-  if (pl->n_tall > 0 || (!any_fused && pl->nbias > 0)) {  // K2: P-hat of the tall matrices (+ bias)
-    rc = launch_k2(pl, true, !any_fused, p, p_hat, divisor, repl, bias_out, (int*)status, st);
+  // K2: P-hat = MGS(P / W) of every matrix (compressors.py:337-338) + the bias mean.
+  // When every matrix is orthogonalised in Gram space (k2_gram checks the
+  // non-finite flags) and a K3 slab launch follows, that launch writes the bias
+  // mean, so k2_gs is not launched for the bias alone.
+  const bool k2_small = pl->wlist.size() + pl->clist.size() > 0;
+  const bool bias_in_k3 = !k2_small && !pl->gram_items.empty() && !pl->g3.empty();
+  if (pl->nmat > 0 || pl->nbias > 0) {
+    rc = launch_k2(pl, !bias_in_k3, p, p_hat, divisor, repl, bias_out, (int*)status, st);
     if (rc) return rc;
   }
-  bool bias_done = !any_fused;
-#else
-  // K2: P-hat of the matrices K1 did not orthogonalise (all of them when W > 1) + bias mean
-  const bool k2 = pl->need_k2 || pl->world > 1 || divisor != 1;
-  // every matrix in Gram space (k2_gram checks the non-finite flags) and a K3 slab launch
-  // follows: that launch writes the bias mean, so k2_gs is not launched for the bias alone
-  const bool tall_only = pl->world == 1 && divisor == 1;
-  const bool k2_small = (tall_only ? pl->wlist_t.size() + pl->clist_t.size() : pl->wlist.size() + pl->clist.size()) > 0;
-  const bool bias_in_k3 = k2 && !k2_small && !pl->gram_items.empty() && !pl->g3.empty();
-  if (k2) {
-    rc = launch_k2(pl, tall_only, !bias_in_k3, p, p_hat, divisor, repl, bias_out, (int*)status, st);
-    if (rc) return rc;
-  }
-  bool bias_done = k2 && !bias_in_k3;
-#endif
-  bool first = true;
-  for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab
-    // right after K1 (no K2 in between) a K3 CTA must wait before loading delta
+  bool bias_done = !bias_in_k3;
+  for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab (after K2: delta is final)
     rc = dispatch_r<RunK3>(gp.r, pl, gp, work, p, (int)divisor, repl, p_hat, q_out, e, bias_out,
-                           bias_done ? 0LL : (long long)pl->nbias, first && !k2, (int*)status, st);
-    first = false;
+                           bias_done ? 0LL : (long long)pl->nbias, (int*)status, st);
     if (rc) return rc;
     bias_done = true;
   }
@@ -3226,43 +2726,9 @@ int psgd_step_single(const psgd_plan* pl, const float* g, float* e, float* work,
   if (!pl) return fail(PSGD_EINVAL, "NULL plan");
   if (pl->world != 1) return fail(PSGD_EINVAL, "psgd_step_single needs a world-1 plan");
   if (!status) return fail(PSGD_EINVAL, "NULL status");
-  if (pl->res && e != nullptr) {
-    if (!g || !work || !q || !p || !p_hat || !repl || (pl->nbias > 0 && (!bias_g || !bias_out)))
-      return fail(PSGD_EINVAL, "psgd_step_single: NULL argument");
-    PSGD_CUDA_CHECK(psgd::res_step(pl->res, g, e, work, q, p, p_hat, repl, bias_g, bias_out, (int*)status,
-                                   static_cast<cudaStream_t>(stream)));
-    return PSGD_OK;
-  }
-  if (pl->ks_ok && e != nullptr && !psgd_force_multi()) return run_ks(pl, g, e, work, q, p, p_hat, bias_g, repl,
-                                                                      bias_out, (int*)status,
-                                                                      static_cast<cudaStream_t>(stream));
-  int rc = psgd_ef_p(pl, g, e, work, q, p, p_hat, repl, bias_g, status, stream);
+  int rc = psgd_ef_p(pl, g, e, work, q, p, bias_g, status, stream);
   if (!rc) rc = psgd_q_ef(pl, work, p, 1, repl, p_hat, q, e, bias_out, status, stream);
   return rc;
-}
-
-int psgd_resident_dryrun(int32_t nmat, const int64_t* n, const int64_t* m, int32_t rank, int32_t nsm,
-                         double* stats, char* why, int32_t why_cap) {
-  if (nmat < 0 || (nmat > 0 && (!n || !m)) || !stats || rank < 1) return fail(PSGD_EINVAL, "bad argument");
-  std::vector<psgd::ResMatIn> rin;
-  long long fo = 0;
-  for (int i = 0; i < nmat; ++i) {
-    const int r = (int)std::min<long long>(std::min<long long>(n[i], m[i]), rank);
-    rin.push_back({fo, 0, 0, 0, (int)n[i], (int)m[i], r, (int)align4(m[i])});
-    fo = align4(fo + n[i] * m[i]);
-  }
-  std::string w;
-  const int ok = psgd::res_dryrun(rin.data(), nmat, nsm, stats, &w);
-  if (why && why_cap > 0) {
-    strncpy(why, w.c_str(), why_cap - 1);
-    why[why_cap - 1] = 0;
-  }
-  return ok;
-}
-
-int psgd_debug_resident_times(const psgd_plan* pl, int64_t* out, int64_t cap) {
-  if (!pl || !out) return fail(PSGD_EINVAL, "NULL argument");
-  return psgd::res_debug_times(pl->res, reinterpret_cast<long long*>(out), cap);
 }
 
 int psgd_momentum_step(const psgd_plan* pl, float* params, float* mom, const float* update, float* bias_params,
@@ -3271,13 +2737,13 @@ int psgd_momentum_step(const psgd_plan* pl, float* params, float* mom, const flo
   if (!pl || (pl->nmat > 0 && (!params || !mom || !update)) ||
       (pl->nbias > 0 && (!bias_params || !bias_mom || !bias_update)))
     return fail(PSGD_EINVAL, "psgd_momentum_step: NULL argument");
-  (void)status;
   const long long n4 = pl->nmat > 0 ? pl->flat_elems / 4 : 0;
   const long long work = std::max(n4, (long long)pl->nbias);
   if (work == 0) return PSGD_OK;
   const int blocks = (int)std::min<long long>((work + 255) / 256, (long long)pl->nsm * 8);
   k_momentum<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(params, mom, update, n4, lr, momentum, bias_params,
-                                                                     bias_mom, bias_update, pl->nbias);
+                                                                     bias_mom, bias_update, pl->nbias,
+                                                                     (const int*)status);
   PSGD_CUDA_CHECK(cudaGetLastError());
   return PSGD_OK;
 }

@@ -19,6 +19,7 @@ the reference seeds it (derive_rng(seed, "warm_start_init", param_index)).
 
 import torch
 
+from . import _lib
 from .catalogs import ParamSpec
 from .comm import DistributedCommunicator
 from .engine import PowerSGDEngine
@@ -75,6 +76,10 @@ class PowerSGDState:
                     eng.q_view(i).copy_(oeng.q_view(oi))
                 self.owner[id(p)] = (eng, i)
             self.engines[key] = eng
+            # engines of a superseded bucket layout own no parameter any more: free them
+            live = {id(e) for e, _ in self.owner.values()}
+            for k in [k for k, e in self.engines.items() if id(e) not in live]:
+                del self.engines[k]
         return eng
 
 
@@ -87,6 +92,12 @@ def powersgd_hook(state, bucket):
     eng.run()
     for i, g in enumerate(grads):
         g.copy_(eng.update_view(i).reshape(g.shape))
+    # A non-finite gradient on any rank (the flags ride in the P all-reduce, so every
+    # rank's status agrees) leaves e and Q untouched but no M-hat: poison the whole
+    # bucket on every rank, so an AMP GradScaler skips the step everywhere instead of
+    # the replicas applying different updates (the reference raises on all workers).
+    bad = (eng.status & (_lib.STATUS_NONFINITE_GRAD | _lib.STATUS_NONFINITE_P)) != 0
+    bucket.buffer().masked_fill_(bad, float("nan"))
     state.calls += 1
     if state.check_every and state.calls % state.check_every == 0:
         eng.check()

@@ -15,9 +15,12 @@ on one device, the packed fp32 buffers of a parameter catalog:
 
 and runs, per step,
 
-    W == 1 (one GPU)        psgd_step_single                       -- 2 kernels
-    W > 1, distributed      K1 | all_reduce(P) | K3 | all_reduce(q) | K5
-    W > 1, simulated        K1 x W | tree_mean | K3 x W | tree_mean | K5
+    W == 1 (one GPU)        psgd_step_single                       (K1, K2, K3)
+    W > 1, distributed      K1 | all_reduce(P) | K2, K3 | all_reduce(q) | K5
+    W > 1, simulated        K1 x W | tree_mean | K2, K3 x W | tree_mean | K5
+
+Every mode can be captured into one CUDA graph (`capture()`), the NCCL
+all-reduces of the distributed mode included.
 
 Q is seeded exactly as the reference (derive_rng(seed, "warm_start_init",
 param_index), compressors.py:362-367) and CommStats are charged exactly as the
@@ -51,10 +54,13 @@ class PowerSGDEngine:
     workers: simulated workers on this device (the reference's W-list model);
              must be 1 when `comm` is a DistributedCommunicator.
     comm:    Communicator / DistributedCommunicator whose CommStats are charged.
+    exchange: run the W > 1 exchange sequence (K1, all-reduce P, K2/K3,
+             all-reduce q, K5) even when the distributed group has one rank, so the
+             collectives are issued (tests the NCCL path on a single GPU).
     """
 
     def __init__(self, specs, rank, *, workers=1, comm=None, seed=0, device=None,
-                 error_feedback=True, param_indices=None):
+                 error_feedback=True, param_indices=None, exchange=False):
         self.specs = list(specs)
         # the reference's param_index (seeds the warm start): catalog position, or the
         # caller's global indices when the specs are a subset (e.g. one DDP bucket)
@@ -71,6 +77,10 @@ class PowerSGDEngine:
             raise ValueError(f"expected {comm.world_size} workers, got {workers}")
         self.world = comm.world_size if self.distributed else int(workers)
         self.nlocal = 1 if self.distributed else int(workers)
+        if exchange and not self.distributed:
+            raise ValueError("exchange=True needs a DistributedCommunicator")
+        self.exchange = bool(exchange) or self.world > 1
+        self.plan_world = max(2, self.world) if self.exchange else 1
         self.comm = comm
         self.stats = comm.stats if comm is not None else CommStats()
         self.seed = int(seed)
@@ -87,7 +97,7 @@ class PowerSGDEngine:
         self.nbias = off
 
         shapes = [self.specs[pi].matrix_shape for pi in self.mat_index]
-        self.plan = Plan(shapes, self.rank, self.world, self.nbias, device)
+        self.plan = Plan(shapes, self.rank, self.plan_world, self.nbias, device)
         dev = self.device = self.plan.device
         pl = self.plan
         z = dict(dtype=torch.float32, device=dev)
@@ -100,7 +110,7 @@ class PowerSGDEngine:
         self.Pm = torch.zeros(pl.p_elems, **z) if L > 1 else self.P[0]
         self.Phat = torch.zeros(pl.p_elems, **z)
         self.Q = torch.zeros(pl.q_elems, **z)
-        self.qbuf = [torch.zeros(pl.q_elems, **z) for _ in range(L)] if self.world > 1 else None
+        self.qbuf = [torch.zeros(pl.q_elems, **z) for _ in range(L)] if self.exchange else None
         self.bias_out = torch.zeros(max(1, self.nbias), **z)
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         # EF off: the EF output of K3 lands in a scratch buffer nobody reads
@@ -156,32 +166,30 @@ class PowerSGDEngine:
         h = pl.handle
         e = self.e if self.error_feedback else [self._e_scratch] * self.nlocal
         ein = self.e if self.error_feedback else [None] * self.nlocal
-        if self.world == 1 and self.error_feedback:
+        if not self.exchange and self.error_feedback:
             _lib.check(lib.psgd_step_single(h, ptr(self.g[0]), ptr(e[0]), ptr(self.work[0]), ptr(self.Q),
                                             ptr(self.P[0]), ptr(self.Phat), ptr(self.bias_g[0]), ptr(self.repl),
                                             ptr(self.bias_out), ptr(self.status), sp), "psgd_step_single")
             return
         for w in range(self.nlocal):      # K1: delta = g + e, P = delta Q  (e NULL: EF off)
             _lib.check(lib.psgd_ef_p(h, ptr(self.g[w]), ptr(ein[w]), ptr(self.work[w]), ptr(self.Q),
-                                     ptr(self.P[w]), ptr(self.Phat), ptr(self.repl), ptr(self.bias_g[w]),
-                                     ptr(self.status), sp), "psgd_ef_p")
-        if self.distributed:              # AR1 (P + bias + flags), / W fused into K3
-            self.comm.all_reduce_sum_(self.P[0])
+                                     ptr(self.P[w]), ptr(self.bias_g[w]), ptr(self.status), sp), "psgd_ef_p")
+        if self.distributed:              # AR1 (P + bias + flags), / W fused into K2
+            self.comm.all_reduce_sum_(self.P[0], force=self.exchange)
             div = self.world
         elif self.nlocal > 1:
             tree_mean_(self.P, self.Pm, stream)
             div = 1
         else:
             div = 1
-        qout = self.Q if self.world == 1 else None
-        for w in range(self.nlocal):      # K3: GS, q_w, e (+ M-hat and Q at W=1)
-            q_w = qout if qout is not None else self.qbuf[w]
+        for w in range(self.nlocal):      # K2 + K3: GS, q_w, e (+ M-hat and Q when there is no exchange)
+            q_w = self.qbuf[w] if self.exchange else self.Q
             _lib.check(lib.psgd_q_ef(h, ptr(self.work[w]), ptr(self.Pm), div, ptr(self.repl), ptr(self.Phat),
                                      ptr(q_w), ptr(e[w]), ptr(self.bias_out), ptr(self.status), sp), "psgd_q_ef")
-        if self.world == 1:
+        if not self.exchange:
             return
         if self.distributed:              # AR2 (q), then Q-bar = q / W and M-hat
-            self.comm.all_reduce_sum_(self.qbuf[0])
+            self.comm.all_reduce_sum_(self.qbuf[0], force=True)
             _lib.check(lib.psgd_decompress(h, ptr(self.Phat), ptr(self.qbuf[0]), self.world, ptr(self.Q),
                                            ptr(self.work[0]), ptr(self.status), sp), "psgd_decompress")
         else:
@@ -246,9 +254,13 @@ class PowerSGDEngine:
             self.check()
 
     def capture(self):
-        """Capture the step into a CUDA graph (single-device modes); later `run`s replay it."""
+        """Capture the step into a CUDA graph; later `run`s replay it.  In the
+        distributed mode the two NCCL all-reduces are captured with the kernels
+        (the communicator is initialised by a warm-up collective first)."""
         if self.distributed:
-            raise NotImplementedError("graph capture of the NCCL path is not enabled")
+            warm = torch.zeros(1, dtype=torch.float32, device=self.device)
+            self.comm.all_reduce_sum_(warm, force=True)
+            torch.cuda.synchronize(self.device)
         s = torch.cuda.Stream(device=self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()
@@ -276,7 +288,7 @@ class PowerSGDEngine:
                 raise NonFiniteGradient(*site)
             raise ContractViolation("orthogonalize input contains non-finite entries")
         if st & _lib.STATUS_REPLACEMENT:
-            raise RuntimeError("Gram-Schmidt needed more than one replacement draw for a column")
+            raise RuntimeError(f"Gram-Schmidt needed more than {_lib.REPL_ATTEMPTS} replacement draws for a column")
 
     def _first_nonfinite(self):
         """(param name, worker) of the first non-finite gradient, worker-major as

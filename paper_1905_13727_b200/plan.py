@@ -68,14 +68,21 @@ class Plan:
         return self.info.p_bias_off
 
     def repl_table(self):
-        """linalg.py:54-58 replacement columns (attempt 0) of every (matrix, column),
-        float64 on the device, column-major per matrix at MatrixInfo.repl_off."""
+        """linalg.py:54-58 replacement columns, float64 on the device: for every distinct
+        row count n, column j of attempt a at repl_off + (a * repl_cols + j) * n
+        (a < REPL_ATTEMPTS).  The draws depend on (n, j, attempt) only, so matrices
+        with equal n share one table."""
         if self._repl is None:
             host = np.zeros(max(1, self.info.repl_elems), dtype=np.float64)
+            done = set()
             for mi in self.matrices:
-                for j in range(mi.r_eff):
-                    o = mi.repl_off + j * mi.n
-                    host[o:o + mi.n] = replacement_column(mi.n, j, 0)
+                if mi.repl_off in done:
+                    continue
+                done.add(mi.repl_off)
+                for a in range(_lib.REPL_ATTEMPTS):
+                    for j in range(mi.repl_cols):
+                        o = mi.repl_off + (a * mi.repl_cols + j) * mi.n
+                        host[o:o + mi.n] = replacement_column(mi.n, j, a)
             self._repl = torch.from_numpy(host).to(self.device)
         return self._repl
 

@@ -26,6 +26,8 @@ def test_reference_arm_line():
     assert d["metric"].startswith("PowerSGD") and d["value"] > 0 and d["warmup"] >= 3
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["config"]["workload"] == "resnet18 rank 2, W=1"  # identical to the B200 arm's
+    assert "numpy" in d["cpu_baseline"] and "cpu_model" in d["cpu_baseline"]
 
 
 @pytest.mark.gpu
@@ -35,7 +37,8 @@ def test_b200_arm_line():
               "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] >= 3 and d["higher_is_better"] is False
-    assert d["config"]["workload"].startswith("resnet18") and "l2" in d["config"]
+    assert d["config"]["workload"] == "resnet18 rank 2, W=1" and "l2" in d["config"]
+    assert d["config"]["back_to_back_ms"] > 0
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5 and r["peak"] > 1000
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
