@@ -83,7 +83,7 @@ struct MatDev {
   long long flat_off, p_off, q_off, repl_off;
   int n, m, r, tall;
   int lg1, qs;  // lg1: log2 lanes per row in K1 (2..9); qs: Q staged in smem by K1
-  int nck, pad1;  // nck: K1 chunks of the matrix
+  int nck, pipe;  // nck: K1 chunks of the matrix; pipe: q / EF / M-hat by k3_pipe (n <= 512, r <= 8)
   int qld, rcols;  // Q is column-major: element (j, k) at q_off + k * qld + j, qld = align4(m);
                   // rcols: columns per attempt of the replacement table at repl_off (shared by equal n)
 };
@@ -160,6 +160,18 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
           su32(dst)),
       "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
       : "memory");
+}
+// 2-D tiled tensor copy global -> shared (TMA, SASS UTMALDG): box at (x = column, y = row)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bar_named(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 #ifndef PSGD_STORE_HINT
 #define PSGD_STORE_HINT 1
@@ -1254,6 +1266,208 @@ __global__ void __launch_bounds__(kThreads, 2)
   }  // !TALL
 }
 
+// ============================================================================= K3 pipeline
+// k3_pipe: q_w = delta^T P-hat, e = delta - P-hat q_w^T and (W = 1) M-hat for
+// every matrix with n <= 512 (compressors.py:339, 375-378; optimizer.py:124-127),
+// as one persistent warp-specialised kernel (1 CTA per SM):
+//   producer warp: takes the next column slab (all n rows x C columns of one
+//     matrix, <= 64 KB) from a global counter (dynamic balance), stages it into
+//     shared memory with 2-D tensor TMA (one box per 256 rows) plus P-hat's n x r
+//     rows with a 1-D bulk copy, on a 2-3 stage mbarrier ring;
+//   8 consumer warps: q from the staged slab (fixed-order warp-shuffle + smem
+//     reduction), then e (and M-hat) from the same staged bytes, float4
+//     streaming stores.  delta is read from HBM once.
+// Slabs of matrices without a tensor map (m % 4 != 0, or beyond K3P_MAXMAPS)
+// are loaded by the consumers themselves (scalar, "direct").  Launched with
+// programmatic dependent launch after K2: delta is final when it starts (K2
+// began after K1 completed), so the slab loads overlap K2; P-hat is fetched
+// after griddepcontrol.wait.
+
+constexpr int K3P_CW = 16;                     // consumer warps
+constexpr int K3P_CT = 32 * K3P_CW;            // consumer threads
+constexpr int K3P_SLAB = 16384;                // floats of delta per stage (all rows x C columns)
+constexpr int K3P_MAXMAPS = 48;
+
+struct PipeItem {
+  int mat, c0, C, map;  // map < 0: direct (consumer) loads
+};
+struct K3Maps {
+  CUtensorMap m[K3P_MAXMAPS];
+};
+struct K3PLayout {
+  int stages, phat_floats, stage_floats;  // stage: slab | P-hat rows
+  int off_red, off_qs, off_bar, total;
+};
+struct K3PHdr {  // what the consumers need of a staged slab (written by the producer)
+  long long base, q_off;  // base: flat offset of (row 0, column c0)
+  int n, m, r, C, c0, direct, qld, live;  // live = 0: no more slabs
+};
+
+template <int R>
+__global__ void __launch_bounds__(K3P_CT + 32, 1)
+    k3_pipe(const __grid_constant__ K3Maps maps, const MatDev* __restrict__ mats, const PipeItem* __restrict__ items,
+            int nitems, K3PLayout L, float* __restrict__ work, const float* __restrict__ Phat,
+            float* __restrict__ qout, float* __restrict__ e, int write_mhat, int* __restrict__ ctr, int* status) {
+  extern __shared__ __align__(1024) unsigned char k3p_smem[];
+  float* red = reinterpret_cast<float*>(k3p_smem + L.off_red);  // K3P_CW x C x r
+  float* qs = reinterpret_cast<float*>(k3p_smem + L.off_qs);    // C x r
+  uint64_t* full = reinterpret_cast<uint64_t*>(k3p_smem + L.off_bar);
+  uint64_t* empty = full + L.stages;
+  K3PHdr* hdr = reinterpret_cast<K3PHdr*>(empty + L.stages);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  if (t == 0) {
+    for (int s = 0; s < L.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], K3P_CW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == K3P_CW) {  // ---------------- producer
+    if (lane == 0) {
+      const uint64_t pol = pol_evict_first();
+      bool waited = false;
+      for (int k = 0;; ++k) {
+        const int s = k % L.stages;
+        mbar_wait(&empty[s], ((k / L.stages) & 1) ^ 1);
+        const int it = atomicAdd(ctr, 1);
+        if (it >= nitems) {
+          hdr[s].live = 0;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        const PipeItem pi = items[it];
+        const MatDev md = mats[pi.mat];
+        float* dst = reinterpret_cast<float*>(k3p_smem) + (long long)s * L.stage_floats;
+        const int br = md.n < 256 ? md.n : 256;
+        const int nbox = (md.n + br - 1) / br;
+        const uint32_t pb = (uint32_t)(((md.n * md.r + 3) & ~3) * 4);
+        hdr[s] = K3PHdr{md.flat_off + pi.c0, md.q_off, md.n, md.m, md.r, pi.C, pi.c0, pi.map < 0, md.qld, 1};
+        mbar_expect_tx(&full[s], (pi.map >= 0 ? (uint32_t)(nbox * br * pi.C * 4) : 0u) + pb);
+        if (pi.map >= 0)
+          for (int b = 0; b < nbox; ++b) tma_load_2d(dst + b * br * pi.C, &maps.m[pi.map], pi.c0, b * br, &full[s], pol);
+        if (!waited) {  // P-hat is K2's output
+          pdl_wait();
+          waited = true;
+        }
+        tma_load(dst + K3P_SLAB, Phat + md.p_off, pb, &full[s], pol);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  pdl_wait();  // K2 complete: P-hat and the status word are final
+  const bool skip = (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) != 0;  // mutate nothing
+  for (int k = 0;; ++k) {
+    const int s = k % L.stages;
+    mbar_wait(&full[s], (k / L.stages) & 1);
+    const K3PHdr hd = hdr[s];
+    if (!hd.live) break;
+    const int n = hd.n, m = hd.m, r = hd.r, C = hd.C, c0 = hd.c0;
+    const float* slab = reinterpret_cast<const float*>(k3p_smem) + (long long)s * L.stage_floats;
+    const float* ph = slab + K3P_SLAB;
+    const long long base = hd.base;
+    if (!skip) {
+      if (hd.direct) {  // direct: the consumers stage the slab themselves
+        float* ds = const_cast<float*>(slab);
+        for (int idx = t; idx < n * C; idx += K3P_CT) {
+          const int i = idx / C, c = idx - i * C;
+          ds[idx] = c0 + c < m ? __ldcs(work + base + (long long)i * m + c) : 0.f;
+        }
+        bar_named(1, K3P_CT);
+      }
+      const int CQ = C >> 2, RG = K3P_CT / CQ;
+      const int cq = t & (CQ - 1), rg = t / CQ;
+      // 1. per-thread partial q over rows rg, rg + RG, ...
+      float qp[4][R];
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int kk = 0; kk < R; ++kk) qp[v][kk] = 0.f;
+#pragma unroll 4
+      for (int i = rg; i < n; i += RG) {
+        const float4 d = *reinterpret_cast<const float4*>(slab + i * C + 4 * cq);
+#pragma unroll
+        for (int kk = 0; kk < R; ++kk) {
+          if (kk < r) {
+            const float p = ph[i * r + kk];
+            qp[0][kk] = fmaf(d.x, p, qp[0][kk]);
+            qp[1][kk] = fmaf(d.y, p, qp[1][kk]);
+            qp[2][kk] = fmaf(d.z, p, qp[2][kk]);
+            qp[3][kk] = fmaf(d.w, p, qp[3][kk]);
+          }
+        }
+      }
+      // 2. fixed-order reduction: lanes of a warp that share cq (butterfly), then warps in order
+      for (int off = CQ; off < 32; off <<= 1)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+          for (int kk = 0; kk < R; ++kk) qp[v][kk] += __shfl_xor_sync(0xffffffffu, qp[v][kk], off);
+      bar_named(1, K3P_CT);  // every consumer is done with the previous slab's qs
+      if (lane < CQ)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+          for (int kk = 0; kk < R; ++kk)
+            if (kk < r) red[(warp * C + 4 * cq + v) * r + kk] = qp[v][kk];
+      bar_named(1, K3P_CT);
+      for (int o = t; o < C * r; o += K3P_CT) {
+        float sacc = 0.f;
+        for (int w = 0; w < K3P_CW; ++w) sacc += red[w * C * r + o];
+        qs[o] = sacc;
+        const int c = o / r, kk = o - c * r;
+        if (c0 + c < m) qout[hd.q_off + (long long)kk * hd.qld + c0 + c] = sacc;  // column-major Q
+      }
+      bar_named(1, K3P_CT);
+      // 3. e = delta - P-hat q^T (and M-hat) from the staged slab
+      float qv[4][R];
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int kk = 0; kk < R; ++kk) qv[v][kk] = kk < r ? qs[(4 * cq + v) * r + kk] : 0.f;
+      const int col = c0 + 4 * cq;
+      if (col < m) {
+        const bool vec = !hd.direct;  // tensor-mapped matrices have m % 4 == 0: whole float4 in range
+#pragma unroll 4
+        for (int i = rg; i < n; i += RG) {
+          const float4 d = *reinterpret_cast<const float4*>(slab + i * C + 4 * cq);
+          float mh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int kk = 0; kk < R; ++kk) {
+            if (kk < r) {
+              const float p = ph[i * r + kk];
+#pragma unroll
+              for (int v = 0; v < 4; ++v) mh[v] = fmaf(p, qv[v][kk], mh[v]);
+            }
+          }
+          const long long a = base + (long long)i * m + 4 * cq;
+          if (vec) {
+            st_stream(reinterpret_cast<float4*>(e + a), make_float4(d.x - mh[0], d.y - mh[1], d.z - mh[2], d.w - mh[3]));
+            if (write_mhat) st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
+          } else {
+            const float dv[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              if (col + v < m) {
+                st_stream(e + a + v, dv[v] - mh[v]);
+                if (write_mhat) st_stream(work + a + v, mh[v]);
+              }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (t == 0 && atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {  // last CTA out resets the counters
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
+}
+
 // K4 / K5 row streaming.  MODE 0 (K4): e = delta - P-hat q^T (+ M-hat in place
 // when write_mhat).  MODE 1 (K5): M-hat = P-hat (q / div)^T; items with
 // row0 == 0 store Q-bar = q / div.
@@ -1823,6 +2037,16 @@ struct psgd_plan {
   long long wsg_elems = 0;
   std::vector<SlabItem> k3;          // fused and tall slabs, grouped by r
   std::vector<Group> g3;
+  // K3 pipeline (k3_pipe): slab items, the matrices with a tensor map (map order), layout
+  std::vector<PipeItem> pipe_items;
+  std::vector<int> pipe_maps, pipe_mapC;
+  K3PLayout k3pl{};
+  int pipe_rmax = 1;
+  PipeItem* d_pipe_items = nullptr;
+  int* d_pipe_ctr = nullptr;
+  mutable std::mutex map_mu;               // tensor maps encode the work buffer's address:
+  mutable const float* maps_for = nullptr;  // re-encoded when a call passes another buffer
+  mutable K3Maps maps{};
 
   // tall path
   std::vector<int> tall_list, all_list;
@@ -2023,7 +2247,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       delete pl;
       return fail(PSGD_EINVAL, "effective rank " + std::to_string(md.r) + " exceeds PSGD_MAX_RANK");
     }
-    md.tall = k3_tall_config(md.n, md.m, md.r).nchunks > 1;
+    md.pipe = (md.n <= kFusedNMax && md.r <= 8) ? 1 : 0;  // k3_pipe: q, EF and M-hat from one staged slab
+    md.tall = !md.pipe && k3_tall_config(md.n, md.m, md.r).nchunks > 1;
     md.lg1 = 5;  // set with the K1 chunk geometry below
     md.qs = 0;  // decided below, once the K1 smem budget is known
     md.flat_off = fo;
@@ -2184,7 +2409,12 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     }
   }
   pl->k2_wblocks = ((int)pl->wlist.size() + K2_THREADS / 32 - 1) / (K2_THREADS / 32);
-  pl->k2_smem = std::max(pl->k2_smem, pl->k2_wregion * (K2_THREADS / 32) * 8);
+  {  // the warp items need smem only when one is beyond the register MGS (n > 512 or r > 4): with no
+     // dynamic smem K2's CTAs fit beside K1's on an SM and wait there (PDL) instead of launching late
+    bool smem_warp = false;
+    for (int mi : pl->wlist) smem_warp |= pl->mats[mi].n > 512 || pl->mats[mi].r > 4;
+    if (smem_warp) pl->k2_smem = std::max(pl->k2_smem, pl->k2_wregion * (K2_THREADS / 32) * 8);
+  }
   // ---- K3 slabs, grouped by r (one launch per group): fused slabs hold all rows
   {
     std::vector<int> rs;
@@ -2194,7 +2424,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       Group gp{r, (int)pl->k3.size(), 0, 0, tall};
       for (int mi = 0; mi < nmat; ++mi) {
         const MatDev& md = pl->mats[mi];
-        if (md.r != r) continue;
+        if (md.r != r || md.pipe) continue;
         const K3Cfg cf = k3_tall_config(md.n, md.m, r);
         if ((cf.nchunks > 1) != (tall == 1)) continue;
         if (tall && k3_tileable(md)) continue;  // K3 column tiles instead
@@ -2225,6 +2455,48 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       gp.end = (int)pl->k3.size();
       if (gp.end > gp.beg) pl->g3.push_back(gp);
     }
+  }
+  // ---- K3 pipeline slabs: all n rows x C columns, C a power of two with the slab <= 64 KB
+  {
+    long long phf = 4, redf = 4;
+    for (int mi = 0; mi < nmat; ++mi) {
+      const MatDev& md = pl->mats[mi];
+      if (!md.pipe) continue;
+      const int rows_pad = md.n <= 256 ? md.n : (md.n + 255) / 256 * 256;
+      int C = 4;
+      while (C < 128 && C < md.m && (long long)(2 * C) * rows_pad <= K3P_SLAB) C *= 2;
+      int map = -1;
+      if (md.m % 4 == 0 && md.flat_off % 4 == 0 && (int)pl->pipe_maps.size() < K3P_MAXMAPS) {
+        map = (int)pl->pipe_maps.size();
+        pl->pipe_maps.push_back(mi);
+        pl->pipe_mapC.push_back(C);
+      }
+      for (int c0 = 0; c0 < md.m; c0 += C) pl->pipe_items.push_back({mi, c0, C, map});
+      phf = std::max(phf, align4((long long)md.n * md.r));
+      redf = std::max(redf, (long long)K3P_CW * C * md.r);
+      pl->pipe_rmax = std::max(pl->pipe_rmax, rmax_of(md.r));
+    }
+    // largest slabs first: the dynamic schedule then ends on small ones
+    std::stable_sort(pl->pipe_items.begin(), pl->pipe_items.end(), [&](const PipeItem& a, const PipeItem& b) {
+      const long long wa = (long long)pl->mats[a.mat].n * std::min(a.C, pl->mats[a.mat].m - a.c0);
+      const long long wb = (long long)pl->mats[b.mat].n * std::min(b.C, pl->mats[b.mat].m - b.c0);
+      return wa > wb;
+    });
+    K3PLayout& L = pl->k3pl;
+    L.phat_floats = (int)phf;
+    L.stage_floats = (int)((K3P_SLAB + phf + 255) / 256 * 256);
+    const long long qsf = 128 * 8;
+    auto total_for = [&](int stages) {
+      long long off = (long long)stages * L.stage_floats * 4;
+      off += (redf + qsf) * 4;
+      off = (off + 15) & ~15LL;
+      return off + 2LL * stages * 8 + (long long)stages * sizeof(K3PHdr) + 16;
+    };
+    L.stages = total_for(3) <= 227 * 1024 ? 3 : 2;
+    L.off_red = L.stages * L.stage_floats * 4;
+    L.off_qs = L.off_red + (int)redf * 4;
+    L.off_bar = (L.off_qs + (int)qsf * 4 + 15) & ~15;
+    L.total = (int)total_for(L.stages);
   }
   build_row_items(pl->mats, true, pl->k4, pl->g4);
   build_tile_items(pl->mats, pl->k4t, pl->g4t);
@@ -2293,6 +2565,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_k3to = take(pl->k3t_off.size() * sizeof(long long));
   const size_t o_k3tp = take((size_t)std::max(1LL, pl->k3t_part_elems) * sizeof(float));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
+  const size_t o_pipe = take(pl->pipe_items.size() * sizeof(PipeItem));
+  const size_t o_pctr = take(2 * sizeof(int));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
   const size_t o_wsq = take((size_t)std::max(1LL, pl->wsq_elems) * sizeof(float));
   const size_t o_cnt = take((size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
@@ -2334,6 +2608,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_k3t_off = reinterpret_cast<long long*>(b + o_k3to);
   pl->d_k3t_part = reinterpret_cast<float*>(b + o_k3tp);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
+  pl->d_pipe_items = reinterpret_cast<PipeItem*>(b + o_pipe);
+  pl->d_pipe_ctr = reinterpret_cast<int*>(b + o_pctr);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
   pl->d_wsq = reinterpret_cast<float*>(b + o_wsq);
   pl->d_counters = reinterpret_cast<int*>(b + o_cnt);
@@ -2367,6 +2643,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_k3t_list, pl->k3t_list.data(), pl->k3t_list.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_k3t_off, pl->k3t_off.data(), pl->k3t_off.size() * sizeof(long long));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
+  if (ce == cudaSuccess) ce = up(pl->d_pipe_items, pl->pipe_items.data(), pl->pipe_items.size() * sizeof(PipeItem));
+  if (ce == cudaSuccess) ce = cudaMemset(pl->d_pipe_ctr, 0, 2 * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_split_cnt, 0, std::max<size_t>(16, pl->splits.size() * sizeof(int)));
   if (ce != cudaSuccess) {
@@ -2412,7 +2690,8 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
     const bool bias_in_k3 = !small && !pl->gram_items.empty() && !pl->g3.empty();
     o->launches_orthogonalize = ((small || (pl->nbias > 0 && !bias_in_k3)) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 3);
   }
-  o->launches_q_ef = o->launches_orthogonalize + nonempty(pl->g3) + nonempty(pl->g4) + nonempty(pl->g4t) +
+  o->launches_q_ef = o->launches_orthogonalize + (pl->pipe_items.empty() ? 0 : 1) + nonempty(pl->g3) +
+                     nonempty(pl->g4) + nonempty(pl->g4t) +
                      nonempty(pl->g4t2) +
                      (pl->k3t.empty() ? 0 : 2);
   (void)any_fused;
@@ -2568,6 +2847,67 @@ struct RunK4T {
 template <int R, bool EXACT>
 using RunK5 = RunK45Mode<1>::F<R, EXACT>;
 
+
+// tensor maps of the pipeline's matrices inside `work` (encoded on the host; cached
+// per work buffer — a CUDA graph captures the maps by value with the launch)
+int encode_pipe_maps(const psgd_plan* pl, const float* work) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return fail(PSGD_ECUDA, "cuTensorMapEncodeTiled is unavailable");
+  for (size_t k = 0; k < pl->pipe_maps.size(); ++k) {
+    const MatDev& md = pl->mats[pl->pipe_maps[k]];
+    cuuint64_t dims[2] = {(cuuint64_t)md.m, (cuuint64_t)md.n};
+    cuuint64_t strides[1] = {(cuuint64_t)md.m * 4};
+    cuuint32_t box[2] = {(cuuint32_t)pl->pipe_mapC[k], (cuuint32_t)std::min(md.n, 256)};
+    cuuint32_t es[2] = {1, 1};
+    const CUresult cr = encode(&pl->maps.m[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                               const_cast<float*>(work) + md.flat_off, dims, strides, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(PSGD_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+  }
+  pl->maps_for = work;
+  return PSGD_OK;
+}
+
+template <int R>
+int launch_pipe_r(const psgd_plan* pl, float* work, const float* phat, float* qout, float* e, int* status,
+                  cudaStream_t st) {
+  auto kern = k3_pipe<R>;
+  PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->k3pl.total));
+  const int grid = (int)std::min<size_t>(pl->nsm, pl->pipe_items.size());
+  K3Maps maps;
+  {
+    std::lock_guard<std::mutex> lk(pl->map_mu);
+    if (pl->maps_for != work) {
+      const int rc = encode_pipe_maps(pl, work);
+      if (rc) return rc;
+    }
+    maps = pl->maps;
+  }
+  PSGD_CUDA_CHECK(launch_ex(kern, grid, K3P_CT + 32, (size_t)pl->k3pl.total, st, PSGD_PDL != 0, maps,
+                            (const MatDev*)pl->d_mats, (const PipeItem*)pl->d_pipe_items, (int)pl->pipe_items.size(),
+                            pl->k3pl, work, phat, qout, e, pl->world == 1 ? 1 : 0, pl->d_pipe_ctr, status));
+  return PSGD_OK;
+}
+
+int launch_pipe(const psgd_plan* pl, float* work, const float* phat, float* qout, float* e, int* status,
+                cudaStream_t st) {
+  if (pl->pipe_items.empty()) return PSGD_OK;
+  switch (pl->pipe_rmax) {
+    case 1: return launch_pipe_r<1>(pl, work, phat, qout, e, status, st);
+    case 2: return launch_pipe_r<2>(pl, work, phat, qout, e, status, st);
+    case 4: return launch_pipe_r<4>(pl, work, phat, qout, e, status, st);
+    default: return launch_pipe_r<8>(pl, work, phat, qout, e, status, st);
+  }
+}
+
 bool check_dev(const psgd_plan* pl) {
   int dev = -1;
   cudaGetDevice(&dev);
@@ -2665,6 +3005,8 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
     if (rc) return rc;
   }
   bool bias_done = !bias_in_k3;
+  rc = launch_pipe(pl, work, p_hat, q_out, e, (int*)status, st);  // K3 pipeline (n <= 512)
+  if (rc) return rc;
   for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab (after K2: delta is final)
     rc = dispatch_r<RunK3>(gp.r, pl, gp, work, p, (int)divisor, repl, p_hat, q_out, e, bias_out,
                            bias_done ? 0LL : (long long)pl->nbias, (int*)status, st);
