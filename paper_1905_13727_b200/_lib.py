@@ -96,7 +96,7 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        _lib = load()
+        _lib = load(os.environ.get("PSGD_LIB", LIB_PATH))  # PSGD_LIB: an in-tree experiment build
     return _lib
 
 

@@ -1285,6 +1285,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 
 constexpr int K3P_CW = 16;                     // consumer warps
 constexpr int K3P_CT = 32 * K3P_CW;            // consumer threads
+#ifndef PSGD_K3P_GROUPS
+#define PSGD_K3P_GROUPS 2
+#endif
+constexpr int K3P_GROUPS = PSGD_K3P_GROUPS;    // consumer groups taking alternate stages
+constexpr int K3P_GW = K3P_CW / K3P_GROUPS;    // warps per group
+constexpr int K3P_GT = 32 * K3P_GW;            // threads per group
+constexpr int K3P_QS = 128 * 8;                // qs floats per group (C <= 128, r <= 8)
 constexpr int K3P_SLAB = 16384;                // floats of delta per stage (all rows x C columns)
 constexpr int K3P_MAXMAPS = 48;
 
@@ -1295,8 +1302,9 @@ struct K3Maps {
   CUtensorMap m[K3P_MAXMAPS];
 };
 struct K3PLayout {
-  int stages, phat_floats, stage_floats;  // stage: slab | P-hat rows
+  int stages, phat_floats, stage_floats, slab_floats;  // stage: slab (slab_floats) | P-hat rows
   int off_red, off_qs, off_bar, total;
+  int red_floats;  // per consumer group: K3P_GW x C x r
 };
 struct K3PHdr {  // what the consumers need of a staged slab (written by the producer)
   long long base, q_off;  // base: flat offset of (row 0, column c0)
@@ -1309,8 +1317,6 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
             int nitems, K3PLayout L, float* __restrict__ work, const float* __restrict__ Phat,
             float* __restrict__ qout, float* __restrict__ e, int write_mhat, int* __restrict__ ctr, int* status) {
   extern __shared__ __align__(1024) unsigned char k3p_smem[];
-  float* red = reinterpret_cast<float*>(k3p_smem + L.off_red);  // K3P_CW x C x r
-  float* qs = reinterpret_cast<float*>(k3p_smem + L.off_qs);    // C x r
   uint64_t* full = reinterpret_cast<uint64_t*>(k3p_smem + L.off_bar);
   uint64_t* empty = full + L.stages;
   K3PHdr* hdr = reinterpret_cast<K3PHdr*>(empty + L.stages);
@@ -1318,7 +1324,7 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
   if (t == 0) {
     for (int s = 0; s < L.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], K3P_CW);
+      mbar_init(&empty[s], K3P_GW);  // a stage is consumed by one group
     }
     fence_mbar_init();
   }
@@ -1328,17 +1334,25 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
     if (lane == 0) {
       const uint64_t pol = pol_evict_first();
       bool waited = false;
-      for (int k = 0;; ++k) {
+      // one item of lookahead: the next slab's index (global atomic) and descriptors
+      // are fetched while the current slab's copies fly, so the dependent
+      // atomic -> item -> matrix loads are off the issue path
+      int it = atomicAdd(ctr, 1);
+      PipeItem pi{};
+      MatDev md{};
+      if (it < nitems) {
+        pi = items[it];
+        md = mats[pi.mat];
+      }
+      for (int k = 0, ends = 0; ends < K3P_GROUPS; ++k) {
         const int s = k % L.stages;
         mbar_wait(&empty[s], ((k / L.stages) & 1) ^ 1);
-        const int it = atomicAdd(ctr, 1);
-        if (it >= nitems) {
+        if (it >= nitems) {  // one end marker per consumer group (groups take alternate stages)
           hdr[s].live = 0;
           mbar_arrive(&full[s]);
-          break;
+          ++ends;
+          continue;
         }
-        const PipeItem pi = items[it];
-        const MatDev md = mats[pi.mat];
         float* dst = reinterpret_cast<float*>(k3p_smem) + (long long)s * L.stage_floats;
         const int br = md.n < 256 ? md.n : 256;
         const int nbox = (md.n + br - 1) / br;
@@ -1351,35 +1365,49 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
           pdl_wait();
           waited = true;
         }
-        tma_load(dst + K3P_SLAB, Phat + md.p_off, pb, &full[s], pol);
+        tma_load(dst + L.slab_floats, Phat + md.p_off, pb, &full[s], pol);
+        it = atomicAdd(ctr, 1);
+        if (it < nitems) {
+          pi = items[it];
+          md = mats[pi.mat];
+        }
       }
     }
     return;
   }
 
-  // ---------------- consumers
+  // ---------------- consumers: K3P_GROUPS groups of K3P_GW warps take alternate
+  // stages (ping-pong), so one group's q reduction overlaps the other's stores
+  const int grp = warp / K3P_GW, gw = warp - grp * K3P_GW, gt = t - grp * K3P_GT;
+  float* red = reinterpret_cast<float*>(k3p_smem + L.off_red) + grp * L.red_floats;  // K3P_GW x C x r
+  float* qs = reinterpret_cast<float*>(k3p_smem + L.off_qs) + grp * K3P_QS;          // C x r
+  const int bar_id = 1 + grp;
   pdl_wait();  // K2 complete: P-hat and the status word are final
   const bool skip = (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) != 0;  // mutate nothing
-  for (int k = 0;; ++k) {
+  for (int k = grp;; k += K3P_GROUPS) {
     const int s = k % L.stages;
     mbar_wait(&full[s], (k / L.stages) & 1);
     const K3PHdr hd = hdr[s];
     if (!hd.live) break;
     const int n = hd.n, m = hd.m, r = hd.r, C = hd.C, c0 = hd.c0;
     const float* slab = reinterpret_cast<const float*>(k3p_smem) + (long long)s * L.stage_floats;
-    const float* ph = slab + K3P_SLAB;
+    const float* ph = slab + L.slab_floats;
     const long long base = hd.base;
+#ifdef PSGD_K3P_NOCONSUME
+    if (false) {
+#else
     if (!skip) {
+#endif
       if (hd.direct) {  // direct: the consumers stage the slab themselves
         float* ds = const_cast<float*>(slab);
-        for (int idx = t; idx < n * C; idx += K3P_CT) {
+        for (int idx = gt; idx < n * C; idx += K3P_GT) {
           const int i = idx / C, c = idx - i * C;
           ds[idx] = c0 + c < m ? __ldcs(work + base + (long long)i * m + c) : 0.f;
         }
-        bar_named(1, K3P_CT);
+        bar_named(bar_id, K3P_GT);
       }
-      const int CQ = C >> 2, RG = K3P_CT / CQ;
-      const int cq = t & (CQ - 1), rg = t / CQ;
+      const int CQ = C >> 2, RG = K3P_GT / CQ;
+      const int cq = gt & (CQ - 1), rg = gt / CQ;
       // 1. per-thread partial q over rows rg, rg + RG, ...
       float qp[4][R];
 #pragma unroll
@@ -1406,22 +1434,22 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
         for (int v = 0; v < 4; ++v)
 #pragma unroll
           for (int kk = 0; kk < R; ++kk) qp[v][kk] += __shfl_xor_sync(0xffffffffu, qp[v][kk], off);
-      bar_named(1, K3P_CT);  // every consumer is done with the previous slab's qs
+      bar_named(bar_id, K3P_GT);  // every thread of the group is done with the previous slab's qs
       if (lane < CQ)
 #pragma unroll
         for (int v = 0; v < 4; ++v)
 #pragma unroll
           for (int kk = 0; kk < R; ++kk)
-            if (kk < r) red[(warp * C + 4 * cq + v) * r + kk] = qp[v][kk];
-      bar_named(1, K3P_CT);
-      for (int o = t; o < C * r; o += K3P_CT) {
+            if (kk < r) red[(gw * C + 4 * cq + v) * r + kk] = qp[v][kk];
+      bar_named(bar_id, K3P_GT);
+      for (int o = gt; o < C * r; o += K3P_GT) {
         float sacc = 0.f;
-        for (int w = 0; w < K3P_CW; ++w) sacc += red[w * C * r + o];
+        for (int w = 0; w < K3P_GW; ++w) sacc += red[w * C * r + o];
         qs[o] = sacc;
         const int c = o / r, kk = o - c * r;
         if (c0 + c < m) qout[hd.q_off + (long long)kk * hd.qld + c0 + c] = sacc;  // column-major Q
       }
-      bar_named(1, K3P_CT);
+      bar_named(bar_id, K3P_GT);
       // 3. e = delta - P-hat q^T (and M-hat) from the staged slab
       float qv[4][R];
 #pragma unroll
@@ -1429,7 +1457,11 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
 #pragma unroll
         for (int kk = 0; kk < R; ++kk) qv[v][kk] = kk < r ? qs[(4 * cq + v) * r + kk] : 0.f;
       const int col = c0 + 4 * cq;
+#ifdef PSGD_K3P_NOSTORE
+      if (col < 0) {
+#else
       if (col < m) {
+#endif
         const bool vec = !hd.direct;  // tensor-mapped matrices have m % 4 == 0: whole float4 in range
 #pragma unroll 4
         for (int i = rg; i < n; i += RG) {
@@ -1462,9 +1494,13 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  if (t == 0 && atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {  // last CTA out resets the counters
-    ctr[0] = 0;
-    ctr[1] = 0;
+  if (t == 0) {  // last CTA out resets the counters
+    // (group 0's thread 0; group 1 may still be draining, but the producer's atomics are done:
+    //  it sent both end markers only after its final atomicAdd)
+    if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
   }
 }
 
@@ -2459,12 +2495,15 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   // ---- K3 pipeline slabs: all n rows x C columns, C a power of two with the slab <= 64 KB
   {
     long long phf = 4, redf = 4;
+    static const int slabf = getenv("PSGD_K3P_SLAB") ? atoi(getenv("PSGD_K3P_SLAB")) : K3P_SLAB;
+    static const int maxst = getenv("PSGD_K3P_STAGES") ? atoi(getenv("PSGD_K3P_STAGES")) : 3;
+    pl->k3pl.slab_floats = slabf;
     for (int mi = 0; mi < nmat; ++mi) {
       const MatDev& md = pl->mats[mi];
       if (!md.pipe) continue;
       const int rows_pad = md.n <= 256 ? md.n : (md.n + 255) / 256 * 256;
       int C = 4;
-      while (C < 128 && C < md.m && (long long)(2 * C) * rows_pad <= K3P_SLAB) C *= 2;
+      while (C < 128 && C < md.m && (long long)(2 * C) * rows_pad <= slabf) C *= 2;
       int map = -1;
       if (md.m % 4 == 0 && md.flat_off % 4 == 0 && (int)pl->pipe_maps.size() < K3P_MAXMAPS) {
         map = (int)pl->pipe_maps.size();
@@ -2473,7 +2512,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       }
       for (int c0 = 0; c0 < md.m; c0 += C) pl->pipe_items.push_back({mi, c0, C, map});
       phf = std::max(phf, align4((long long)md.n * md.r));
-      redf = std::max(redf, (long long)K3P_CW * C * md.r);
+      redf = std::max(redf, (long long)K3P_GW * C * md.r);
       pl->pipe_rmax = std::max(pl->pipe_rmax, rmax_of(md.r));
     }
     // largest slabs first: the dynamic schedule then ends on small ones
@@ -2484,15 +2523,18 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     });
     K3PLayout& L = pl->k3pl;
     L.phat_floats = (int)phf;
-    L.stage_floats = (int)((K3P_SLAB + phf + 255) / 256 * 256);
-    const long long qsf = 128 * 8;
+    L.stage_floats = (int)((L.slab_floats + phf + 255) / 256 * 256);
+    L.red_floats = (int)align4(redf);
+    redf = (long long)K3P_GROUPS * L.red_floats;
+    const long long qsf = (long long)K3P_GROUPS * K3P_QS;
     auto total_for = [&](int stages) {
       long long off = (long long)stages * L.stage_floats * 4;
       off += (redf + qsf) * 4;
       off = (off + 15) & ~15LL;
       return off + 2LL * stages * 8 + (long long)stages * sizeof(K3PHdr) + 16;
     };
-    L.stages = total_for(3) <= 227 * 1024 ? 3 : 2;
+    L.stages = 2;
+    while (L.stages < maxst && total_for(L.stages + 1) <= 227 * 1024) ++L.stages;
     L.off_red = L.stages * L.stage_floats * 4;
     L.off_qs = L.off_red + (int)redf * 4;
     L.off_bar = (L.off_qs + (int)qsf * 4 + 15) & ~15;

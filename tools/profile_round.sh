@@ -10,7 +10,7 @@ python bench.py --rank 4 --no-cpu > gpurun_out/bench_r4.json 2> gpurun_out/bench
 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu --no-graph > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k1_ef_p|k2_gs|k3_slab" -s 3 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"k1_ef_p|k2_gs|k3_slab|k3_pipe" -s 3 -c 3 \
     -o gpurun_out/prof_full python tools/prof_step.py --steps 3 > gpurun_out/ncu_full.log 2>&1
 
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
