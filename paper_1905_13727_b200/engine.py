@@ -238,10 +238,21 @@ class PowerSGDEngine:
 
     def run(self, stream=None):
         """Enqueue one step on `stream` (default: current) without synchronising."""
+        self._run_device(stream)
+        self._account()
+
+    def _run_device(self, stream=None):
         if self._graph is not None:
-            self._graph.replay()
+            if stream is not None:
+                with torch.cuda.stream(stream):
+                    self._graph.replay()
+            else:
+                self._graph.replay()
         else:
             self._enqueue(stream)
+
+    def _account(self):
+        """CommStats of one step, charged as the reference charges them."""
         b, f, d = self._charge
         self.stats.bits_allreduced += b
         self.stats.compress_flops += f

@@ -7,13 +7,19 @@ position, so the warm start is seeded exactly as the reference seeds it), and pe
 group the host->device copy, the compression step (optimizer.py:110-129) and the
 device->host copy of M-hat / the bias mean run on three streams:
 
-    h2d:      g_0 | g_1 | g_2 | g_3
-    compute:        step_0 | step_1 | step_2 | step_3
-    d2h:                   M_0    | M_1    | M_2    | M_3
+    h2d:      g_0 | g_1 | g_2 | ... | g_G-1
+    compute:        step_0 | step_1 | ...   | step_G-1
+    d2h:                   M_0    | M_1 ... |          M_G-1
 
 so the copies of one group overlap the other groups' compression and the two PCIe
-directions overlap each other.  Results are identical to one engine over the whole
-catalog (the reference's per-parameter loop is independent across parameters).
+directions overlap each other.  The step time is then about the bidirectional
+transfer time plus the first group's H2D and the last group's D2H, so the first
+and the last group are small (the catalog's smallest parameters) and the rest are
+balanced.  The whole multi-stream step (copies, kernels, cross-stream
+dependencies) is captured into one CUDA graph: replaying it avoids the tens of
+microseconds an eager cross-stream event hand-off costs per group.  Results are
+identical to one engine over the whole catalog (the reference's per-parameter loop
+is independent across parameters).
 """
 
 import torch
@@ -36,11 +42,49 @@ def split_groups(specs, groups):
     return [g for g in out if g]
 
 
+def transfer_groups(specs, groups, edge=0.02):
+    """Groups in transfer order for the pipelined step: a small first group (the
+    smallest parameters, ~`edge` of the bytes, so compression starts early), a small
+    last group (the next smallest, so the final D2H is short), and the remaining
+    parameters in catalog order cut into `groups - 2` groups of ~equal size.  Every
+    parameter appears exactly once; each group lists its parameters in catalog order."""
+    n = len(specs)
+    if groups < 3 or n < 3:
+        return split_groups(specs, max(1, groups))
+    total = sum(s.size for s in specs) or 1
+    by_size = sorted(range(n), key=lambda i: (specs[i].size, i))
+    first, last, acc = [], [], 0
+    it = iter(by_size)
+    for i in it:
+        first.append(i)
+        acc += specs[i].size
+        if acc >= edge * total:
+            break
+    acc = 0
+    for i in it:
+        last.append(i)
+        acc += specs[i].size
+        if acc >= edge * total:
+            break
+    taken = set(first) | set(last)
+    rest = [i for i in range(n) if i not in taken]
+    if not rest:
+        return [sorted(first), sorted(last)]
+    sub = split_groups([specs[i] for i in rest], max(1, groups - 2))
+    middle = [[rest[j] for j in g] for g in sub]
+    return [g for g in [sorted(first)] + middle + [sorted(last)] if g]
+
+
 class HostPipelinedEngine:
-    def __init__(self, specs, rank, *, groups=4, seed=0, device=None, graphs=True):
+    """graphs: "step" (default) captures the whole pipelined step into one CUDA
+    graph; "engine" captures each group's compression only (cross-stream hand-offs
+    eager); False runs everything eagerly."""
+
+    def __init__(self, specs, rank, *, groups=8, seed=0, device=None, graphs="step", order="transfer"):
         self.specs = list(specs)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.groups = split_groups(self.specs, groups)
+        self.groups = (transfer_groups(self.specs, groups) if order == "transfer"
+                       else split_groups(self.specs, groups))
         self.engines = [PowerSGDEngine([self.specs[i] for i in g], rank, seed=seed, device=self.device,
                                        param_indices=g) for g in self.groups]
         self.where = {pi: (k, j) for k, g in enumerate(self.groups) for j, pi in enumerate(g)}
@@ -52,9 +96,12 @@ class HostPipelinedEngine:
         self.s_h2d = torch.cuda.Stream(device=self.device)
         self.s_cmp = torch.cuda.Stream(device=self.device)
         self.s_d2h = torch.cuda.Stream(device=self.device)
-        if graphs:
+        self._graph = None
+        if graphs == "engine" or graphs is True:
             for e in self.engines:
                 e.capture()
+        elif graphs == "step":
+            self._capture()
 
     # host views in the spec shapes (the engines' packed layouts, pinned)
     def _host(self, flat, bias, k, j):
@@ -84,32 +131,56 @@ class HostPipelinedEngine:
     def d2h_bytes(self):
         return 4 * sum(t.numel() for t in self.out_host + self.bias_out_host)
 
-    def step(self):
-        """Enqueue one step (transfers + compression) after the current stream's work;
-        the current stream waits for the last device->host copy."""
-        cur = torch.cuda.current_stream(self.device)
+    def _enqueue(self, origin, raw):
+        """The pipelined step after `origin`'s work; `origin` waits for its end.
+        raw: launch the compression kernels directly (inside a graph capture)."""
         for s in (self.s_h2d, self.s_cmp, self.s_d2h):
-            s.wait_stream(cur)
+            s.wait_stream(origin)
         done_in, done_cmp = [], []
         with torch.cuda.stream(self.s_h2d):
             for k, e in enumerate(self.engines):
                 e.g[0].copy_(self.g_host[k], non_blocking=True)
-                e.bias_g[0].copy_(self.bias_host[k], non_blocking=True)
+                if e.nbias:
+                    e.bias_g[0].copy_(self.bias_host[k], non_blocking=True)
                 done_in.append(torch.cuda.Event())
                 done_in[-1].record(self.s_h2d)
         with torch.cuda.stream(self.s_cmp):
             for k, e in enumerate(self.engines):
                 self.s_cmp.wait_event(done_in[k])
-                e.run(self.s_cmp)
+                if raw:
+                    e._enqueue(self.s_cmp)
+                else:
+                    e._run_device(self.s_cmp)
                 done_cmp.append(torch.cuda.Event())
                 done_cmp[-1].record(self.s_cmp)
         with torch.cuda.stream(self.s_d2h):
             for k, e in enumerate(self.engines):
                 self.s_d2h.wait_event(done_cmp[k])
                 self.out_host[k].copy_(e.work[0], non_blocking=True)
-                self.bias_out_host[k].copy_(e.bias_out, non_blocking=True)
-        cur.wait_stream(self.s_d2h)
-        cur.wait_stream(self.s_cmp)
+                if e.nbias:
+                    self.bias_out_host[k].copy_(e.bias_out, non_blocking=True)
+        origin.wait_stream(self.s_d2h)
+        origin.wait_stream(self.s_cmp)
+
+    def _capture(self):
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                self._enqueue(s, raw=True)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self._graph = g
+
+    def step(self):
+        """Enqueue one step (transfers + compression) after the current stream's work;
+        the current stream waits for the last device->host copy."""
+        if self._graph is not None:
+            self._graph.replay()
+        else:
+            self._enqueue(torch.cuda.current_stream(self.device), raw=False)
+        for e in self.engines:
+            e._account()
 
     def check(self):
         for e in self.engines:

@@ -92,3 +92,20 @@ def test_compressor_accounting_matches_reference():
     assert decode_cost(LowRank(np.zeros((6, 2)), np.zeros((5, 2)))) == 2 * 6 * 5 * 2
     ctx = CompressionContext(3, 4, 5)
     assert np.array_equal(ctx.rng("x").standard_normal(3), O.derive_rng(3, "x", 4, 5).standard_normal(3))
+
+
+def test_transfer_groups_cover_every_parameter_once():
+    """pipeline.transfer_groups: small first and last groups, every parameter once."""
+    from paper_1905_13727_b200 import catalogs
+    from paper_1905_13727_b200.pipeline import transfer_groups
+    for name in ("resnet18", "lstm"):
+        specs = list(catalogs.get_catalog(name).params)
+        total = sum(s.size for s in specs)
+        for groups in (3, 4, 8, 12):
+            gs = transfer_groups(specs, groups)
+            flat = sorted(i for g in gs for i in g)
+            assert flat == list(range(len(specs)))
+            assert all(g == sorted(g) for g in gs)
+            if name == "resnet18":
+                sizes = [sum(specs[i].size for i in g) for g in gs]
+                assert sizes[0] <= 0.1 * total and sizes[-1] <= 0.1 * total, sizes

@@ -18,9 +18,10 @@ def test_groups_cover_the_catalog_in_order():
     assert [i for g in gs for i in g] == list(range(len(specs))) and len(gs) == 4
 
 
-def test_pipelined_host_step_matches_engine_and_oracle():
+@pytest.mark.parametrize("groups,graphs", [(8, "step"), (4, "engine"), (5, False)])
+def test_pipelined_host_step_matches_engine_and_oracle(groups, graphs):
     specs = list(catalogs.RESNET18.params)
-    pipe = HostPipelinedEngine(specs, 2, groups=4, seed=0)
+    pipe = HostPipelinedEngine(specs, 2, groups=groups, seed=0, graphs=graphs)
     ref = PowerSGDEngine(specs, 2, seed=0)
     ospecs = [O.ParamSpec(s.name, s.shape) for s in specs]
     comp, comm, workers = O.PowerSGD(2), O.Communicator(1), [O.WorkerState(0)]
