@@ -521,7 +521,7 @@ def e2e_pipelined(specs, a, dev, flush, barrier, stream):
     import statistics
     import torch
     from paper_1905_13727_b200.pipeline import HostPipelinedEngine
-    pipe = HostPipelinedEngine(specs, a.rank, groups=int(os.environ.get("PSGD_E2E_GROUPS", "8")), seed=0, device=dev)
+    pipe = HostPipelinedEngine(specs, a.rank, groups=int(os.environ.get("PSGD_E2E_GROUPS", "10")), seed=0, device=dev)
     for t in pipe.g_host + pipe.bias_host:
         t.normal_()
     for _ in range(3):

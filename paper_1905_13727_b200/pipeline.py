@@ -22,6 +22,8 @@ identical to one engine over the whole catalog (the reference's per-parameter lo
 is independent across parameters).
 """
 
+import os
+
 import torch
 
 from .engine import PowerSGDEngine
@@ -42,37 +44,38 @@ def split_groups(specs, groups):
     return [g for g in out if g]
 
 
-def transfer_groups(specs, groups, edge=0.02):
-    """Groups in transfer order for the pipelined step: a small first group (the
-    smallest parameters, ~`edge` of the bytes, so compression starts early), a small
-    last group (the next smallest, so the final D2H is short), and the remaining
-    parameters in catalog order cut into `groups - 2` groups of ~equal size.  Every
-    parameter appears exactly once; each group lists its parameters in catalog order."""
+def transfer_groups(specs, groups, edge=0.02, edge_groups=1):
+    """Groups in transfer order for the pipelined step: `edge_groups` small groups
+    first (the smallest parameters, ~`edge` of the bytes each, so compression and the
+    device->host stream start early), `edge_groups` small groups last (the next
+    smallest, so the final device->host copies are short), and the remaining
+    parameters in catalog order cut into `groups - 2 edge_groups` groups of ~equal
+    size.  Every parameter appears exactly once; each group lists its parameters in
+    catalog order."""
     n = len(specs)
-    if groups < 3 or n < 3:
+    ne = max(1, int(edge_groups))
+    if groups < 2 * ne + 1 or n < 2 * ne + 1:
         return split_groups(specs, max(1, groups))
     total = sum(s.size for s in specs) or 1
-    by_size = sorted(range(n), key=lambda i: (specs[i].size, i))
-    first, last, acc = [], [], 0
-    it = iter(by_size)
-    for i in it:
-        first.append(i)
-        acc += specs[i].size
-        if acc >= edge * total:
-            break
-    acc = 0
-    for i in it:
-        last.append(i)
-        acc += specs[i].size
-        if acc >= edge * total:
-            break
-    taken = set(first) | set(last)
+    order = iter(sorted(range(n), key=lambda i: (specs[i].size, i)))
+    edges = []
+    for _ in range(2 * ne):
+        cur, acc = [], 0
+        for i in order:
+            cur.append(i)
+            acc += specs[i].size
+            if acc >= edge * total:
+                break
+        if cur:
+            edges.append(sorted(cur))
+    taken = {i for g in edges for i in g}
     rest = [i for i in range(n) if i not in taken]
-    if not rest:
-        return [sorted(first), sorted(last)]
-    sub = split_groups([specs[i] for i in rest], max(1, groups - 2))
-    middle = [[rest[j] for j in g] for g in sub]
-    return [g for g in [sorted(first)] + middle + [sorted(last)] if g]
+    middle = []
+    if rest:
+        sub = split_groups([specs[i] for i in rest], max(1, groups - 2 * ne))
+        middle = [[rest[j] for j in g] for g in sub]
+    first, last = edges[0::2], edges[1::2][::-1]  # the smallest at the very start and the very end
+    return [g for g in first + middle + last if g]
 
 
 class HostPipelinedEngine:
@@ -80,10 +83,13 @@ class HostPipelinedEngine:
     graph; "engine" captures each group's compression only (cross-stream hand-offs
     eager); False runs everything eagerly."""
 
-    def __init__(self, specs, rank, *, groups=8, seed=0, device=None, graphs="step", order="transfer"):
+    def __init__(self, specs, rank, *, groups=10, seed=0, device=None, graphs="step", order="transfer",
+                 edge_groups=None):
         self.specs = list(specs)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.groups = (transfer_groups(self.specs, groups) if order == "transfer"
+        if edge_groups is None:
+            edge_groups = int(os.environ.get("PSGD_E2E_EDGE", "1"))
+        self.groups = (transfer_groups(self.specs, groups, edge_groups=edge_groups) if order == "transfer"
                        else split_groups(self.specs, groups))
         self.engines = [PowerSGDEngine([self.specs[i] for i in g], rank, seed=seed, device=self.device,
                                        param_indices=g) for g in self.groups]
