@@ -50,6 +50,7 @@ def parse_args():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-opt", action="store_true", help="skip the step + optimizer timing")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     if a.rank is None:
@@ -390,6 +391,11 @@ def run_ours(a):
         barrier()
         nccl_us = 1e3 * e0.elapsed_time(e1) / 100
 
+    # ---------------- the step + heavy-ball update (optimizer.py:131-134), separate vs fused
+    opt = None
+    if world == 1 and N * 4 < (2 << 30) and not a.no_opt:
+        opt = optimizer_timing(specs, a, dev, flush, barrier, stream)
+
     # ---------------- e2e: host gradients in, M-hat + bias mean out, every step
     if world == 1 and N * 4 < (2 << 30):  # the public host-pipelined API (pipeline.py)
         e2e_ms, h2d, d2h = e2e_pipelined(specs, a, dev, flush, barrier, stream)
@@ -460,6 +466,7 @@ def run_ours(a):
                               "frac": round(t_roof_us / (ms * 1e3), 4),
                               "frac_back_to_back": round(t_roof_us / (ms_b2b * 1e3), 4)},
             "kernels_ms": {k: round(v, 5) for k, v in kern_ms.items()},
+            "optimizer_step": opt,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/step", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -474,6 +481,50 @@ def run_ours(a):
         dist.destroy_process_group()
     return 0
 
+
+
+def optimizer_timing(specs, a, dev, flush, barrier, stream):
+    """Compression step + heavy-ball update per step (CUDA graph, L2 flushed), with the
+    update as the separate one-pass kernel vs fused into K3's M-hat epilogue."""
+    import statistics
+    import torch
+    from paper_1905_13727_b200 import PowerSGDEngine
+    out = {}
+    for name, fused, keep in (("separate_ms", False, True), ("fused_ms", True, True),
+                              ("fused_no_mhat_ms", True, False)):
+        eng = PowerSGDEngine(specs, a.rank, seed=0, device=dev)
+        gen = torch.Generator(device=dev).manual_seed(1000)
+        eng.g[0].normal_(generator=gen)
+        eng.bias_g[0].normal_(generator=gen)
+        eng.attach_optimizer(0.01, 0.9, fused=fused, keep_update=keep)
+        if fused:
+            out["fused_in_kernel"] = eng.fused_in_kernel
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                eng._enqueue(s)
+                eng.optimizer_step(s)
+        stream.wait_stream(s)
+        for _ in range(a.warmup):
+            flush.zero_() if flush is not None else None
+            g.replay()
+        barrier()
+        ts = []
+        for _ in range(a.steps):
+            if flush is not None:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            ts.append((e0, e1))
+        barrier()
+        eng.check()
+        out[name] = round(statistics.mean(x.elapsed_time(y) for x, y in ts), 5)
+        del g, eng
+    return out
 
 
 def e2e_serial(eng, a, world, dev, flush, barrier, stream, dist):

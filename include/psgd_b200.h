@@ -69,8 +69,24 @@ typedef struct {
     int32_t launches_q_ef;
     int32_t launches_decompress;
     int32_t launches_step_single; /* kernel launches issued by one psgd_step_single call */
-    int32_t pad;
+    int32_t opt_fusable;  /* 1: psgd_step_single_sgd (world 1) / psgd_decompress_sgd (world > 1) accept this plan */
 } psgd_plan_info;
+
+/* Heavy-ball optimizer state for the fused update of optimizer.py:131-134
+ * (m = momentum * m + u ; x -= lr * (u + m), u = M-hat / the bias mean): params
+ * and mom in the plan's flat layout (flat_elems), bias_params / bias_mom in the
+ * bias layout (nbias).  keep_update = 0: M-hat is consumed in registers and not
+ * written to `work` (the bias mean is still written to bias_out). */
+typedef struct {
+    float* params;
+    float* mom;
+    float* bias_params;
+    float* bias_mom;
+    float lr;
+    float momentum;
+    int32_t keep_update;
+    int32_t pad;
+} psgd_sgd;
 
 typedef struct {
     int64_t flat_off;     /* element offset of the n x m row-major matrix in g / e / work */
@@ -145,6 +161,23 @@ int psgd_decompress(const psgd_plan* plan, const float* p_hat, const float* q_su
 int psgd_step_single(const psgd_plan* plan, const float* g, float* e, float* work, float* q,
                      float* p, float* p_hat, const float* bias_g, const double* repl,
                      float* bias_out, int32_t* status, void* stream);
+
+/* One W == 1 step with the optimizer update (optimizer.py:131-134) fused into
+ * the M-hat epilogue: K3 applies m = momentum m + M-hat, x -= lr (M-hat + m) from
+ * the registers that hold M-hat (and the bias update from the bias mean), so M-hat
+ * never makes an HBM round trip.  Replaces psgd_step_single + psgd_momentum_step.
+ * PSGD_EINVAL unless psgd_plan_info.opt_fusable.  A failed step (status) leaves
+ * params and mom untouched. */
+int psgd_step_single_sgd(const psgd_plan* plan, const float* g, float* e, float* work, float* q,
+                         float* p, float* p_hat, const float* bias_g, const double* repl,
+                         float* bias_out, const psgd_sgd* opt, int32_t* status, void* stream);
+
+/* K5 with the optimizer update fused (world > 1): psgd_decompress, then
+ * optimizer.py:131-134 on M-hat in registers and on bias_mean (the bias mean
+ * psgd_q_ef wrote).  Replaces psgd_decompress + psgd_momentum_step. */
+int psgd_decompress_sgd(const psgd_plan* plan, const float* p_hat, const float* q_sum, int32_t divisor,
+                        float* q_store, float* mhat, const float* bias_mean, const psgd_sgd* opt,
+                        const int32_t* status, void* stream);
 
 /* Simulated-worker mean — replaces comm.py:84-98 (tree_reduce :51-67 then / W)
  * for the single-GPU W-list mode: out = tree_sum(bufs[0..nbuf)) / nbuf, in the

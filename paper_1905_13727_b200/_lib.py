@@ -28,7 +28,8 @@ REPL_ATTEMPTS = 3  # PSGD_REPL_ATTEMPTS: replacement draws per column held on th
 EXPORTS = (
     "psgd_plan_create", "psgd_plan_destroy", "psgd_plan_get_info", "psgd_plan_matrix",
     "psgd_ef_p", "psgd_orthogonalize", "psgd_orthogonalize_f64", "psgd_q_ef", "psgd_decompress", "psgd_step_single",
-    "psgd_tree_mean", "psgd_momentum_step", "psgd_last_error", "psgd_version",
+    "psgd_tree_mean", "psgd_momentum_step", "psgd_step_single_sgd", "psgd_decompress_sgd",
+    "psgd_last_error", "psgd_version",
 )
 
 
@@ -41,7 +42,16 @@ class PlanInfo(ctypes.Structure):
         ("n_tall", ctypes.c_int32), ("items_k1", ctypes.c_int64), ("items_k3", ctypes.c_int64),
         ("launches_ef_p", ctypes.c_int32), ("launches_orthogonalize", ctypes.c_int32),
         ("launches_q_ef", ctypes.c_int32), ("launches_decompress", ctypes.c_int32),
-        ("launches_step_single", ctypes.c_int32), ("pad", ctypes.c_int32),
+        ("launches_step_single", ctypes.c_int32), ("opt_fusable", ctypes.c_int32),
+    ]
+
+
+class Sgd(ctypes.Structure):
+    """psgd_sgd: heavy-ball state of the fused update (optimizer.py:131-134)."""
+    _fields_ = [
+        ("params", ctypes.c_void_p), ("mom", ctypes.c_void_p), ("bias_params", ctypes.c_void_p),
+        ("bias_mom", ctypes.c_void_p), ("lr", ctypes.c_float), ("momentum", ctypes.c_float),
+        ("keep_update", ctypes.c_int32), ("pad", ctypes.c_int32),
     ]
 
 
@@ -72,6 +82,8 @@ _SIGNATURES = {
     "psgd_step_single": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "psgd_tree_mean": (_I32, [ctypes.POINTER(_P), _I32, _I64, _P, _P]),
     "psgd_momentum_step": (_I32, [_P, _P, _P, _P, _P, _P, _P, ctypes.c_float, ctypes.c_float, _P, _P]),
+    "psgd_step_single_sgd": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_void_p, _P, _P]),
+    "psgd_decompress_sgd": (_I32, [_P, _P, _P, _I32, _P, _P, _P, ctypes.c_void_p, _P, _P]),
     "psgd_last_error": (ctypes.c_char_p, []),
     "psgd_version": (_I32, []),
 }

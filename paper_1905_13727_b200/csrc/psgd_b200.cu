@@ -88,6 +88,33 @@ struct MatDev {
                   // rcols: columns per attempt of the replacement table at repl_off (shared by equal n)
 };
 
+struct SgdArgs {   // fused heavy-ball update (optimizer.py:131-134); x == nullptr: off
+  float *x, *mom, *bx, *bm;
+  const float* bu;   // bias mean (the bias update u)
+  long long nbias;   // bias scalars this launch updates (0: none)
+  float lr, mu;
+  int keep;          // 1: M-hat is still stored
+};
+
+// m = mu m + u ; x -= lr (u + m)  (one rounding for mu m + u; the reference's numpy
+// does buf *= mu; buf += u in float64 — within the fp32 tolerance)
+__device__ __forceinline__ void sgd4(float4& x, float4& m, const float4& u, float lr, float mu) {
+  m.x = fmaf(mu, m.x, u.x); m.y = fmaf(mu, m.y, u.y); m.z = fmaf(mu, m.z, u.z); m.w = fmaf(mu, m.w, u.w);
+  x.x -= lr * (u.x + m.x); x.y -= lr * (u.y + m.y); x.z -= lr * (u.z + m.z); x.w -= lr * (u.w + m.w);
+}
+__device__ __forceinline__ void sgd1(float& x, float& m, float u, float lr, float mu) {
+  m = fmaf(mu, m, u);
+  x -= lr * (u + m);
+}
+__device__ __forceinline__ void sgd_bias(const SgdArgs& sg, long long t0, long long stride) {
+  for (long long i = t0; i < sg.nbias; i += stride) {
+    float x = sg.bx[i], m = sg.bm[i];
+    sgd1(x, m, sg.bu[i], sg.lr, sg.mu);
+    sg.bm[i] = m;
+    sg.bx[i] = x;
+  }
+}
+
 struct RowItem {   // K4 / K5 warp item: rows [row0, row0 + nrows) of `mat`, 2^lg lanes per row
   int mat, row0, nrows, lg;
 };
@@ -1315,7 +1342,8 @@ template <int R>
 __global__ void __launch_bounds__(K3P_CT + 32, 1)
     k3_pipe(const __grid_constant__ K3Maps maps, const MatDev* __restrict__ mats, const PipeItem* __restrict__ items,
             int nitems, K3PLayout L, float* __restrict__ work, const float* __restrict__ Phat,
-            float* __restrict__ qout, float* __restrict__ e, int write_mhat, int* __restrict__ ctr, int* status) {
+            float* __restrict__ qout, float* __restrict__ e, int write_mhat, int* __restrict__ ctr, int* status,
+            SgdArgs sg) {
   extern __shared__ __align__(1024) unsigned char k3p_smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(k3p_smem + L.off_bar);
   uint64_t* empty = full + L.stages;
@@ -1384,6 +1412,9 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
   const int bar_id = 1 + grp;
   pdl_wait();  // K2 complete: P-hat and the status word are final
   const bool skip = (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) != 0;  // mutate nothing
+  if (sg.x && !skip) sgd_bias(sg, (long long)blockIdx.x * K3P_CT + t, (long long)gridDim.x * K3P_CT);
+  const bool fuse = sg.x != nullptr;
+  const bool store_mhat = write_mhat && (!fuse || sg.keep);
   for (int k = grp;; k += K3P_GROUPS) {
     const int s = k % L.stages;
     mbar_wait(&full[s], (k / L.stages) & 1);
@@ -1463,6 +1494,46 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
       if (col < m) {
 #endif
         const bool vec = !hd.direct;  // tensor-mapped matrices have m % 4 == 0: whole float4 in range
+        if (fuse && vec) {
+          // fused optimizer (optimizer.py:131-134): x and m of 4 rows are loaded together,
+          // M-hat is consumed from the registers (a software-pipelined prefetch of the
+          // next 4 rows measured slower: it needs registers the 17-warp CTA does not have)
+          for (int i0 = rg; i0 < n; i0 += 4 * RG) {
+            float4 xv[4], mv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + u * RG;
+              if (i < n) {
+                const long long a = base + (long long)i * m + 4 * cq;
+                xv[u] = __ldcs(reinterpret_cast<const float4*>(sg.x + a));
+                mv[u] = __ldcs(reinterpret_cast<const float4*>(sg.mom + a));
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = i0 + u * RG;
+              if (i < n) {
+                const float4 d = *reinterpret_cast<const float4*>(slab + i * C + 4 * cq);
+                float mh[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int kk = 0; kk < R; ++kk) {
+                  if (kk < r) {
+                    const float p = ph[i * r + kk];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) mh[v] = fmaf(p, qv[v][kk], mh[v]);
+                  }
+                }
+                const long long a = base + (long long)i * m + 4 * cq;
+                const float4 u4 = make_float4(mh[0], mh[1], mh[2], mh[3]);
+                st_stream(reinterpret_cast<float4*>(e + a), make_float4(d.x - mh[0], d.y - mh[1], d.z - mh[2], d.w - mh[3]));
+                if (store_mhat) st_stream(reinterpret_cast<float4*>(work + a), u4);
+                sgd4(xv[u], mv[u], u4, sg.lr, sg.mu);
+                st_stream(reinterpret_cast<float4*>(sg.mom + a), mv[u]);
+                st_stream(reinterpret_cast<float4*>(sg.x + a), xv[u]);
+              }
+            }
+          }
+        } else {
 #pragma unroll 4
         for (int i = rg; i < n; i += RG) {
           const float4 d = *reinterpret_cast<const float4*>(slab + i * C + 4 * cq);
@@ -1478,16 +1549,23 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
           const long long a = base + (long long)i * m + 4 * cq;
           if (vec) {
             st_stream(reinterpret_cast<float4*>(e + a), make_float4(d.x - mh[0], d.y - mh[1], d.z - mh[2], d.w - mh[3]));
-            if (write_mhat) st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
+            if (store_mhat) st_stream(reinterpret_cast<float4*>(work + a), make_float4(mh[0], mh[1], mh[2], mh[3]));
           } else {
             const float dv[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
             for (int v = 0; v < 4; ++v)
               if (col + v < m) {
                 st_stream(e + a + v, dv[v] - mh[v]);
-                if (write_mhat) st_stream(work + a + v, mh[v]);
+                if (store_mhat) st_stream(work + a + v, mh[v]);
+                if (fuse) {
+                  float xx = sg.x[a + v], mm = sg.mom[a + v];
+                  sgd1(xx, mm, mh[v], sg.lr, sg.mu);
+                  sg.mom[a + v] = mm;
+                  sg.x[a + v] = xx;
+                }
               }
           }
+        }
         }
       }
     }
@@ -1516,8 +1594,11 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
                                                      const float* __restrict__ Phat,
                                                      const float* __restrict__ qsrc, int divisor,
                                                      float* __restrict__ qstore, int write_mhat,
-                                                     const int* __restrict__ status) {
+                                                     const int* __restrict__ status, SgdArgs sg) {
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
+  const bool fuse = MODE == 1 && sg.x != nullptr;  // K5 with the optimizer update (optimizer.py:131-134)
+  if (fuse) sgd_bias(sg, (long long)blockIdx.x * kThreads + threadIdx.x, (long long)gridDim.x * kThreads);
+  const bool store = MODE == 0 || !fuse || sg.keep;
   const int lane = threadIdx.x & 31;
   const int wi = beg + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   if (wi >= end) return;
@@ -1565,7 +1646,13 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
         st_stream(e + o + j, d - mh);
         if (write_mhat) st_stream(work + o + j, mh);
       } else {
-        st_stream(work + o + j, mh);
+        if (store) st_stream(work + o + j, mh);
+        if (fuse) {
+          float xx = sg.x[o + j], mm = sg.mom[o + j];
+          sgd1(xx, mm, mh, sg.lr, sg.mu);
+          sg.mom[o + j] = mm;
+          sg.x[o + j] = xx;
+        }
       }
     }
     const float* __restrict__ qrow = Q + head;
@@ -1579,6 +1666,17 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
 #pragma unroll
         for (int v = 0; v < 4; ++v)
           d[v] = c0 + v * G < body4 ? __ldcs(w4 + c0 + v * G) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float4 xs[4], ms[4];
+      if (fuse) {
+        const float4* x4 = reinterpret_cast<const float4*>(sg.x + o + head);
+        const float4* m4 = reinterpret_cast<const float4*>(sg.mom + o + head);
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (c0 + v * G < body4) {
+            xs[v] = __ldcs(x4 + c0 + v * G);
+            ms[v] = __ldcs(m4 + c0 + v * G);
+          }
       }
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
@@ -1600,7 +1698,13 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
           st_stream(e4 + c, make_float4(d[v].x - mh[0], d[v].y - mh[1], d[v].z - mh[2], d[v].w - mh[3]));
           if (write_mhat) st_stream(w4 + c, make_float4(mh[0], mh[1], mh[2], mh[3]));
         } else {
-          st_stream(w4 + c, make_float4(mh[0], mh[1], mh[2], mh[3]));
+          const float4 u4 = make_float4(mh[0], mh[1], mh[2], mh[3]);
+          if (store) st_stream(w4 + c, u4);
+          if (fuse) {
+            sgd4(xs[v], ms[v], u4, sg.lr, sg.mu);
+            st_stream(reinterpret_cast<float4*>(sg.mom + o + head) + c, ms[v]);
+            st_stream(reinterpret_cast<float4*>(sg.x + o + head) + c, xs[v]);
+          }
         }
       }
     }
@@ -2246,9 +2350,13 @@ K3Cfg k3_tall_config(int n, int m, int r) {
 
 }  // namespace
 
+namespace {
+bool opt_fusable(const psgd_plan* pl);
+}
+
 extern "C" {
 
-int32_t psgd_version(void) { return 2; }
+int32_t psgd_version(void) { return 3; }
 
 const char* psgd_last_error(void) { return g_last_error.c_str(); }
 
@@ -2739,6 +2847,7 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
   o->launches_step_single = o->launches_ef_p + o->launches_q_ef;
+  o->opt_fusable = opt_fusable(pl) ? 1 : 0;
   return PSGD_OK;
 }
 
@@ -2847,13 +2956,13 @@ struct RunK45Mode {
   struct F {
     static int run(const psgd_plan* pl, const RowItem* items, const Group& gp, float* work, float* e,
                    const float* phat, const float* qsrc, int divisor, float* qstore, int write_mhat,
-                   const int* status, cudaStream_t st) {
+                   const int* status, cudaStream_t st, SgdArgs sg = SgdArgs{}) {
       const int nitems = gp.end - gp.beg;
       if (nitems <= 0) return PSGD_OK;
       const int blocks = (nitems + 7) / 8;
       k45_rows<R, EXACT, MODE><<<blocks, kThreads, 0, st>>>(pl->d_mats, items, gp.beg, gp.end, work,
                                                             e, phat, qsrc, divisor, qstore,
-                                                            write_mhat, status);
+                                                            write_mhat, status, sg);
       PSGD_CUDA_CHECK(cudaGetLastError());
       return PSGD_OK;
     }
@@ -2920,7 +3029,7 @@ int encode_pipe_maps(const psgd_plan* pl, const float* work) {
 
 template <int R>
 int launch_pipe_r(const psgd_plan* pl, float* work, const float* phat, float* qout, float* e, int* status,
-                  cudaStream_t st) {
+                  cudaStream_t st, const SgdArgs& sg) {
   auto kern = k3_pipe<R>;
   PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->k3pl.total));
   const int grid = (int)std::min<size_t>(pl->nsm, pl->pipe_items.size());
@@ -2935,18 +3044,18 @@ int launch_pipe_r(const psgd_plan* pl, float* work, const float* phat, float* qo
   }
   PSGD_CUDA_CHECK(launch_ex(kern, grid, K3P_CT + 32, (size_t)pl->k3pl.total, st, PSGD_PDL != 0, maps,
                             (const MatDev*)pl->d_mats, (const PipeItem*)pl->d_pipe_items, (int)pl->pipe_items.size(),
-                            pl->k3pl, work, phat, qout, e, pl->world == 1 ? 1 : 0, pl->d_pipe_ctr, status));
+                            pl->k3pl, work, phat, qout, e, pl->world == 1 ? 1 : 0, pl->d_pipe_ctr, status, sg));
   return PSGD_OK;
 }
 
 int launch_pipe(const psgd_plan* pl, float* work, const float* phat, float* qout, float* e, int* status,
-                cudaStream_t st) {
+                cudaStream_t st, const SgdArgs& sg) {
   if (pl->pipe_items.empty()) return PSGD_OK;
   switch (pl->pipe_rmax) {
-    case 1: return launch_pipe_r<1>(pl, work, phat, qout, e, status, st);
-    case 2: return launch_pipe_r<2>(pl, work, phat, qout, e, status, st);
-    case 4: return launch_pipe_r<4>(pl, work, phat, qout, e, status, st);
-    default: return launch_pipe_r<8>(pl, work, phat, qout, e, status, st);
+    case 1: return launch_pipe_r<1>(pl, work, phat, qout, e, status, st, sg);
+    case 2: return launch_pipe_r<2>(pl, work, phat, qout, e, status, st, sg);
+    case 4: return launch_pipe_r<4>(pl, work, phat, qout, e, status, st, sg);
+    default: return launch_pipe_r<8>(pl, work, phat, qout, e, status, st, sg);
   }
 }
 
@@ -3029,12 +3138,14 @@ int psgd_orthogonalize_f64(const psgd_plan* pl, int32_t i, const double* p, cons
   return PSGD_OK;
 }
 
-int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor, const double* repl,
-              float* p_hat, float* q_out, float* e, float* bias_out, int32_t* status, void* stream) {
-  if (!pl || !status || divisor < 1 ||
-      (pl->nmat > 0 && (!work || !p || !repl || !p_hat || !q_out || !e)) || (pl->nbias > 0 && !bias_out))
-    return fail(PSGD_EINVAL, "psgd_q_ef: bad argument");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+}  // extern "C"
+
+namespace {
+
+// K2 + K3 (+ K4); sg: the fused optimizer update (W = 1 plans that are opt_fusable)
+int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor, const double* repl,
+              float* p_hat, float* q_out, float* e, float* bias_out, int32_t* status, cudaStream_t st,
+              const SgdArgs& sg) {
   int rc = PSGD_OK;
   // K2: P-hat = MGS(P / W) of every matrix (compressors.py:337-338) + the bias mean.
   // When every matrix is orthogonalised in Gram space (k2_gram checks the
@@ -3047,7 +3158,7 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
     if (rc) return rc;
   }
   bool bias_done = !bias_in_k3;
-  rc = launch_pipe(pl, work, p_hat, q_out, e, (int*)status, st);  // K3 pipeline (n <= 512)
+  rc = launch_pipe(pl, work, p_hat, q_out, e, (int*)status, st, sg);  // K3 pipeline (n <= 512)
   if (rc) return rc;
   for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab (after K2: delta is final)
     rc = dispatch_r<RunK3>(gp.r, pl, gp, work, p, (int)divisor, repl, p_hat, q_out, e, bias_out,
@@ -3091,17 +3202,63 @@ int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
   return PSGD_OK;
 }
 
+int decompress_impl(const psgd_plan* pl, const float* p_hat, const float* q_sum, int32_t divisor,
+                    float* q_store, float* mhat, const int32_t* status, cudaStream_t st, SgdArgs sg) {
+  for (const Group& gp : pl->g5) {
+    int rc = dispatch_r<RunK5>(gp.r, pl, (const RowItem*)pl->d_k5, gp, mhat, (float*)nullptr, p_hat,
+                               q_sum, divisor, q_store, 1, (const int*)status, st, sg);
+    if (rc) return rc;
+    sg.nbias = 0;  // the first launch updates the bias parameters
+  }
+  return PSGD_OK;
+}
+
+bool opt_fusable(const psgd_plan* pl) {
+  if (pl->nmat == 0) return false;
+  if (pl->world > 1) return true;  // K5 writes every M-hat
+  for (const MatDev& md : pl->mats)
+    if (!md.pipe) return false;      // W = 1: k3_pipe writes every M-hat
+  return true;
+}
+
+bool make_sgd(const psgd_plan* pl, const psgd_sgd* o, const float* bias_mean, SgdArgs* sg) {
+  if (!o || !o->params || !o->mom || (pl->nbias > 0 && (!o->bias_params || !o->bias_mom || !bias_mean)))
+    return false;
+  *sg = SgdArgs{o->params, o->mom, o->bias_params, o->bias_mom, bias_mean, pl->nbias, o->lr, o->momentum,
+                o->keep_update ? 1 : 0};
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int psgd_q_ef(const psgd_plan* pl, float* work, const float* p, int32_t divisor, const double* repl,
+              float* p_hat, float* q_out, float* e, float* bias_out, int32_t* status, void* stream) {
+  if (!pl || !status || divisor < 1 ||
+      (pl->nmat > 0 && (!work || !p || !repl || !p_hat || !q_out || !e)) || (pl->nbias > 0 && !bias_out))
+    return fail(PSGD_EINVAL, "psgd_q_ef: bad argument");
+  return q_ef_impl(pl, work, p, divisor, repl, p_hat, q_out, e, bias_out, status, static_cast<cudaStream_t>(stream),
+                   SgdArgs{});
+}
+
 int psgd_decompress(const psgd_plan* pl, const float* p_hat, const float* q_sum, int32_t divisor,
                     float* q_store, float* mhat, const int32_t* status, void* stream) {
   if (!pl || !status || divisor < 1 || (pl->nmat > 0 && (!p_hat || !q_sum || !mhat)))
     return fail(PSGD_EINVAL, "psgd_decompress: bad argument");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  for (const Group& gp : pl->g5) {
-    int rc = dispatch_r<RunK5>(gp.r, pl, (const RowItem*)pl->d_k5, gp, mhat, (float*)nullptr, p_hat,
-                               q_sum, divisor, q_store, 1, (const int*)status, st);
-    if (rc) return rc;
-  }
-  return PSGD_OK;
+  return decompress_impl(pl, p_hat, q_sum, divisor, q_store, mhat, status, static_cast<cudaStream_t>(stream),
+                         SgdArgs{});
+}
+
+int psgd_decompress_sgd(const psgd_plan* pl, const float* p_hat, const float* q_sum, int32_t divisor,
+                        float* q_store, float* mhat, const float* bias_mean, const psgd_sgd* opt,
+                        const int32_t* status, void* stream) {
+  if (!pl || !status || divisor < 1 || (pl->nmat > 0 && (!p_hat || !q_sum || !mhat)))
+    return fail(PSGD_EINVAL, "psgd_decompress_sgd: bad argument");
+  if (pl->world < 2 || !opt_fusable(pl)) return fail(PSGD_EINVAL, "psgd_decompress_sgd: plan is not opt_fusable");
+  SgdArgs sg;
+  if (!make_sgd(pl, opt, bias_mean, &sg)) return fail(PSGD_EINVAL, "psgd_decompress_sgd: NULL optimizer buffer");
+  return decompress_impl(pl, p_hat, q_sum, divisor, q_store, mhat, status, static_cast<cudaStream_t>(stream), sg);
 }
 
 int psgd_step_single(const psgd_plan* pl, const float* g, float* e, float* work, float* q, float* p,
@@ -3112,6 +3269,21 @@ int psgd_step_single(const psgd_plan* pl, const float* g, float* e, float* work,
   if (!status) return fail(PSGD_EINVAL, "NULL status");
   int rc = psgd_ef_p(pl, g, e, work, q, p, bias_g, status, stream);
   if (!rc) rc = psgd_q_ef(pl, work, p, 1, repl, p_hat, q, e, bias_out, status, stream);
+  return rc;
+}
+
+int psgd_step_single_sgd(const psgd_plan* pl, const float* g, float* e, float* work, float* q, float* p,
+                         float* p_hat, const float* bias_g, const double* repl, float* bias_out,
+                         const psgd_sgd* opt, int32_t* status, void* stream) {
+  if (!pl) return fail(PSGD_EINVAL, "NULL plan");
+  if (pl->world != 1 || !opt_fusable(pl)) return fail(PSGD_EINVAL, "psgd_step_single_sgd: plan is not opt_fusable");
+  if (!status || !repl || !p_hat || !e || (pl->nbias > 0 && !bias_out))
+    return fail(PSGD_EINVAL, "psgd_step_single_sgd: NULL argument");
+  SgdArgs sg;
+  if (!make_sgd(pl, opt, bias_out, &sg)) return fail(PSGD_EINVAL, "psgd_step_single_sgd: NULL optimizer buffer");
+  int rc = psgd_ef_p(pl, g, e, work, q, p, bias_g, status, stream);
+  if (!rc)
+    rc = q_ef_impl(pl, work, p, 1, repl, p_hat, q, e, bias_out, status, static_cast<cudaStream_t>(stream), sg);
   return rc;
 }
 

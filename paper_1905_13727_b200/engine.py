@@ -27,6 +27,8 @@ param_index), compressors.py:362-367) and CommStats are charged exactly as the
 reference charges them (compressors.py:248-249, 374; comm.py:96).
 """
 
+import ctypes
+
 import torch
 
 from . import _lib
@@ -122,6 +124,7 @@ class PowerSGDEngine:
             pl.q_view(self.Q, k).copy_(torch.from_numpy(q0))
         self.step_count = 0
         self._graph = None
+        self.fused = self._fused_ok = False
         # host-side accounting per step (integers), charged as the reference does
         self._charge = step_charges([(mi.n, mi.m, mi.r_eff) for mi in pl.matrices], self.nbias, self.world)
 
@@ -166,10 +169,18 @@ class PowerSGDEngine:
         h = pl.handle
         e = self.e if self.error_feedback else [self._e_scratch] * self.nlocal
         ein = self.e if self.error_feedback else [None] * self.nlocal
+        sgd = self._sgd_struct() if self._fused_ok else None
         if not self.exchange and self.error_feedback:
+            if sgd is not None:  # K3 applies the heavy-ball update from the M-hat registers
+                _lib.check(lib.psgd_step_single_sgd(
+                    h, ptr(self.g[0]), ptr(e[0]), ptr(self.work[0]), ptr(self.Q), ptr(self.P[0]), ptr(self.Phat),
+                    ptr(self.bias_g[0]), ptr(self.repl), ptr(self.bias_out), ctypes.byref(sgd), ptr(self.status),
+                    sp), "psgd_step_single_sgd")
+                return
             _lib.check(lib.psgd_step_single(h, ptr(self.g[0]), ptr(e[0]), ptr(self.work[0]), ptr(self.Q),
                                             ptr(self.P[0]), ptr(self.Phat), ptr(self.bias_g[0]), ptr(self.repl),
                                             ptr(self.bias_out), ptr(self.status), sp), "psgd_step_single")
+            self._unfused_update(sp)
             return
         for w in range(self.nlocal):      # K1: delta = g + e, P = delta Q  (e NULL: EF off)
             _lib.check(lib.psgd_ef_p(h, ptr(self.g[w]), ptr(ein[w]), ptr(self.work[w]), ptr(self.Q),
@@ -187,26 +198,44 @@ class PowerSGDEngine:
             _lib.check(lib.psgd_q_ef(h, ptr(self.work[w]), ptr(self.Pm), div, ptr(self.repl), ptr(self.Phat),
                                      ptr(q_w), ptr(e[w]), ptr(self.bias_out), ptr(self.status), sp), "psgd_q_ef")
         if not self.exchange:
+            self._unfused_update(sp)
             return
         if self.distributed:              # AR2 (q), then Q-bar = q / W and M-hat
             self.comm.all_reduce_sum_(self.qbuf[0], force=True)
-            _lib.check(lib.psgd_decompress(h, ptr(self.Phat), ptr(self.qbuf[0]), self.world, ptr(self.Q),
-                                           ptr(self.work[0]), ptr(self.status), sp), "psgd_decompress")
+            qs, div, qstore = self.qbuf[0], self.world, self.Q
         else:
             tree_mean_(self.qbuf, self.Q, stream)
-            _lib.check(lib.psgd_decompress(h, ptr(self.Phat), ptr(self.Q), 1, None, ptr(self.work[0]),
-                                           ptr(self.status), sp), "psgd_decompress")
+            qs, div, qstore = self.Q, 1, None
+        if sgd is not None:               # K5 applies the heavy-ball update from the M-hat registers
+            _lib.check(lib.psgd_decompress_sgd(h, ptr(self.Phat), ptr(qs), div, ptr(qstore), ptr(self.work[0]),
+                                               ptr(self.bias_out), ctypes.byref(sgd), ptr(self.status), sp),
+                       "psgd_decompress_sgd")
+            return
+        _lib.check(lib.psgd_decompress(h, ptr(self.Phat), ptr(qs), div, ptr(qstore), ptr(self.work[0]),
+                                       ptr(self.status), sp), "psgd_decompress")
+        self._unfused_update(sp)
 
     def _scratch_e(self):
         return self._e_scratch
 
     # ------------------------------------------------------------------ optimizer (optimizer.py:131-134)
-    def attach_optimizer(self, lr, momentum, params=None):
+    def attach_optimizer(self, lr, momentum, params=None, fused=False, keep_update=True):
         """Heavy-ball state on the device, in the plan's packed layout: parameters
         x and momentum buffers m (Optimizer.params / momentum_buffers,
-        optimizer.py:47-55).  `params`: initial values in catalog order."""
+        optimizer.py:47-55).  `params`: initial values in catalog order.
+
+        fused=True: every later step applies the update itself, like the
+        reference's optimizer.step (optimizer.py:98-135) — inside the kernel that
+        produces M-hat (K3 at W = 1, K5 at W > 1), consuming M-hat from registers,
+        when the plan allows it (`fused_in_kernel`), else with the one-pass update
+        kernel appended to the step; `optimizer_step()` is then a no-op.
+        keep_update=False (fused only): M-hat is not stored (update_view is stale)."""
         z = dict(dtype=torch.float32, device=self.device)
         self.lr, self.momentum = float(lr), float(momentum)
+        self.fused = bool(fused)
+        self.keep_update = bool(keep_update) or not self.fused
+        self._fused_ok = self.fused and bool(self.plan.info.opt_fusable) and (self.exchange or self.error_feedback)
+        self._graph = None  # a captured step no longer matches
         self.params = torch.zeros(self.plan.flat_elems, **z)
         self.mom = torch.zeros(self.plan.flat_elems, **z)
         self.bias_params = torch.zeros(max(1, self.nbias), **z)
@@ -228,13 +257,32 @@ class PowerSGDEngine:
     def momentum_view(self, param_index):
         return self._flat_view(self.mom, self.bias_mom, param_index)
 
+    @property
+    def fused_in_kernel(self):
+        """The attached optimizer runs inside K3 / K5 (not as a separate pass)."""
+        return self._fused_ok
+
+    def _sgd_struct(self):
+        return _lib.Sgd(self.params.data_ptr(), self.mom.data_ptr(), self.bias_params.data_ptr(),
+                        self.bias_mom.data_ptr(), self.lr, self.momentum, 1 if self.keep_update else 0, 0)
+
+    def _unfused_update(self, sp):
+        if self.fused and not self._fused_ok:
+            self._momentum_launch(sp)
+
     def optimizer_step(self, stream=None):
         """m = momentum m + u ; x -= lr (u + m) for every parameter, one kernel,
-        with u = the aggregated update of the last step (M-hat, bias mean)."""
+        with u = the aggregated update of the last step (M-hat, bias mean).
+        A no-op when the optimizer is fused into the step (attach_optimizer(fused=True))."""
+        if self.fused:
+            return
+        self._momentum_launch(stream_ptr(stream))
+
+    def _momentum_launch(self, sp):
         _lib.check(_lib.lib().psgd_momentum_step(
             self.plan.handle, ptr(self.params), ptr(self.mom), ptr(self.work[0]), ptr(self.bias_params),
             ptr(self.bias_mom), ptr(self.bias_out), self.lr, self.momentum, ptr(self.status),
-            stream_ptr(stream)), "psgd_momentum_step")
+            sp), "psgd_momentum_step")
 
     def run(self, stream=None):
         """Enqueue one step on `stream` (default: current) without synchronising."""

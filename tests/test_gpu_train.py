@@ -21,13 +21,16 @@ from test_oracle import GOLDEN_TRAIN
 pytestmark = pytest.mark.gpu
 
 
-def test_golden_train_csv_replayed_on_gpu():
+@pytest.mark.parametrize("fused", [False, True])
+def test_golden_train_csv_replayed_on_gpu(fused):
+    """fused=True: the heavy-ball update runs inside K5 (psgd_decompress_sgd)."""
     seed, world, rank, lr, mom = 1, 2, 2, 0.01, 0.9
     prob = O.LeastSquares(seed)
     specs = [ParamSpec(s.name, s.shape) for s in prob.specs]
     comm = Communicator(world)
     eng = PowerSGDEngine(specs, rank, workers=world, comm=comm, seed=seed)
-    eng.attach_optimizer(lr, mom, params=prob.init_params())
+    eng.attach_optimizer(lr, mom, params=prob.init_params(), fused=fused)
+    assert eng.fused_in_kernel == fused
     rows = [(0, prob.loss(prob.init_params()), 0, 0)]
     for t in range(3):
         params = [eng.param_view(i).double().cpu().numpy() for i in range(len(specs))]
@@ -43,12 +46,16 @@ def test_golden_train_csv_replayed_on_gpu():
         assert abs(got[1] - want[1]) <= 1e-5 * abs(want[1]), (got, want)
 
 
-def test_momentum_kernel_matches_reference_update():
+@pytest.mark.parametrize("fused", [False, True])
+def test_momentum_kernel_matches_reference_update(fused):
+    """fused=True: the update runs in K3's epilogue (psgd_step_single_sgd), including
+    the scalar (m % 4 != 0) slab path of (10, 27)."""
     specs = [ParamSpec("w", (64, 576)), ParamSpec("b", (64,)), ParamSpec("v", (10, 27))]
     eng = PowerSGDEngine(specs, 2)
     rng = np.random.default_rng(0)
     x0 = [rng.standard_normal(s.shape) for s in specs]
-    eng.attach_optimizer(0.05, 0.9, params=x0)
+    eng.attach_optimizer(0.05, 0.9, params=x0, fused=fused)
+    assert eng.fused_in_kernel == fused
     xs = [a.copy() for a in x0]
     bufs = [np.zeros(s.shape) for s in specs]
     for _ in range(3):
