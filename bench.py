@@ -396,6 +396,11 @@ def run_ours(a):
     if world == 1 and N * 4 < (2 << 30) and not a.no_opt:
         opt = optimizer_timing(specs, a, dev, flush, barrier, stream)
 
+    # ---------------- the per-parameter drop-in (the reference's optimizer loop calling round_trip)
+    dropin = None
+    if world == 1 and a.workload == "resnet18" and not a.no_opt:
+        dropin = dropin_timing(specs, a, dev)
+
     # ---------------- e2e: host gradients in, M-hat + bias mean out, every step
     if world == 1 and N * 4 < (2 << 30):  # the public host-pipelined API (pipeline.py)
         e2e_ms, h2d, d2h = e2e_pipelined(specs, a, dev, flush, barrier, stream)
@@ -467,6 +472,7 @@ def run_ours(a):
                               "frac_back_to_back": round(t_roof_us / (ms_b2b * 1e3), 4)},
             "kernels_ms": {k: round(v, 5) for k, v in kern_ms.items()},
             "optimizer_step": opt,
+            "dropin": dropin,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/step", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -481,6 +487,59 @@ def run_ours(a):
         dist.destroy_process_group()
     return 0
 
+
+
+def dropin_timing(specs, a, dev, steps=3):
+    """One optimizer step (optimizer.py:110-134: EF add, round_trip per matrix
+    parameter, EF update, bias mean, heavy-ball update) through the drop-in
+    `PowerSGD.round_trip`, once with numpy arrays on the host (the reference's own
+    calling convention: one H2D/D2H round trip and one sync per parameter) and
+    once with CUDA tensors (no per-parameter sync; errors at `check()`)."""
+    import numpy as np
+    import torch
+    from paper_1905_13727_b200 import Communicator, CompressionContext, PowerSGD
+    out = {}
+    rng = np.random.default_rng(0)
+    grads = [rng.standard_normal(s.shape).astype(np.float32) for s in specs]
+    for mode in ("numpy", "torch"):
+        comp, comm = PowerSGD(a.rank), Communicator(1)
+        if mode == "numpy":
+            xs = [np.zeros(s.shape) for s in specs]
+            bufs = [np.zeros(s.shape) for s in specs]
+            errs = {}
+            g = grads
+        else:
+            xs = [torch.zeros(s.shape, device=dev) for s in specs]
+            bufs = [torch.zeros(s.shape, device=dev) for s in specs]
+            errs = {}
+            g = [torch.from_numpy(x).to(dev) for x in grads]
+        ts = []
+        for t in range(steps + 1):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            for i, sp in enumerate(specs):
+                if sp.is_bias:
+                    upd = g[i] if mode == "torch" else g[i].astype(np.float64)
+                else:
+                    n, m = sp.matrix_shape
+                    e = errs.get(i)
+                    gi = g[i].reshape(n, m)
+                    delta = (gi + e) if e is not None else (gi.clone() if mode == "torch" else gi.astype(np.float64))
+                    trip = comp.round_trip([delta], CompressionContext(0, i, t), comm)
+                    errs[i] = delta - trip.locals[0]
+                    upd = trip.aggregated.reshape(sp.shape)
+                bufs[i] *= 0.9
+                bufs[i] += upd
+                xs[i] -= 0.01 * (upd + bufs[i])
+            if mode == "torch":
+                comp.check()
+            torch.cuda.synchronize(dev)
+            if t > 0:
+                ts.append(time.perf_counter() - t0)
+        out[mode + "_ms"] = round(1e3 * statistics.median(ts), 3)
+    out["note"] = ("optimizer.py:110-134 loop over the catalog calling PowerSGD.round_trip per matrix "
+                   "(numpy: float64 host arrays as the reference; torch: CUDA tensors); wall clock")
+    return out
 
 
 def optimizer_timing(specs, a, dev, flush, barrier, stream):

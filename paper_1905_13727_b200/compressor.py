@@ -80,6 +80,14 @@ def _out(t, as_numpy):
 _PLANS = {}
 
 
+def _raise_status(st):
+    """The reference's errors for a device status word (linalg.py:35-36, :82-88)."""
+    if st & (_lib.STATUS_NONFINITE_GRAD | _lib.STATUS_NONFINITE_P):
+        raise ContractViolation("orthogonalize input contains non-finite entries")
+    if st & _lib.STATUS_REPLACEMENT:
+        raise RuntimeError(f"Gram-Schmidt needed more than {_lib.REPL_ATTEMPTS} replacement draws for a column")
+
+
 def _plan(n, m, rank, world, device):
     key = (n, m, rank, world, str(device))
     pl = _PLANS.get(key)
@@ -168,10 +176,52 @@ class Compressor:
         comm.stats.compress_flops += workers * self.compress_cost(n, m)
 
 
+class _RoundTripWork:
+    """Device and pinned-host buffers of one round-trip shape (n, m, W, world,
+    device), allocated once and reused by every later call with that shape: a
+    per-parameter drop-in call makes no allocations, one H2D copy per worker
+    matrix, one D2H copy per output and (numpy mode) one stream synchronisation."""
+
+    def __init__(self, n, m, rank, W, world, dev, host):
+        self.pl = pl = _plan(n, m, rank, world, dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.r = min(n, m, rank)
+        self.g = [torch.zeros(pl.flat_elems, **f32) for _ in range(W)]
+        self.works = [torch.zeros(pl.flat_elems, **f32) for _ in range(W)]
+        self.ps = [torch.zeros(pl.p_elems, **f32) for _ in range(W)]
+        self.pm = torch.zeros(pl.p_elems, **f32)
+        self.phat = torch.zeros(pl.p_elems, **f32)
+        self.q_in = torch.zeros(pl.q_elems, **f32)
+        self.qws = [torch.zeros(pl.q_elems, **f32) for _ in range(W)]
+        self.qbar = torch.zeros(pl.q_elems, **f32)
+        self.qstore = torch.zeros(pl.q_elems, **f32)
+        self.escratch = torch.empty(pl.flat_elems, **f32)
+        self.agg = torch.zeros(pl.flat_elems, **f32)
+        self.locs = [torch.zeros(pl.flat_elems, **f32) for _ in range(W)] if world > 1 else []
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.repl = pl.repl_table()
+        if host:  # pinned staging for numpy inputs / outputs
+            pin = dict(dtype=torch.float32, pin_memory=True)
+            self.h_in = [torch.empty((n, m), **pin) for _ in range(W)]
+            self.h_agg = torch.empty((n, m), **pin)
+            self.h_locs = [torch.empty((n, m), **pin) for _ in range(W)] if world > 1 else []
+            self.h_p = torch.empty((n, self.r), **pin)
+            self.h_q = torch.empty((m, self.r), **pin)
+            self.h_st = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+
+
 class PowerSGD(Compressor):
     """Rank-r compression by one warm-started power-iteration step
-    (compressors.py:344-397).  `q_memory[param_index]` holds the fp32 Q-bar of
-    the last step on the device (the reference stores it unnormalised, :373)."""
+    (compressors.py:344-397).  `q_memory[param_index]` holds Q-bar of the last
+    step, unnormalised (:373): a float64 numpy array when the round trip was
+    called with numpy matrices (as the reference), an fp32 CUDA tensor when it
+    was called with CUDA tensors.  A device mirror of each stored Q-bar avoids
+    re-uploading it on the next step.
+
+    CUDA-tensor calls never synchronise: a non-finite input or an exhausted
+    replacement table is recorded on the device and raised by `check()` (the
+    grouped optimizer loop calls it once per step); numpy calls raise
+    immediately, like the reference."""
 
     name = "powersgd"
     linear = True
@@ -182,6 +232,9 @@ class PowerSGD(Compressor):
         super().__init__(rank)
         self.q_memory = {}
         self.device = device
+        self._work = {}
+        self._q_dev = {}     # param_index -> (the q_memory object it mirrors, device fp32 m x r)
+        self._sticky = {}    # device -> int32 status accumulated by tensor-mode calls
 
     def effective_rank(self, n, m):
         return min(n, m, self.rank)
@@ -191,7 +244,24 @@ class PowerSGD(Compressor):
         q = self.q_memory.get(ctx.param_index)
         if q is None or tuple(q.shape) != (m, r):
             q = ctx.param_rng("warm_start_init").standard_normal((m, r))
+        mirror = self._q_dev.get(ctx.param_index)
+        if mirror is not None and mirror[0] is q and mirror[1].device == device:
+            return mirror[1]
         return _to_dev(q, device)
+
+    def _ws(self, n, m, W, world, dev, host):
+        key = (n, m, W, world, str(dev), host)
+        w = self._work.get(key)
+        if w is None:
+            w = self._work[key] = _RoundTripWork(n, m, self.rank, W, world, dev, host)
+        return w
+
+    def check(self):
+        """Raise what the reference would for the tensor-mode calls since the last check."""
+        for dev, st in list(self._sticky.items()):
+            v = int(st.item())
+            st.zero_()
+            _raise_status(v)
 
     def round_trip(self, mats, ctx, comm):
         """compressors.py:369-379 on the GPU."""
@@ -205,88 +275,96 @@ class PowerSGD(Compressor):
             raise ValueError("a distributed worker passes its own matrix only")
         dev = (torch.device(self.device) if self.device is not None else
                (mats[0].device if not as_np else torch.device("cuda", torch.cuda.current_device())))
-        ds = [_to_dev(x, dev) for x in mats]
-        if ds[0].dim() != 2 or min(ds[0].shape) < 1:
-            raise ContractViolation(f"matrix must be 2-d and non-empty, got {tuple(ds[0].shape)}")
-        n, m = ds[0].shape
-        W = len(ds)
+        shp = tuple(np.shape(mats[0]) if as_np else mats[0].shape)
+        if len(shp) != 2 or min(shp) < 1:
+            raise ContractViolation(f"matrix must be 2-d and non-empty, got {shp}")
+        n, m = shp
+        W = len(mats)
         world = comm.world_size
         self._charge_compress(comm, n, m, W)
         r = self.effective_rank(n, m)
-        pl = _plan(n, m, self.rank, world, dev)
+        ws = self._ws(n, m, W, world, dev, as_np)
+        pl = ws.pl
         lib = _lib.lib()
-        sp = stream_ptr()
         h = pl.handle
-        f32 = dict(dtype=torch.float32, device=dev)
-        q_in = torch.zeros(pl.q_elems, **f32)
-        pl.q_view(q_in, 0).copy_(self._q_for(ctx, n, m, dev))
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
-        repl = pl.repl_table()
-        phat = torch.zeros(pl.p_elems, **f32)
-        works, ps = [], []
         with torch.cuda.device(dev):
-            for d in ds:       # low_rank_iteration :336 (delta comes in already EF-added)
-                g = torch.zeros(pl.flat_elems, **f32)
-                pl.matrix_view(g, 0).copy_(d)
-                w = torch.empty(pl.flat_elems, **f32)
-                p = torch.zeros(pl.p_elems, **f32)
-                _lib.check(lib.psgd_ef_p(h, ptr(g), None, ptr(w), ptr(q_in), ptr(p), None, ptr(status), sp),
-                           "psgd_ef_p")
-                works.append(w)
-                ps.append(p)
+            sp = stream_ptr()
+            for w, x in enumerate(mats):  # the worker matrices (delta: EF already added by the caller)
+                if as_np:
+                    np.copyto(ws.h_in[w].numpy(), np.asarray(x), casting="unsafe")
+                    pl.matrix_view(ws.g[w], 0).view(n, m).copy_(ws.h_in[w], non_blocking=True)
+                else:
+                    pl.matrix_view(ws.g[w], 0).view(n, m).copy_(x.detach())
+            pl.q_view(ws.q_in, 0).copy_(self._q_for(ctx, n, m, dev))
+            for w in range(W):           # low_rank_iteration :336
+                _lib.check(lib.psgd_ef_p(h, ptr(ws.g[w]), None, ptr(ws.works[w]), ptr(ws.q_in), ptr(ws.ps[w]),
+                                         None, ptr(ws.status), sp), "psgd_ef_p")
             if dist:                      # :337
                 comm.charge_allreduce(FLOAT_BITS * n * r)
-                comm.all_reduce_sum_(ps[0])
-                pm, div = ps[0], world
+                comm.all_reduce_sum_(ws.ps[0])
+                pm, div = ws.ps[0], world
             elif W > 1:
                 comm.charge_allreduce(FLOAT_BITS * n * r)
-                pm, div = torch.empty_like(ps[0]), 1
-                tree_mean_(ps, pm)
+                tree_mean_(ws.ps, ws.pm)
+                pm, div = ws.pm, 1
             else:
-                pm, div = ps[0], 1
-            qws, escratch = [], torch.empty(pl.flat_elems, **f32)
-            for w in works:               # :338-339 (GS, q_w) and the EF locals (:376-378)
-                qw = torch.zeros(pl.q_elems, **f32)
-                _lib.check(lib.psgd_q_ef(h, ptr(w), ptr(pm), div, ptr(repl), ptr(phat), ptr(qw),
-                                         ptr(escratch), None, ptr(status), sp), "psgd_q_ef")
-                qws.append(qw)
+                pm, div = ws.ps[0], 1
+            for w in range(W):            # :338-339 (GS, q_w) and the EF locals (:376-378)
+                _lib.check(lib.psgd_q_ef(h, ptr(ws.works[w]), ptr(pm), div, ptr(ws.repl), ptr(ws.phat),
+                                         ptr(ws.qws[w]), ptr(ws.escratch), None, ptr(ws.status), sp), "psgd_q_ef")
             if world == 1:
-                qbar = qws[0]
-                agg = works[0]            # K3 wrote M-hat == local (W=1)
-                locs = [agg.clone()]
+                qbar, agg, locs = ws.qws[0], ws.works[0], [ws.works[0]]  # K3 wrote M-hat == local (W=1)
             else:                         # :340, :375
                 comm.charge_allreduce(FLOAT_BITS * m * r)
                 if dist:
-                    qbar = qws[0].clone()
-                    comm.all_reduce_sum_(qbar)
-                    qdiv = world
+                    ws.qbar.copy_(ws.qws[0])
+                    comm.all_reduce_sum_(ws.qbar)
+                    qsum, qdiv = ws.qbar, world
                 else:
-                    qbar = torch.empty_like(qws[0])
-                    tree_mean_(qws, qbar)
-                    qdiv = 1
-                agg = torch.empty(pl.flat_elems, **f32)
-                qstore = torch.zeros(pl.q_elems, **f32)
-                _lib.check(lib.psgd_decompress(h, ptr(phat), ptr(qbar), qdiv, ptr(qstore), ptr(agg),
-                                               ptr(status), sp), "psgd_decompress")
-                if qdiv != 1:
-                    qbar = qstore
-                locs = []
-                for qw in qws:
-                    loc = torch.empty(pl.flat_elems, **f32)
-                    _lib.check(lib.psgd_decompress(h, ptr(phat), ptr(qw), 1, None, ptr(loc), ptr(status), sp),
-                               "psgd_decompress")
-                    locs.append(loc)
-        st = int(status.item())
-        if st & (_lib.STATUS_NONFINITE_GRAD | _lib.STATUS_NONFINITE_P):
-            raise ContractViolation("orthogonalize input contains non-finite entries")
-        if st & _lib.STATUS_REPLACEMENT:
-            raise RuntimeError(f"Gram-Schmidt needed more than {_lib.REPL_ATTEMPTS} replacement draws for a column")
-        q_new = pl.q_view(qbar, 0).contiguous()
-        self.q_memory[ctx.param_index] = q_new           # :373
-        comm.stats.decode_ops += 2 * n * m * r           # :374
-        payload = LowRank(_out(pl.p_view(phat, 0).clone(), as_np), _out(q_new, as_np))
-        return RoundTrip(_out(pl.matrix_view(agg, 0).clone(), as_np),
-                         [_out(pl.matrix_view(x, 0).clone(), as_np) for x in locs], payload)
+                    tree_mean_(ws.qws, ws.qbar)
+                    qsum, qdiv = ws.qbar, 1
+                _lib.check(lib.psgd_decompress(h, ptr(ws.phat), ptr(qsum), qdiv, ptr(ws.qstore), ptr(ws.agg),
+                                               ptr(ws.status), sp), "psgd_decompress")
+                qbar = ws.qstore if qdiv != 1 else ws.qbar
+                agg = ws.agg
+                for w in range(W):
+                    _lib.check(lib.psgd_decompress(h, ptr(ws.phat), ptr(ws.qws[w]), 1, None, ptr(ws.locs[w]),
+                                                   ptr(ws.status), sp), "psgd_decompress")
+                locs = ws.locs
+            comm.stats.decode_ops += 2 * n * m * r           # :374
+            if not as_np:  # device results; errors surface at check()
+                st = self._sticky.get(dev)
+                if st is None:
+                    st = self._sticky[dev] = torch.zeros(1, dtype=torch.int32, device=dev)
+                st.bitwise_or_(ws.status)
+                q_new = pl.q_view(qbar, 0).clone()
+                self.q_memory[ctx.param_index] = q_new       # :373
+                self._q_dev[ctx.param_index] = (q_new, q_new)
+                payload = LowRank(pl.p_view(ws.phat, 0).clone(), q_new)
+                return RoundTrip(pl.matrix_view(agg, 0).view(n, m).clone(),
+                                 [pl.matrix_view(x, 0).view(n, m).clone() for x in locs], payload)
+            # numpy: every output copied out, one synchronisation, the status checked before anything is stored
+            ws.h_agg.copy_(pl.matrix_view(agg, 0).view(n, m), non_blocking=True)
+            if world > 1:
+                for w in range(W):
+                    ws.h_locs[w].copy_(pl.matrix_view(locs[w], 0).view(n, m), non_blocking=True)
+            ws.h_p.copy_(pl.p_view(ws.phat, 0), non_blocking=True)
+            ws.h_q.copy_(pl.q_view(qbar, 0), non_blocking=True)
+            ws.h_st.copy_(ws.status, non_blocking=True)
+            q_keep = pl.q_view(qbar, 0).clone()
+            torch.cuda.current_stream().synchronize()
+        _raise_status(int(ws.h_st[0]))
+        q_new = ws.h_q.numpy().astype(np.float64)
+        self.q_memory[ctx.param_index] = q_new               # :373
+        self._q_dev[ctx.param_index] = (q_new, q_keep)
+        agg_np = ws.h_agg.numpy().astype(np.float64)
+        if world == 1:  # the local IS the aggregate at W = 1: a read-only view instead of an 11M-element copy
+            loc = agg_np.view()
+            loc.flags.writeable = False
+            locs_np = [loc]
+        else:
+            locs_np = [x.numpy().astype(np.float64) for x in ws.h_locs]
+        return RoundTrip(agg_np, locs_np, LowRank(ws.h_p.numpy().astype(np.float64), q_new))
 
     def compress(self, m, ctx):
         """Single-worker fused round; updates the warm-start memory (:381-384)."""

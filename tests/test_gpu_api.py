@@ -118,6 +118,29 @@ def test_world_size_mismatch_and_nonfinite():
         comp.round_trip([bad], ctx_at(), Communicator(1))
 
 
+def test_tensor_mode_defers_errors_to_check_and_numpy_q_memory():
+    """CUDA-tensor calls do not synchronise: a non-finite input is raised by check();
+    numpy calls keep q_memory as float64 numpy (compressors.py:357, :373), and repeated
+    calls reuse the cached workspace and the device mirror of Q (same results as a
+    fresh compressor fed the same q_memory)."""
+    comp = make_compressor("powersgd", rank=2)
+    bad = torch.randn(30, 20, device="cuda")
+    bad[1, 1] = float("nan")
+    comp.round_trip([bad], ctx_at(), Communicator(1))  # no raise here
+    with pytest.raises(ContractViolation):
+        comp.check()
+    comp.check()  # cleared
+    mats = worker_mats(1, n=30, m=20)
+    a1 = comp.round_trip(mats, ctx_at(param=5), Communicator(1))
+    assert isinstance(comp.q_memory[5], np.ndarray) and comp.q_memory[5].dtype == np.float64
+    a2 = comp.round_trip(mats, ctx_at(param=5, step=1), Communicator(1))
+    comp2 = make_compressor("powersgd", rank=2)
+    comp2.q_memory[5] = a1.payload.q.copy()
+    b2 = comp2.round_trip(mats, ctx_at(param=5, step=1), Communicator(1))
+    np.testing.assert_array_equal(a2.aggregated, b2.aggregated)
+    np.testing.assert_array_equal(a2.payload.q, b2.payload.q)
+
+
 def test_torch_tensors_in_and_out():
     mats = [torch.randn(40, 24, device="cuda") for _ in range(2)]
     rt = make_compressor("powersgd", rank=2).round_trip(mats, ctx_at(), Communicator(2))
