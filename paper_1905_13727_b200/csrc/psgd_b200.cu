@@ -809,6 +809,7 @@ __global__ void __launch_bounds__(256)
   __shared__ double red[64];
   __shared__ int s_last, s_direct, s_refine;
   pdl_wait();
+  pdl_trigger();  // the next pass / k2_apply may stage in; it waits for this grid itself
   if (PASS == 1) {
     int bad = 0;  // a non-finite gradient on any worker (flags ride in P): mutate nothing
     for (int x = threadIdx.x; x < nflags; x += blockDim.x) bad |= P[flag_off + x] != 0.f;
@@ -989,6 +990,7 @@ __global__ void __launch_bounds__(256)
              const int* __restrict__ blk_row0, const float* __restrict__ P, int divisor,
              const double* __restrict__ wsT, float* __restrict__ Phat, const int* status) {
   pdl_wait();
+  pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
   const int gidx = blk_mat[blockIdx.x];
   const double* T = wsT + (long long)gidx * K2G_TS;
@@ -1061,6 +1063,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   constexpr int DCAP = k3_dcap(R);
   extern __shared__ __align__(16) unsigned char k3smem[];
   __shared__ int s_flag;
+  pdl_trigger();  // dependents only stage in; they wait for this grid before reading its output
   const SlabItem it = items[blockIdx.x];
   const int t = threadIdx.x;
   const bool fused = !TALL;  // fused: all n rows in this CTA; tall: split rows, q partials
@@ -1595,6 +1598,8 @@ __global__ void __launch_bounds__(kThreads) k45_rows(const MatDev* __restrict__ 
                                                      const float* __restrict__ qsrc, int divisor,
                                                      float* __restrict__ qstore, int write_mhat,
                                                      const int* __restrict__ status, SgdArgs sg) {
+  pdl_wait();
+  pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
   const bool fuse = MODE == 1 && sg.x != nullptr;  // K5 with the optimizer update (optimizer.py:131-134)
   if (fuse) sgd_bias(sg, (long long)blockIdx.x * kThreads + threadIdx.x, (long long)gridDim.x * kThreads);
@@ -1725,6 +1730,8 @@ __global__ void __launch_bounds__(kThreads) k4_tile(const MatDev* __restrict__ m
                                                     int beg, int end, float* __restrict__ work, float* __restrict__ e,
                                                     const float* __restrict__ Phat, const float* __restrict__ qsrc,
                                                     int write_mhat, const int* __restrict__ status) {
+  pdl_wait();
+  pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
   const int lane = threadIdx.x & 31;
   const int wi = beg + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
@@ -1907,6 +1914,8 @@ __global__ void __launch_bounds__(kThreads) k3_tile(const MatDev* __restrict__ m
                                                     int nitems, const long long* __restrict__ part_off,
                                                     const float* __restrict__ work, const float* __restrict__ Phat,
                                                     float* __restrict__ part, const int* __restrict__ status) {
+  pdl_wait();
+  pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
   const int lane = threadIdx.x & 31;
   const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
@@ -1964,6 +1973,8 @@ __global__ void __launch_bounds__(256) k3_tile_reduce(const MatDev* __restrict__
                                                       const long long* __restrict__ part_off,
                                                       const float* __restrict__ part, float* __restrict__ qout,
                                                       const int* __restrict__ status) {
+  pdl_wait();
+  pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
   const int mi = list[blockIdx.y];
   const MatDev md = mats[mi];
@@ -1994,6 +2005,8 @@ __global__ void __launch_bounds__(kThreads) k4_tile2(const MatDev* __restrict__ 
                                                      int beg, int end, float* __restrict__ work, float* __restrict__ e,
                                                      const float* __restrict__ Phat, const float* __restrict__ qsrc,
                                                      int write_mhat, const int* __restrict__ status) {
+  pdl_wait();
+  pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
   const int lane = threadIdx.x & 31;
   const int wi = beg + blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
@@ -2960,10 +2973,9 @@ struct RunK45Mode {
       const int nitems = gp.end - gp.beg;
       if (nitems <= 0) return PSGD_OK;
       const int blocks = (nitems + 7) / 8;
-      k45_rows<R, EXACT, MODE><<<blocks, kThreads, 0, st>>>(pl->d_mats, items, gp.beg, gp.end, work,
-                                                            e, phat, qsrc, divisor, qstore,
-                                                            write_mhat, status, sg);
-      PSGD_CUDA_CHECK(cudaGetLastError());
+      PSGD_CUDA_CHECK(launch_ex(k45_rows<R, EXACT, MODE>, blocks, kThreads, 0, st, PSGD_PDL != 0,
+                                (const MatDev*)pl->d_mats, items, gp.beg, gp.end, work, e, phat, qsrc, divisor,
+                                qstore, write_mhat, status, sg));
       return PSGD_OK;
     }
   };
@@ -2977,9 +2989,9 @@ int RunK4T2<R, EXACT>::run(const psgd_plan* pl, const Group& gp, float* work, fl
                            const float* q, int write_mhat, const int* status, cudaStream_t st) {
   const int nitems = gp.end - gp.beg;
   if (nitems <= 0) return PSGD_OK;
-  k4_tile2<R, EXACT><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k4t, gp.beg, gp.end, work, e, phat, q,
-                                                              write_mhat, status);
-  PSGD_CUDA_CHECK(cudaGetLastError());
+  PSGD_CUDA_CHECK(launch_ex(k4_tile2<R, EXACT>, (nitems + 7) / 8, kThreads, 0, st, PSGD_PDL != 0,
+                            (const MatDev*)pl->d_mats, (const TileItem*)pl->d_k4t, gp.beg, gp.end, work, e, phat, q,
+                            write_mhat, status));
   return PSGD_OK;
 }
 
@@ -2989,9 +3001,9 @@ struct RunK4T {
                  int write_mhat, const int* status, cudaStream_t st) {
     const int nitems = gp.end - gp.beg;
     if (nitems <= 0) return PSGD_OK;
-    k4_tile<R, EXACT><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k4t, gp.beg, gp.end, work, e, phat, q,
-                                                               write_mhat, status);
-    PSGD_CUDA_CHECK(cudaGetLastError());
+    PSGD_CUDA_CHECK(launch_ex(k4_tile<R, EXACT>, (nitems + 7) / 8, kThreads, 0, st, PSGD_PDL != 0,
+                              (const MatDev*)pl->d_mats, (const TileItem*)pl->d_k4t, gp.beg, gp.end, work, e, phat,
+                              q, write_mhat, status));
     return PSGD_OK;
   }
 };
@@ -3086,11 +3098,12 @@ int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, 
   }
   if (!pl->gram_items.empty()) {
     for (int pass = 1; pass <= 2; ++pass)  // pass 2 (re-orthogonalisation) exits at once unless pass 1 asks for it
-      PSGD_CUDA_CHECK(launch_ex(pass == 1 ? k2_gram<1> : k2_gram<2>, (int)pl->gram_items.size(), 256, 0, st, false,
+      PSGD_CUDA_CHECK(launch_ex(pass == 1 ? k2_gram<1> : k2_gram<2>, (int)pl->gram_items.size(), 256, 0, st,
+                                PSGD_PDL != 0,
                                 (const MatDev*)pl->d_mats, (const GramItem*)pl->d_gram_items, p, divisor, repl,
                                 pl->d_wsg, pl->d_wsT, pl->d_gram_cnt, (long long)pl->flag_off, pl->nflags,
                                 pl->d_gsws, phat, status));
-    PSGD_CUDA_CHECK(launch_ex(k2_apply, (int)pl->apply_mat.size(), 256, 0, st, false, (const MatDev*)pl->d_mats,
+    PSGD_CUDA_CHECK(launch_ex(k2_apply, (int)pl->apply_mat.size(), 256, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
                               (const int*)pl->d_gram_list, (const int*)pl->d_apply_mat,
                               (const int*)pl->d_apply_row0, p, divisor, (const double*)pl->d_wsT, phat,
                               (const int*)status));
@@ -3169,19 +3182,29 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
   if (!pl->k3t.empty()) {  // K3 column tiles (tall, m % 4 == 0), then the in-order block reduction
     const int nitems = (int)pl->k3t.size();
     switch (pl->rmax) {
-      case 1: k3_tile<1><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
-      case 2: k3_tile<2><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
-      case 4: k3_tile<4><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
-      case 8: k3_tile<8><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
-      default: k3_tile<16><<<(nitems + 7) / 8, kThreads, 0, st>>>(pl->d_mats, pl->d_k3t, nitems, pl->d_k3t_off, work, p_hat, pl->d_k3t_part, (const int*)status); break;
+      case 1: PSGD_CUDA_CHECK(launch_ex(k3_tile<1>, (nitems + 7) / 8, kThreads, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats, (const TileItem*)pl->d_k3t, nitems, (const long long*)pl->d_k3t_off, (const float*)work, (const float*)p_hat, pl->d_k3t_part, (const int*)status)); break;
+      case 2: PSGD_CUDA_CHECK(launch_ex(k3_tile<2>, (nitems + 7) / 8, kThreads, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats, (const TileItem*)pl->d_k3t, nitems, (const long long*)pl->d_k3t_off, (const float*)work, (const float*)p_hat, pl->d_k3t_part, (const int*)status)); break;
+      case 4: PSGD_CUDA_CHECK(launch_ex(k3_tile<4>, (nitems + 7) / 8, kThreads, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats, (const TileItem*)pl->d_k3t, nitems, (const long long*)pl->d_k3t_off, (const float*)work, (const float*)p_hat, pl->d_k3t_part, (const int*)status)); break;
+      case 8: PSGD_CUDA_CHECK(launch_ex(k3_tile<8>, (nitems + 7) / 8, kThreads, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats, (const TileItem*)pl->d_k3t, nitems, (const long long*)pl->d_k3t_off, (const float*)work, (const float*)p_hat, pl->d_k3t_part, (const int*)status)); break;
+      default: PSGD_CUDA_CHECK(launch_ex(k3_tile<16>, (nitems + 7) / 8, kThreads, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats, (const TileItem*)pl->d_k3t, nitems, (const long long*)pl->d_k3t_off, (const float*)work, (const float*)p_hat, pl->d_k3t_part, (const int*)status)); break;
     }
-    PSGD_CUDA_CHECK(cudaGetLastError());
     long long maxmr = 0;
     for (int mi : pl->k3t_list) maxmr = std::max(maxmr, (long long)pl->mats[mi].m * pl->mats[mi].r);
     dim3 grid((unsigned)std::min<long long>((maxmr + 255) / 256, 64), (unsigned)pl->k3t_list.size());
-    k3_tile_reduce<<<grid, 256, 0, st>>>(pl->d_mats, pl->d_k3t_list, pl->d_k3t_off, pl->d_k3t_part, q_out,
-                                         (const int*)status);
-    PSGD_CUDA_CHECK(cudaGetLastError());
+    {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(256);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = PSGD_PDL ? 1 : 0;
+      PSGD_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_tile_reduce, (const MatDev*)pl->d_mats, (const int*)pl->d_k3t_list,
+                                         (const long long*)pl->d_k3t_off, (const float*)pl->d_k3t_part, q_out,
+                                         (const int*)status));
+    }
   }
   for (const Group& gp : pl->g4) {
     rc = dispatch_r<RunK4>(gp.r, pl, (const RowItem*)pl->d_k4, gp, work, e, (const float*)p_hat,
