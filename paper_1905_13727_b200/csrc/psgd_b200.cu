@@ -1336,17 +1336,120 @@ struct K3PLayout {
   int off_red, off_qs, off_bar, total;
   int red_floats;  // per consumer group: K3P_GW x C x r
 };
+struct K3GS {  // Gram-Schmidt of the pipeline's matrices inside k3_pipe (no K2 launch for them)
+  const int* list;     // matrices orthogonalised here; CTA b owns list[b], list[b + grid], ...
+  int n;               // 0: P-hat comes from K2 (the previous launch)
+  int* ready;          // per matrix: 1 once its P-hat is published (reset by the last CTA out)
+  const float* P;      // summed P: flag tail at flag_off, bias tail at bias_off
+  const double* repl;
+  float* bias_out;     // non-null: this launch writes the bias mean
+  long long flag_off, bias_off, nbias;
+  int nflags, divisor;
+};
 struct K3PHdr {  // what the consumers need of a staged slab (written by the producer)
   long long base, q_off;  // base: flat offset of (row 0, column c0)
   int n, m, r, C, c0, direct, qld, live;  // live = 0: no more slabs
 };
+
+// linalg.py:61-90 for one matrix (n <= 512, r <= R) by one consumer group of k3_pipe:
+// thread gt owns rows gt and gt + 256 in registers (float64), reductions over the
+// group's named barrier; the same MGS sequence, threshold and seeded replacement loop
+// (linalg.py:82-88, draws from repl) as mgs_inplace.
+struct GroupReducer256 {
+  double* red;  // 2 x K3P_GW doubles
+  int* parity;
+  int bar_id;
+  __device__ double sum(double v) const {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, gw = (threadIdx.x >> 5) % K3P_GW;
+    double* buf = red + K3P_GW * (*parity & 1);
+    ++*parity;
+    if (lane == 0) buf[gw] = v;
+    bar_named(bar_id, K3P_GT);
+    double t2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < K3P_GW; ++w) t2 += buf[w];
+    return t2;
+  }
+};
+
+template <int R>
+__device__ void group_mgs(const MatDev& md, const float* __restrict__ P, int divisor, const double* __restrict__ repl,
+                          float* __restrict__ Phat, int* status, const GroupReducer256& red, int gt) {
+  const int n = md.n, r = md.r;
+  const double inv_div = 1.0 / (double)divisor;
+  double x[2][R];
+  bool bad = false;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = gt + K3P_GT * h;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const float v = (i < n && j < r) ? __ldcg(P + md.p_off + (long long)i * r + j) : 0.f;
+      bad |= !finite1(v);
+      x[h][j] = (double)v * inv_div;
+    }
+  }
+  if (red.sum(bad ? 1.0 : 0.0) != 0.0) {  // linalg.py:35-36 (ContractViolation)
+    if (gt == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
+    return;
+  }
+  auto dot = [&](int a, int b) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) s2 = fma(x[h][a], x[h][b], s2);
+    return red.sum(s2);
+  };
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j >= r) break;
+    double before = sqrt(dot(j, j));
+    double nrm = before;
+    for (int attempt = 0;; ++attempt) {  // attempt a > 0: after the a-th replacement draw
+      if (attempt > 0 || j > 0) {
+#pragma unroll
+        for (int i2 = 0; i2 < R; ++i2) {
+          if (i2 >= j) break;
+          const double c = dot(i2, j);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) x[h][j] -= c * x[h][i2];
+        }
+        nrm = sqrt(dot(j, j));
+      }
+      if (!(nrm < 1e-12 * (before + 1.0))) break;  // linalg.py:82-88
+      if (attempt == PSGD_REPL_ATTEMPTS) {
+        if (gt == 0) atomicOr(status, PSGD_STATUS_REPLACEMENT);
+        break;
+      }
+      const double* rv = repl + md.repl_off + ((long long)attempt * md.rcols + j) * n;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = gt + K3P_GT * h;
+        x[h][j] = i < n ? rv[i] : 0.0;
+      }
+      before = 1.0;
+    }
+    const double inv = 1.0 / nrm;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) x[h][j] *= inv;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int i = gt + K3P_GT * h;
+    if (i < n)
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (j < r) Phat[md.p_off + (long long)i * r + j] = (float)x[h][j];
+  }
+}
 
 template <int R>
 __global__ void __launch_bounds__(K3P_CT + 32, 1)
     k3_pipe(const __grid_constant__ K3Maps maps, const MatDev* __restrict__ mats, const PipeItem* __restrict__ items,
             int nitems, K3PLayout L, float* __restrict__ work, const float* __restrict__ Phat,
             float* __restrict__ qout, float* __restrict__ e, int write_mhat, int* __restrict__ ctr, int* status,
-            SgdArgs sg) {
+            SgdArgs sg, K3GS gs) {
   extern __shared__ __align__(1024) unsigned char k3p_smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(k3p_smem + L.off_bar);
   uint64_t* empty = full + L.stages;
@@ -1365,6 +1468,10 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
     if (lane == 0) {
       const uint64_t pol = pol_evict_first();
       bool waited = false;
+      if (gs.n > 0) {  // no K2 in front: delta (K1's output) is final only after this
+        pdl_wait();
+        waited = true;
+      }
       // one item of lookahead: the next slab's index (global atomic) and descriptors
       // are fetched while the current slab's copies fly, so the dependent
       // atomic -> item -> matrix loads are off the issue path
@@ -1396,6 +1503,8 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
           pdl_wait();
           waited = true;
         }
+        if (gs.n > 0)  // P-hat of this matrix published by its owner CTA
+          while (ld_acquire(gs.ready + pi.mat) == 0) __nanosleep(32);
         tma_load(dst + L.slab_floats, Phat + md.p_off, pb, &full[s], pol);
         it = atomicAdd(ctr, 1);
         if (it < nitems) {
@@ -1413,8 +1522,33 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
   float* red = reinterpret_cast<float*>(k3p_smem + L.off_red) + grp * L.red_floats;  // K3P_GW x C x r
   float* qs = reinterpret_cast<float*>(k3p_smem + L.off_qs) + grp * K3P_QS;          // C x r
   const int bar_id = 1 + grp;
-  pdl_wait();  // K2 complete: P-hat and the status word are final
-  const bool skip = (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) != 0;  // mutate nothing
+  pdl_wait();  // K2 / K1 / the P all-reduce complete: P (or P-hat) and the status word are final
+  bool skip = (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) != 0;  // mutate nothing
+  if (gs.n > 0) {
+    // no K2 in front: the non-finite flags of every K1 CTA (optimizer.py:72-76, carried in P)
+    bool fl = false;
+    for (int x = lane; x < gs.nflags; x += 32) fl |= gs.P[gs.flag_off + x] != 0.f;
+    fl = __any_sync(0xffffffffu, fl);
+    skip |= fl;
+    if (blockIdx.x == 0 && t == 0 && fl) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+    if (gs.bias_out && !skip)  // bias mean (optimizer.py:111-113)
+      for (long long x = (long long)blockIdx.x * K3P_CT + t; x < gs.nbias; x += (long long)gridDim.x * K3P_CT) {
+        const float v = gs.P[gs.bias_off + x];
+        gs.bias_out[x] = gs.divisor == 1 ? v : v / (float)gs.divisor;
+      }
+    if (grp == 0) {  // this CTA's matrices: P-hat = MGS(P / W) (linalg.py:61-90), then publish
+      __shared__ double gsred[2 * K3P_GW];
+      int par = 0;
+      GroupReducer256 gr{gsred, &par, bar_id};
+      for (int k = blockIdx.x; k < gs.n; k += gridDim.x) {
+        const int mi = gs.list[k];
+        if (!skip) group_mgs<R>(mats[mi], gs.P, gs.divisor, gs.repl, const_cast<float*>(Phat), status, gr, gt);
+        __threadfence();
+        bar_named(bar_id, K3P_GT);
+        if (gt == 0) st_release(gs.ready + mi, 1);
+      }
+    }
+  }
   if (sg.x && !skip) sgd_bias(sg, (long long)blockIdx.x * K3P_CT + t, (long long)gridDim.x * K3P_CT);
   const bool fuse = sg.x != nullptr;
   const bool store_mhat = write_mhat && (!fuse || sg.keep);
@@ -1581,6 +1715,7 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
     if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
       ctr[0] = 0;
       ctr[1] = 0;
+      for (int k = 0; k < gs.n; ++k) gs.ready[gs.list[k]] = 0;  // every producer is done with them
     }
   }
 }
@@ -2184,6 +2319,9 @@ struct psgd_plan {
   int k2_smem = 0;
   std::vector<int> small_list, gram_list;   // K2 in smem / in Gram space
   std::vector<int> wlist, clist;             // K2 small: warp items / CTA items
+  std::vector<int> wlist3, clist3;           // the same without the matrices k3_pipe orthogonalises
+  std::vector<int> gs3_list;                 // matrices orthogonalised inside k3_pipe (psgd_q_ef)
+  int *d_small_list3 = nullptr, *d_gs3_list = nullptr, *d_gs3_ready = nullptr;
   int k2_wregion = 0, k2_wblocks = 0;
   std::vector<GramItem> gram_items;
   std::vector<int> apply_mat, apply_row0;   // k2_apply blocks
@@ -2655,11 +2793,20 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       return off + 2LL * stages * 8 + (long long)stages * sizeof(K3PHdr) + 16;
     };
     L.stages = 2;
-    while (L.stages < maxst && total_for(L.stages + 1) <= 227 * 1024) ++L.stages;
+    while (L.stages < maxst && total_for(L.stages + 1) <= 225 * 1024) ++L.stages;  // + static smem
     L.off_red = L.stages * L.stage_floats * 4;
     L.off_qs = L.off_red + (int)redf * 4;
     L.off_bar = (L.off_qs + (int)qsf * 4 + 15) & ~15;
     L.total = (int)total_for(L.stages);
+  }
+  {  // Gram-Schmidt of the pipeline's matrices inside k3_pipe (owner CTAs), not in K2
+    static const bool off = getenv("PSGD_K3_GS") && getenv("PSGD_K3_GS")[0] == '0';
+    for (int mi = 0; mi < nmat && !off; ++mi)
+      if (pl->mats[mi].pipe) pl->gs3_list.push_back(mi);
+    for (int mi : pl->wlist)
+      if (std::find(pl->gs3_list.begin(), pl->gs3_list.end(), mi) == pl->gs3_list.end()) pl->wlist3.push_back(mi);
+    for (int mi : pl->clist)
+      if (std::find(pl->gs3_list.begin(), pl->gs3_list.end(), mi) == pl->gs3_list.end()) pl->clist3.push_back(mi);
   }
   build_row_items(pl->mats, true, pl->k4, pl->g4);
   build_tile_items(pl->mats, pl->k4t, pl->g4t);
@@ -2708,7 +2855,9 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_k3 = take(pl->k3.size() * sizeof(SlabItem));
   const size_t o_tl = take(pl->tall_list.size() * sizeof(int));
   const size_t o_al = take(pl->all_list.size() * sizeof(int));
-  const size_t o_sl = take((pl->wlist.size() + pl->clist.size()) * sizeof(int));
+  const size_t o_sl = take((pl->wlist.size() + pl->clist.size() + pl->wlist3.size() + pl->clist3.size()) * sizeof(int));
+  const size_t o_g3l = take(pl->gs3_list.size() * sizeof(int));
+  const size_t o_g3r = take((size_t)std::max(1, nmat) * sizeof(int));
   const size_t o_gl = take(pl->gram_list.size() * sizeof(int));
   const size_t o_gi = take(pl->gram_items.size() * sizeof(GramItem));
   const size_t o_am = take(pl->apply_mat.size() * sizeof(int));
@@ -2749,6 +2898,9 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_tall_list = reinterpret_cast<int*>(b + o_tl);
   pl->d_all_list = reinterpret_cast<int*>(b + o_al);
   pl->d_small_list = reinterpret_cast<int*>(b + o_sl);
+  pl->d_small_list3 = pl->d_small_list + pl->wlist.size() + pl->clist.size();
+  pl->d_gs3_list = reinterpret_cast<int*>(b + o_g3l);
+  pl->d_gs3_ready = reinterpret_cast<int*>(b + o_g3r);
   pl->d_gram_list = reinterpret_cast<int*>(b + o_gl);
   pl->d_gram_items = reinterpret_cast<GramItem*>(b + o_gi);
   pl->d_apply_mat = reinterpret_cast<int*>(b + o_am);
@@ -2789,9 +2941,13 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   {
     std::vector<int> wc(pl->wlist);
     wc.insert(wc.end(), pl->clist.begin(), pl->clist.end());
+    wc.insert(wc.end(), pl->wlist3.begin(), pl->wlist3.end());
+    wc.insert(wc.end(), pl->clist3.begin(), pl->clist3.end());
     if (ce == cudaSuccess) ce = up(pl->d_small_list, wc.data(), wc.size() * sizeof(int));
   }
   if (ce == cudaSuccess) ce = up(pl->d_gram_list, pl->gram_list.data(), pl->gram_list.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_gs3_list, pl->gs3_list.data(), pl->gs3_list.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = cudaMemset(pl->d_gs3_ready, 0, (size_t)std::max(1, nmat) * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_gram_items, pl->gram_items.data(), pl->gram_items.size() * sizeof(GramItem));
   if (ce == cudaSuccess) ce = up(pl->d_apply_mat, pl->apply_mat.data(), pl->apply_mat.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_apply_row0, pl->apply_row0.data(), pl->apply_row0.size() * sizeof(int));
@@ -2848,12 +3004,19 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   const bool any_fused = pl->n_tall < pl->nmat;
   o->launches_ef_p = ((pl->k1.empty() && pl->nbias == 0) ? 0 : 1) + (pl->k1t.empty() ? 0 : 2);
   o->launches_orthogonalize = (pl->nmat + (pl->nbias > 0)) > 0 ? 1 : 0;
-  {  // same rule as psgd_q_ef: k2_gs runs for small matrices, or for the bias unless K3 takes it
+  int k2_in_q_ef;
+  {  // same rules as psgd_orthogonalize and psgd_q_ef (where k3_pipe takes the pipeline's GS and maybe the bias)
     const bool small = pl->wlist.size() + pl->clist.size() > 0;
     const bool bias_in_k3 = !small && !pl->gram_items.empty() && !pl->g3.empty();
-    o->launches_orthogonalize = ((small || (pl->nbias > 0 && !bias_in_k3)) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 3);
+    o->launches_orthogonalize = ((small || pl->nbias > 0) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 3);
+    const bool gs3 = !pl->gs3_list.empty() && !pl->pipe_items.empty();
+    const bool small3 = (gs3 ? pl->wlist3.size() + pl->clist3.size() : pl->wlist.size() + pl->clist.size()) > 0;
+    const bool bias_k3 = !small3 && !pl->gram_items.empty() && !pl->g3.empty();
+    const bool bias_pipe = gs3 && !small3 && !bias_k3;
+    k2_in_q_ef = ((small3 || (pl->nbias > 0 && !bias_k3 && !bias_pipe)) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 3);
+    (void)bias_in_k3;
   }
-  o->launches_q_ef = o->launches_orthogonalize + (pl->pipe_items.empty() ? 0 : 1) + nonempty(pl->g3) +
+  o->launches_q_ef = k2_in_q_ef + (pl->pipe_items.empty() ? 0 : 1) + nonempty(pl->g3) +
                      nonempty(pl->g4) + nonempty(pl->g4t) +
                      nonempty(pl->g4t2) +
                      (pl->k3t.empty() ? 0 : 2);
@@ -3041,7 +3204,7 @@ int encode_pipe_maps(const psgd_plan* pl, const float* work) {
 
 template <int R>
 int launch_pipe_r(const psgd_plan* pl, float* work, const float* phat, float* qout, float* e, int* status,
-                  cudaStream_t st, const SgdArgs& sg) {
+                  cudaStream_t st, const SgdArgs& sg, const K3GS& gs) {
   auto kern = k3_pipe<R>;
   PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->k3pl.total));
   const int grid = (int)std::min<size_t>(pl->nsm, pl->pipe_items.size());
@@ -3056,18 +3219,19 @@ int launch_pipe_r(const psgd_plan* pl, float* work, const float* phat, float* qo
   }
   PSGD_CUDA_CHECK(launch_ex(kern, grid, K3P_CT + 32, (size_t)pl->k3pl.total, st, PSGD_PDL != 0, maps,
                             (const MatDev*)pl->d_mats, (const PipeItem*)pl->d_pipe_items, (int)pl->pipe_items.size(),
-                            pl->k3pl, work, phat, qout, e, pl->world == 1 ? 1 : 0, pl->d_pipe_ctr, status, sg));
+                            pl->k3pl, work, phat, qout, e, pl->world == 1 ? 1 : 0, pl->d_pipe_ctr, status, sg,
+                            gs));
   return PSGD_OK;
 }
 
 int launch_pipe(const psgd_plan* pl, float* work, const float* phat, float* qout, float* e, int* status,
-                cudaStream_t st, const SgdArgs& sg) {
+                cudaStream_t st, const SgdArgs& sg, const K3GS& gs) {
   if (pl->pipe_items.empty()) return PSGD_OK;
   switch (pl->pipe_rmax) {
-    case 1: return launch_pipe_r<1>(pl, work, phat, qout, e, status, st, sg);
-    case 2: return launch_pipe_r<2>(pl, work, phat, qout, e, status, st, sg);
-    case 4: return launch_pipe_r<4>(pl, work, phat, qout, e, status, st, sg);
-    default: return launch_pipe_r<8>(pl, work, phat, qout, e, status, st, sg);
+    case 1: return launch_pipe_r<1>(pl, work, phat, qout, e, status, st, sg, gs);
+    case 2: return launch_pipe_r<2>(pl, work, phat, qout, e, status, st, sg, gs);
+    case 4: return launch_pipe_r<4>(pl, work, phat, qout, e, status, st, sg, gs);
+    default: return launch_pipe_r<8>(pl, work, phat, qout, e, status, st, sg, gs);
   }
 }
 
@@ -3078,10 +3242,11 @@ bool check_dev(const psgd_plan* pl) {
 }
 
 int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, int divisor,
-              const double* repl, float* bias_out, int* status, cudaStream_t st) {
-  const int nw = (int)pl->wlist.size();
-  const int nci = (int)pl->clist.size();
-  const int* wl = pl->d_small_list;
+              const double* repl, float* bias_out, int* status, cudaStream_t st, bool skip_pipe = false) {
+  // skip_pipe: the pipeline's matrices are orthogonalised inside k3_pipe
+  const int nw = (int)(skip_pipe ? pl->wlist3 : pl->wlist).size();
+  const int nci = (int)(skip_pipe ? pl->clist3 : pl->clist).size();
+  const int* wl = skip_pipe ? pl->d_small_list3 : pl->d_small_list;
   const int* cl = wl + nw;
   const int nwb = (nw + K2_THREADS / 32 - 1) / (K2_THREADS / 32);
   const int bias_blocks =
@@ -3164,14 +3329,21 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
   // When every matrix is orthogonalised in Gram space (k2_gram checks the
   // non-finite flags) and a K3 slab launch follows, that launch writes the bias
   // mean, so k2_gs is not launched for the bias alone.
-  const bool k2_small = pl->wlist.size() + pl->clist.size() > 0;
+  // The pipeline's matrices are orthogonalised inside k3_pipe (its owner CTAs), so no
+  // K2 launch sits between K1 (or the P all-reduce) and K3 for them.
+  const bool gs3 = !pl->gs3_list.empty() && !pl->pipe_items.empty();
+  const bool k2_small = (gs3 ? pl->wlist3.size() + pl->clist3.size() : pl->wlist.size() + pl->clist.size()) > 0;
   const bool bias_in_k3 = !k2_small && !pl->gram_items.empty() && !pl->g3.empty();
-  if (pl->nmat > 0 || pl->nbias > 0) {
-    rc = launch_k2(pl, !bias_in_k3, p, p_hat, divisor, repl, bias_out, (int*)status, st);
+  const bool bias_in_pipe = gs3 && !k2_small && !bias_in_k3;
+  if (k2_small || !pl->gram_items.empty() || (pl->nbias > 0 && !bias_in_k3 && !bias_in_pipe)) {
+    rc = launch_k2(pl, !bias_in_k3 && !bias_in_pipe, p, p_hat, divisor, repl, bias_out, (int*)status, st, gs3);
     if (rc) return rc;
   }
   bool bias_done = !bias_in_k3;
-  rc = launch_pipe(pl, work, p_hat, q_out, e, (int*)status, st, sg);  // K3 pipeline (n <= 512)
+  K3GS gs{pl->d_gs3_list, gs3 ? (int)pl->gs3_list.size() : 0, pl->d_gs3_ready, p, repl,
+          (bias_in_pipe && pl->nbias > 0) ? bias_out : nullptr, (long long)pl->flag_off, (long long)pl->p_bias_off,
+          (long long)pl->nbias, pl->nflags, (int)divisor};
+  rc = launch_pipe(pl, work, p_hat, q_out, e, (int*)status, st, sg, gs);  // K3 pipeline (n <= 512)
   if (rc) return rc;
   for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab (after K2: delta is final)
     rc = dispatch_r<RunK3>(gp.r, pl, gp, work, p, (int)divisor, repl, p_hat, q_out, e, bias_out,
