@@ -396,6 +396,11 @@ def run_ours(a):
     if world == 1 and N * 4 < (2 << 30) and not a.no_opt:
         opt = optimizer_timing(specs, a, dev, flush, barrier, stream)
 
+    # ---------------- configs[0]: the reference's own workload, 2 simulated workers on this GPU
+    sim2 = None
+    if world == 1 and a.workload == "resnet18" and not a.no_opt:
+        sim2 = simulated_w2_timing(specs, a, dev, flush, barrier, stream)
+
     # ---------------- the per-parameter drop-in (the reference's optimizer loop calling round_trip)
     dropin = None
     if world == 1 and a.workload == "resnet18" and not a.no_opt:
@@ -473,6 +478,7 @@ def run_ours(a):
             "kernels_ms": {k: round(v, 5) for k, v in kern_ms.items()},
             "optimizer_step": opt,
             "dropin": dropin,
+            "simulated_w2": sim2,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/step", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
@@ -489,7 +495,38 @@ def run_ours(a):
 
 
 
-def dropin_timing(specs, a, dev, steps=3):
+def simulated_w2_timing(specs, a, dev, flush, barrier, stream):
+    """BASELINE configs[0]: W = 2 simulated workers on one GPU (K1 x 2, tree mean of P,
+    K2/K3 x 2, tree mean of q, K5), CUDA graph, L2 flushed before every step."""
+    import statistics
+    import torch
+    from paper_1905_13727_b200 import Communicator, PowerSGDEngine
+    eng = PowerSGDEngine(specs, a.rank, workers=2, comm=Communicator(2), seed=0, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(1000)
+    for w in range(2):
+        eng.g[w].normal_(generator=gen)
+        eng.bias_g[w].normal_(generator=gen)
+    eng.capture()
+    for _ in range(a.warmup):
+        eng.run()
+    barrier()
+    ts = []
+    for _ in range(a.steps):
+        if flush is not None:
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.run()
+        e1.record(stream)
+        ts.append((e0, e1))
+    barrier()
+    eng.check()
+    return {"ms_per_step": round(statistics.mean(x.elapsed_time(y) for x, y in ts), 5),
+            "note": "configs[0]: ResNet-18 r=2, 2 simulated workers on one GPU (the CPU reference's own "
+                    "workload), CUDA graph, L2 flushed"}
+
+
+def dropin_timing(specs, a, dev, steps=5):
     """One optimizer step (optimizer.py:110-134: EF add, round_trip per matrix
     parameter, EF update, bias mean, heavy-ball update) through the drop-in
     `PowerSGD.round_trip`, once with numpy arrays on the host (the reference's own

@@ -1454,12 +1454,14 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(k3p_smem + L.off_bar);
   uint64_t* empty = full + L.stages;
   K3PHdr* hdr = reinterpret_cast<K3PHdr*>(empty + L.stages);
+  __shared__ int s_next, s_claim[K3P_GROUPS];  // stage claiming: the next ring position, per-group broadcast
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) {
     for (int s = 0; s < L.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], K3P_GW);  // a stage is consumed by one group
     }
+    s_next = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -1516,8 +1518,8 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
     return;
   }
 
-  // ---------------- consumers: K3P_GROUPS groups of K3P_GW warps take alternate
-  // stages (ping-pong), so one group's q reduction overlaps the other's stores
+  // ---------------- consumers: K3P_GROUPS groups of K3P_GW warps, each claiming the next
+  // filled stage when free (ping-pong), so one group's q reduction overlaps the other's stores
   const int grp = warp / K3P_GW, gw = warp - grp * K3P_GW, gt = t - grp * K3P_GT;
   float* red = reinterpret_cast<float*>(k3p_smem + L.off_red) + grp * L.red_floats;  // K3P_GW x C x r
   float* qs = reinterpret_cast<float*>(k3p_smem + L.off_qs) + grp * K3P_QS;          // C x r
@@ -1552,7 +1554,13 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
   if (sg.x && !skip) sgd_bias(sg, (long long)blockIdx.x * K3P_CT + t, (long long)gridDim.x * K3P_CT);
   const bool fuse = sg.x != nullptr;
   const bool store_mhat = write_mhat && (!fuse || sg.keep);
-  for (int k = grp;; k += K3P_GROUPS) {
+  for (;;) {
+    // a free group claims the next ring position (the producer fills them in order), so a
+    // group busy with an owner GS or a long slab never holds up the other one
+    if (gt == 0) s_claim[grp] = atomicAdd(&s_next, 1);
+    bar_named(bar_id, K3P_GT);
+    const int k = s_claim[grp];
+    bar_named(bar_id, K3P_GT);
     const int s = k % L.stages;
     mbar_wait(&full[s], (k / L.stages) & 1);
     const K3PHdr hd = hdr[s];
@@ -3331,7 +3339,8 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
   // mean, so k2_gs is not launched for the bias alone.
   // The pipeline's matrices are orthogonalised inside k3_pipe (its owner CTAs), so no
   // K2 launch sits between K1 (or the P all-reduce) and K3 for them.
-  const bool gs3 = !pl->gs3_list.empty() && !pl->pipe_items.empty();
+  // (not with the fused optimizer: measured 11 us slower there, 93 -> 104 us, profiles/r2/sweeps/opt_ab*.txt)
+  const bool gs3 = !pl->gs3_list.empty() && !pl->pipe_items.empty() && sg.x == nullptr;
   const bool k2_small = (gs3 ? pl->wlist3.size() + pl->clist3.size() : pl->wlist.size() + pl->clist.size()) > 0;
   const bool bias_in_k3 = !k2_small && !pl->gram_items.empty() && !pl->g3.empty();
   const bool bias_in_pipe = gs3 && !k2_small && !bias_in_k3;

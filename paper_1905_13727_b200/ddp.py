@@ -1,8 +1,9 @@
 """PyTorch DDP communication hook backed by the B200 PowerSGD path.
 
 Gradients arrive bucket by bucket during backward; each bucket is compressed as
-soon as DDP hands it over, so compression overlaps the rest of backward (the
-reference packs one flat buffer after backward, PAPER.md).  Per bucket, a
+soon as DDP hands it over, on a side stream, so compression and its exchanges
+overlap the rest of backward (the reference packs one flat buffer after backward,
+PAPER.md).  Per bucket, a
 `PowerSGDEngine` over the bucket's parameters runs the reference's per-parameter
 step (optimizer.py:110-129): delta = g + e, P = delta Q, all-reduce P (+ bias),
 P-hat = MGS(P / W), q_w = delta^T P-hat, e = delta - P-hat q_w^T, all-reduce q,
@@ -40,6 +41,13 @@ class PowerSGDState:
         self.owner = {}  # id(param) -> (engine, index in it): where its EF memory and Q live
         self.check_every = int(check_every)  # 0: never synchronise inside the hook
         self.calls = 0
+        self.streams = {}  # device -> side stream the buckets' work runs on
+
+    def stream_for(self, dev):
+        s = self.streams.get(dev)
+        if s is None:
+            s = self.streams[dev] = torch.cuda.Stream(device=dev)
+        return s
 
     @property
     def stats(self):
@@ -84,23 +92,33 @@ class PowerSGDState:
 
 
 def powersgd_hook(state, bucket):
-    """DDP comm hook: compress, exchange and decompress one gradient bucket."""
+    """DDP comm hook: compress, exchange and decompress one gradient bucket.
+
+    The bucket's work (copies, kernels, the two all-reduces) is enqueued on a side
+    stream that first waits for the backward stream, so it overlaps the rest of
+    backward on the device; the hook never blocks the host.  The returned Future is
+    CUDA-aware: DDP's use of the result waits for the side stream."""
     eng = state.engine_for(bucket)
     _, grads = state._pair(bucket)
-    for i, g in enumerate(grads):
-        eng.grad_view(i).copy_(g.view(eng.specs[i].shape))
-    eng.run()
-    for i, g in enumerate(grads):
-        g.copy_(eng.update_view(i).reshape(g.shape))
-    # A non-finite gradient on any rank (the flags ride in the P all-reduce, so every
-    # rank's status agrees) leaves e and Q untouched but no M-hat: poison the whole
-    # bucket on every rank, so an AMP GradScaler skips the step everywhere instead of
-    # the replicas applying different updates (the reference raises on all workers).
-    bad = (eng.status & (_lib.STATUS_NONFINITE_GRAD | _lib.STATUS_NONFINITE_P)) != 0
-    bucket.buffer().masked_fill_(bad, float("nan"))
-    state.calls += 1
-    if state.check_every and state.calls % state.check_every == 0:
-        eng.check()
-    fut = torch.futures.Future()
-    fut.set_result(bucket.buffer())
+    dev = eng.device
+    cur = torch.cuda.current_stream(dev)
+    side = state.stream_for(dev)
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        for i, g in enumerate(grads):
+            eng.grad_view(i).copy_(g.view(eng.specs[i].shape))
+        eng.run(side)
+        for i, g in enumerate(grads):
+            g.copy_(eng.update_view(i).reshape(g.shape))
+        # A non-finite gradient on any rank (the flags ride in the P all-reduce, so every
+        # rank's status agrees) leaves e and Q untouched but no M-hat: poison the whole
+        # bucket on every rank, so an AMP GradScaler skips the step everywhere instead of
+        # the replicas applying different updates (the reference raises on all workers).
+        bad = (eng.status & (_lib.STATUS_NONFINITE_GRAD | _lib.STATUS_NONFINITE_P)) != 0
+        bucket.buffer().masked_fill_(bad, float("nan"))
+        state.calls += 1
+        if state.check_every and state.calls % state.check_every == 0:
+            eng.check()
+        fut = torch.futures.Future(devices=[dev])
+        fut.set_result(bucket.buffer())
     return fut
