@@ -1239,7 +1239,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int o = t; o < ncols * r; o += kThreads) {
         const int k = o / ncols, cc = o - k * ncols;
         float s = 0.f;
-        for (int ch = 0; ch < it.nchunks; ++ch) s += __ldcg(part + (long long)ch * C * r + cc * r + k);
+        const float* pc = part + cc * r + k;
+        int ch = 0;
+        for (; ch + 8 <= it.nchunks; ch += 8) {  // 8 loads in flight, summed in chunk order
+          float y[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) y[u] = __ldcg(pc + (long long)(ch + u) * C * r);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s += y[u];
+        }
+        for (; ch < it.nchunks; ++ch) s += __ldcg(pc + (long long)ch * C * r);
         qdst[(long long)k * md.qld + cc] = s;
       }
       if (t == 0) counters[it.slab] = 0;
