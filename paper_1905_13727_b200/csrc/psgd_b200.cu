@@ -1330,7 +1330,6 @@ constexpr int K3P_CT = 32 * K3P_CW;            // consumer threads
 constexpr int K3P_GROUPS = PSGD_K3P_GROUPS;    // consumer groups taking alternate stages
 constexpr int K3P_GW = K3P_CW / K3P_GROUPS;    // warps per group
 constexpr int K3P_GT = 32 * K3P_GW;            // threads per group
-constexpr int K3P_QS = 128 * 8;                // qs floats per group (C <= 128, r <= 8)
 constexpr int K3P_SLAB = 16384;                // floats of delta per stage (all rows x C columns)
 constexpr int K3P_MAXMAPS = 48;
 
@@ -1344,6 +1343,7 @@ struct K3PLayout {
   int stages, phat_floats, stage_floats, slab_floats;  // stage: slab (slab_floats) | P-hat rows
   int off_red, off_qs, off_bar, total;
   int red_floats;  // per consumer group: K3P_GW x C x r
+  int qs_floats;   // per consumer group: C x r (largest slab of the plan)
 };
 struct K3GS {  // Gram-Schmidt of the pipeline's matrices inside k3_pipe (no K2 launch for them)
   const int* list;     // matrices orthogonalised here; CTA b owns list[b], list[b + grid], ...
@@ -1531,7 +1531,7 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
   // filled stage when free (ping-pong), so one group's q reduction overlaps the other's stores
   const int grp = warp / K3P_GW, gw = warp - grp * K3P_GW, gt = t - grp * K3P_GT;
   float* red = reinterpret_cast<float*>(k3p_smem + L.off_red) + grp * L.red_floats;  // K3P_GW x C x r
-  float* qs = reinterpret_cast<float*>(k3p_smem + L.off_qs) + grp * K3P_QS;          // C x r
+  float* qs = reinterpret_cast<float*>(k3p_smem + L.off_qs) + grp * L.qs_floats;     // C x r
   const int bar_id = 1 + grp;
   pdl_wait();  // K2 / K1 / the P all-reduce complete: P (or P-hat) and the status word are final
   bool skip = (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) != 0;  // mutate nothing
@@ -2770,7 +2770,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   }
   // ---- K3 pipeline slabs: all n rows x C columns, C a power of two with the slab <= 64 KB
   {
-    long long phf = 4, redf = 4;
+    long long phf = 4, redf = 4, qsmax = 4;
     static const int slabf = getenv("PSGD_K3P_SLAB") ? atoi(getenv("PSGD_K3P_SLAB")) : K3P_SLAB;
     static const int maxst = getenv("PSGD_K3P_STAGES") ? atoi(getenv("PSGD_K3P_STAGES")) : 3;
     pl->k3pl.slab_floats = slabf;
@@ -2789,6 +2789,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       for (int c0 = 0; c0 < md.m; c0 += C) pl->pipe_items.push_back({mi, c0, C, map});
       phf = std::max(phf, align4((long long)md.n * md.r));
       redf = std::max(redf, (long long)K3P_GW * C * md.r);
+      qsmax = std::max(qsmax, (long long)C * md.r);
       pl->pipe_rmax = std::max(pl->pipe_rmax, rmax_of(md.r));
     }
     // largest slabs first: the dynamic schedule then ends on small ones
@@ -2802,7 +2803,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     L.stage_floats = (int)((L.slab_floats + phf + 255) / 256 * 256);
     L.red_floats = (int)align4(redf);
     redf = (long long)K3P_GROUPS * L.red_floats;
-    const long long qsf = (long long)K3P_GROUPS * K3P_QS;
+    L.qs_floats = (int)align4(qsmax);  // sized to the plan: r = 4 keeps 3 stages of 64 KB slabs
+    const long long qsf = (long long)K3P_GROUPS * L.qs_floats;
     auto total_for = [&](int stages) {
       long long off = (long long)stages * L.stage_floats * 4;
       off += (redf + qsf) * 4;
@@ -2810,7 +2812,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       return off + 2LL * stages * 8 + (long long)stages * sizeof(K3PHdr) + 16;
     };
     L.stages = 2;
-    while (L.stages < maxst && total_for(L.stages + 1) <= 225 * 1024) ++L.stages;  // + static smem
+    while (L.stages < maxst && total_for(L.stages + 1) <= 232448 - 512) ++L.stages;  // 227 KB - static smem
     L.off_red = L.stages * L.stage_floats * 4;
     L.off_qs = L.off_red + (int)redf * 4;
     L.off_bar = (L.off_qs + (int)qsf * 4 + 15) & ~15;
