@@ -428,13 +428,16 @@ def run_ours(a):
     dom = "ef_p"
     dom_bytes = k1_bytes
     achieved = dom_bytes / (kern_ms[dom] * 1e-3) / 1e9
-    traffic = None
-    try:  # dram bytes per launch of the same kernel from the committed ncu capture
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+    traffic, traffic_src = None, None
+    prof_file = {("resnet18", 2): os.path.join("profiles", "ncu_summary.json"),
+                 ("lstm", 4): os.path.join("profiles", "r2", "ncu_summary_lstm.json")}.get((a.workload, a.rank))
+    try:  # dram bytes per launch of the same kernel from the committed ncu capture of this workload
+        with open(os.path.join(ROOT, prof_file)) as f:
             prof = json.load(f)
         for name, v in prof["kernels"].items():
-            if name.startswith("k1_ef_p") and a.workload == "resnet18" and a.rank == 2:
+            if name.startswith("k1_ef_p"):
                 traffic = v["traffic_bytes"]
+                traffic_src = f"{prof_file} (ncu --set full, one launch)"
     except Exception:
         pass
     b_alg = 24 * N + 20 * snr + 16 * smr
@@ -469,7 +472,7 @@ def run_ours(a):
             "roofline": {"bound": "hbm", "kernel": "k1_ef_p (psgd_ef_p)", "achieved": round(achieved, 1),
                          "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                          "algorithmic_bytes": dom_bytes, "peak_source": peak_src,
-                         "traffic_source": "profiles/ncu_summary.json (ncu --set full, one launch)"},
+                         "traffic_source": traffic_src},
             "step_roofline": {"algorithmic_bytes": b_alg, "t_hbm_us": round(t_hbm_us, 2),
                               "nvlink_bytes_per_gpu": round(nvl_bytes), "t_nvlink_us": round(t_nvl_us, 3),
                               "t_roof_us": round(t_roof_us, 2), "t_measured_us": round(ms * 1e3, 2),
