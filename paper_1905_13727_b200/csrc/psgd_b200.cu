@@ -2348,7 +2348,7 @@ struct psgd_plan {
   // K3 pipeline (k3_pipe): slab items, the matrices with a tensor map (map order), layout
   std::vector<PipeItem> pipe_items;
   std::vector<int> pipe_maps, pipe_mapC;
-  K3PLayout k3pl{};
+  K3PLayout k3pl{}, k3pl_f{};  // k3pl_f: the layout of the fused-optimizer launch
   int pipe_rmax = 1;
   PipeItem* d_pipe_items = nullptr;
   int* d_pipe_ctr = nullptr;
@@ -2803,20 +2803,34 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     L.stage_floats = (int)((L.slab_floats + phf + 255) / 256 * 256);
     L.red_floats = (int)align4(redf);
     redf = (long long)K3P_GROUPS * L.red_floats;
-    L.qs_floats = (int)align4(qsmax);  // sized to the plan: r = 4 keeps 3 stages of 64 KB slabs
-    const long long qsf = (long long)K3P_GROUPS * L.qs_floats;
-    auto total_for = [&](int stages) {
-      long long off = (long long)stages * L.stage_floats * 4;
-      off += (redf + qsf) * 4;
-      off = (off + 15) & ~15LL;
-      return off + 2LL * stages * 8 + (long long)stages * sizeof(K3PHdr) + 16;
+    // The q buffer is sized to the plan (r = 4 then keeps 3 stages).  The fused-optimizer launch
+    // uses the same layout with the q buffer padded to 1024 floats per group: measured faster there
+    // (ResNet-18 r=2 step + update 105 -> 92 us), while the plain step is faster with the tight
+    // layout (59.7 -> 58.2 us) — profiles/r2/sweeps/opt_ab5.txt.
+    static const int qs_pad = getenv("PSGD_K3P_QSPAD") ? atoi(getenv("PSGD_K3P_QSPAD")) : 0;
+    const long long redf_all = redf;
+    auto finish = [&](K3PLayout& X, long long qsf_group) {
+      X = L;
+      X.qs_floats = (int)align4(qsf_group);
+      const long long qsf = (long long)K3P_GROUPS * X.qs_floats;
+      auto total_for = [&](int stages) {
+        long long off = (long long)stages * X.stage_floats * 4;
+        off += (redf_all + qsf) * 4;
+        off = (off + 15) & ~15LL;
+        return off + 2LL * stages * 8 + (long long)stages * sizeof(K3PHdr) + 16;
+      };
+      X.stages = 2;
+      while (X.stages < maxst && total_for(X.stages + 1) <= 232448 - 512) ++X.stages;  // 227 KB - static smem
+      X.off_red = X.stages * X.stage_floats * 4;
+      X.off_qs = X.off_red + (int)redf_all * 4;
+      X.off_bar = (X.off_qs + (int)qsf * 4 + 15) & ~15;
+      X.total = (int)total_for(X.stages);
     };
-    L.stages = 2;
-    while (L.stages < maxst && total_for(L.stages + 1) <= 232448 - 512) ++L.stages;  // 227 KB - static smem
-    L.off_red = L.stages * L.stage_floats * 4;
-    L.off_qs = L.off_red + (int)redf * 4;
-    L.off_bar = (L.off_qs + (int)qsf * 4 + 15) & ~15;
-    L.total = (int)total_for(L.stages);
+    K3PLayout tight{}, padded{};
+    finish(tight, std::max<long long>(qsmax, qs_pad));
+    finish(padded, std::max<long long>(qsmax, 1024));
+    L = tight;
+    pl->k3pl_f = padded;
   }
   {  // Gram-Schmidt of the pipeline's matrices inside k3_pipe (owner CTAs), not in K2
     static const bool off = getenv("PSGD_K3_GS") && getenv("PSGD_K3_GS")[0] == '0';
@@ -3225,7 +3239,8 @@ template <int R>
 int launch_pipe_r(const psgd_plan* pl, float* work, const float* phat, float* qout, float* e, int* status,
                   cudaStream_t st, const SgdArgs& sg, const K3GS& gs) {
   auto kern = k3_pipe<R>;
-  PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->k3pl.total));
+  const K3PLayout& L = sg.x ? pl->k3pl_f : pl->k3pl;
+  PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
   const int grid = (int)std::min<size_t>(pl->nsm, pl->pipe_items.size());
   K3Maps maps;
   {
@@ -3236,9 +3251,9 @@ int launch_pipe_r(const psgd_plan* pl, float* work, const float* phat, float* qo
     }
     maps = pl->maps;
   }
-  PSGD_CUDA_CHECK(launch_ex(kern, grid, K3P_CT + 32, (size_t)pl->k3pl.total, st, PSGD_PDL != 0, maps,
+  PSGD_CUDA_CHECK(launch_ex(kern, grid, K3P_CT + 32, (size_t)L.total, st, PSGD_PDL != 0, maps,
                             (const MatDev*)pl->d_mats, (const PipeItem*)pl->d_pipe_items, (int)pl->pipe_items.size(),
-                            pl->k3pl, work, phat, qout, e, pl->world == 1 ? 1 : 0, pl->d_pipe_ctr, status, sg,
+                            L, work, phat, qout, e, pl->world == 1 ? 1 : 0, pl->d_pipe_ctr, status, sg,
                             gs));
   return PSGD_OK;
 }
