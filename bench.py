@@ -530,11 +530,12 @@ def simulated_w2_timing(specs, a, dev, flush, barrier, stream):
 
 
 def dropin_timing(specs, a, dev, steps=5):
-    """One optimizer step (optimizer.py:110-134: EF add, round_trip per matrix
-    parameter, EF update, bias mean, heavy-ball update) through the drop-in
-    `PowerSGD.round_trip`, once with numpy arrays on the host (the reference's own
-    calling convention: one H2D/D2H round trip and one sync per parameter) and
-    once with CUDA tensors (no per-parameter sync; errors at `check()`)."""
+    """The compression part of one optimizer step (optimizer.py:110-129: EF add,
+    round_trip per matrix parameter, EF update, bias mean — the same work the
+    reference arm times) through the drop-in `PowerSGD.round_trip`, once with numpy
+    arrays on the host (the reference's own calling convention: one H2D/D2H round
+    trip and one sync per parameter) and once with CUDA tensors (no per-parameter
+    sync; errors at `check()`)."""
     import numpy as np
     import torch
     from paper_1905_13727_b200 import Communicator, CompressionContext, PowerSGD
@@ -544,13 +545,11 @@ def dropin_timing(specs, a, dev, steps=5):
     for mode in ("numpy", "torch"):
         comp, comm = PowerSGD(a.rank), Communicator(1)
         if mode == "numpy":
-            xs = [np.zeros(s.shape) for s in specs]
-            bufs = [np.zeros(s.shape) for s in specs]
+            xs = [None] * len(specs)
             errs = {}
             g = grads
         else:
-            xs = [torch.zeros(s.shape, device=dev) for s in specs]
-            bufs = [torch.zeros(s.shape, device=dev) for s in specs]
+            xs = [None] * len(specs)
             errs = {}
             g = [torch.from_numpy(x).to(dev) for x in grads]
         ts = []
@@ -568,17 +567,15 @@ def dropin_timing(specs, a, dev, steps=5):
                     trip = comp.round_trip([delta], CompressionContext(0, i, t), comm)
                     errs[i] = delta - trip.locals[0]
                     upd = trip.aggregated.reshape(sp.shape)
-                bufs[i] *= 0.9
-                bufs[i] += upd
-                xs[i] -= 0.01 * (upd + bufs[i])
+                xs[i] = upd  # the aggregated update the optimizer would apply (optimizer.py:130)
             if mode == "torch":
                 comp.check()
             torch.cuda.synchronize(dev)
             if t > 0:
                 ts.append(time.perf_counter() - t0)
         out[mode + "_ms"] = round(1e3 * statistics.median(ts), 3)
-    out["note"] = ("optimizer.py:110-134 loop over the catalog calling PowerSGD.round_trip per matrix "
-                   "(numpy: float64 host arrays as the reference; torch: CUDA tensors); wall clock")
+    out["note"] = ("optimizer.py:110-129 loop over the catalog calling PowerSGD.round_trip per matrix, "
+                   "as the reference arm (numpy: float64 host arrays; torch: CUDA tensors); wall clock")
     return out
 
 
