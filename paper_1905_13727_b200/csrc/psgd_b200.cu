@@ -1750,7 +1750,7 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
 //                   (compressors.py:376-378, optimizer.py:124-127)
 constexpr int KR_THREADS = 256;
 constexpr int KR_QROWS = 128;
-constexpr int KR_EROWS = 64;
+constexpr int KR_EROWS = 32;  // measured: 32 rows per EF item (LSTM 226 -> 220 us vs 64; sweeps/swer*.txt)
 constexpr int KR_GROUPS = 16;
 struct RowsItem {
   int mat, r0, nrows, pad;
@@ -2811,7 +2811,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
         pl->kr_gpart_elems += (long long)KR_GROUPS * mr;
         pl->kr_counters += xb;
         gp.xblocks = std::max(gp.xblocks, xb);
-        for (int r0 = 0; r0 < md.n; r0 += KR_EROWS) pl->kr_e.push_back({mi, r0, std::min(KR_EROWS, md.n - r0), 0, 0});
+        static const int erows = getenv("PSGD_KR_EROWS") ? atoi(getenv("PSGD_KR_EROWS")) : KR_EROWS;
+        for (int r0 = 0; r0 < md.n; r0 += erows) pl->kr_e.push_back({mi, r0, std::min(erows, md.n - r0), 0, 0});
       }
       gp.qend = (int)pl->kr_q.size();
       gp.eend = (int)pl->kr_e.size();
