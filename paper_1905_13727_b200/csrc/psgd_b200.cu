@@ -83,10 +83,10 @@ struct MatDev {
   long long flat_off, p_off, q_off, repl_off;
   int n, m, r, tall;
   int lg1, qs;  // lg1: log2 lanes per row in K1 (2..9); qs: Q staged in smem by K1
+                // (tall == 2: a tall matrix whose EF pass is k4_rows)
   int nck, pipe;  // nck: K1 chunks of the matrix; pipe: q / EF / M-hat by k3_pipe (n <= 512, r <= 8)
   int qld, rcols;  // Q is column-major: element (j, k) at q_off + k * qld + j, qld = align4(m);
                   // rcols: columns per attempt of the replacement table at repl_off (shared by equal n)
-  int rows2, pad1;  // rows2: tall matrix on the row-oriented q / EF kernels (even m <= 1024, r <= 4)
 };
 
 struct SgdArgs {   // fused heavy-ball update (optimizer.py:131-134); x == nullptr: off
@@ -1739,26 +1739,17 @@ __global__ void __launch_bounds__(K3P_CT + 32, 1)
 }
 
 // ============================================================================= tall, row-oriented
-// Tall matrices with an even m <= 1024 and r <= 4 (LSTM: 28869 x 650, 2600 x 650):
-// a CTA streams whole rows (contiguous memory, 8-byte pieces — even m keeps every row
-// 8-byte aligned), thread t owning the column pairs t and t + 256, so its q (or
-// q-bar) values stay in registers for all rows it touches.
-//   k3_rows:        q partial of a 128-row block for all m columns (compressors.py:339)
-//   k3_rows_reduce: partials summed in a fixed two-level order (16 groups of
-//                   consecutive blocks, then the groups in order) -> q / Q store
-//   k4_rows:        e = delta - P-hat q^T (and M-hat at W = 1) of a 64-row block
-//                   (compressors.py:376-378, optimizer.py:124-127)
+// k4_rows — the EF pass of tall matrices with m = 2 (mod 4), m <= 1024 and r <= 4
+// (LSTM: 28869 x 650, 2600 x 650): e = delta - P-hat q^T (and M-hat at W = 1) of a
+// 32-row block (compressors.py:376-378, optimizer.py:124-127).  A CTA streams whole
+// rows (contiguous memory, 8-byte pieces — even m keeps every row 8-byte aligned),
+// thread t owning the column pairs t and t + 256, so its q values stay in registers.
+// (A row-oriented q pass with an ordered two-level partial reduction measured slower
+// than k3_slab — 65-70 + 10 us vs 51 us on LSTM — and is not kept.)
 constexpr int KR_THREADS = 256;
-constexpr int KR_QROWS = 128;
 constexpr int KR_EROWS = 32;  // measured: 32 rows per EF item (LSTM 226 -> 220 us vs 64; sweeps/swer*.txt)
-constexpr int KR_GROUPS = 16;
 struct RowsItem {
   int mat, r0, nrows, pad;
-  long long poff;  // q items: float offset of the item's partial (r x m, like Q)
-};
-struct RowsMat {  // per rows matrix: its partials and reduction scratch
-  int mat, nitems, cbase, pad;  // cbase: first reduction counter of the matrix
-  long long pbase, gbase;       // float offsets of its first partial and of its group sums
 };
 
 template <int R>
@@ -1773,107 +1764,6 @@ __device__ __forceinline__ void kr_prow(const float* __restrict__ Phat, const Ma
   }
 #pragma unroll
   for (int k = 0; k < R; ++k) p[k] = k < md.r ? __ldg(pr + k) : 0.f;
-}
-
-template <int R>
-__global__ void __launch_bounds__(KR_THREADS)
-    k3_rows(const MatDev* __restrict__ mats, const RowsItem* __restrict__ items, const float* __restrict__ work,
-            const float* __restrict__ Phat, float* __restrict__ part, const int* __restrict__ status) {
-  pdl_wait();
-  pdl_trigger();
-  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
-  const RowsItem it = items[blockIdx.x];
-  const MatDev md = mats[it.mat];
-  const int m = md.m, r = md.r, np = m >> 1, t = threadIdx.x;
-  const bool ok0 = t < np, ok1 = t + KR_THREADS < np;
-  float acc[2][2][R];
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int k = 0; k < R; ++k) acc[h][c][k] = 0.f;
-  const float* __restrict__ base = work + md.flat_off + (long long)it.r0 * m;
-  for (int i0 = 0; i0 < it.nrows; i0 += 8) {
-    float2 d0[8], d1[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {  // 8 rows of loads in flight
-      const bool in = i0 + u < it.nrows;
-      const float2* row = reinterpret_cast<const float2*>(base + (long long)(i0 + u) * m);
-      d0[u] = (in && ok0) ? __ldcs(row + t) : make_float2(0.f, 0.f);
-      d1[u] = (in && ok1) ? __ldcs(row + t + KR_THREADS) : make_float2(0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (i0 + u >= it.nrows) break;
-      float p[R];
-      kr_prow<R>(Phat, md, it.r0 + i0 + u, p);
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        acc[0][0][k] = fmaf(d0[u].x, p[k], acc[0][0][k]);
-        acc[0][1][k] = fmaf(d0[u].y, p[k], acc[0][1][k]);
-        acc[1][0][k] = fmaf(d1[u].x, p[k], acc[1][0][k]);
-        acc[1][1][k] = fmaf(d1[u].y, p[k], acc[1][1][k]);
-      }
-    }
-  }
-  float* pt = part + it.poff;  // [k][column], like Q
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    if (!(h == 0 ? ok0 : ok1)) continue;
-    const int c = 2 * (t + h * KR_THREADS);
-#pragma unroll
-    for (int k = 0; k < R; ++k)
-      if (k < r) *reinterpret_cast<float2*>(pt + (long long)k * m + c) = make_float2(acc[h][0][k], acc[h][1][k]);
-  }
-}
-
-// grid (ceil(r m / 256), KR_GROUPS, rows matrices): block (x, g) sums the partials of item
-// group g for 256 outputs; the last group block of x sums the KR_GROUPS group sums in order
-__global__ void __launch_bounds__(KR_THREADS)
-    k3_rows_reduce(const MatDev* __restrict__ mats, const RowsMat* __restrict__ rmats, const float* __restrict__ part,
-                   float* __restrict__ gpart, int* __restrict__ counters, float* __restrict__ qout,
-                   const int* __restrict__ status) {
-  pdl_wait();
-  pdl_trigger();
-  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
-  __shared__ int s_last;
-  const RowsMat rm = rmats[blockIdx.z];
-  const MatDev md = mats[rm.mat];
-  const int mr = md.m * md.r;
-  const int o = blockIdx.x * KR_THREADS + threadIdx.x;
-  if ((int)blockIdx.x * KR_THREADS >= mr) return;  // (block-uniform)
-  const int g = blockIdx.y;
-  const int S = (rm.nitems + KR_GROUPS - 1) / KR_GROUPS;
-  const int i0 = g * S, i1 = min(rm.nitems, i0 + S);
-  float s2 = 0.f;
-  if (o < mr) {
-    const float* src = part + rm.pbase + o;
-    int i = i0;
-    for (; i + 8 <= i1; i += 8) {  // 8 loads in flight, summed in item order
-      float y[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) y[u] = __ldcg(src + (long long)(i + u) * mr);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s2 += y[u];
-    }
-    for (; i < i1; ++i) s2 += __ldcg(src + (long long)i * mr);
-    gpart[rm.gbase + (long long)g * mr + o] = s2;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(counters + rm.cbase + blockIdx.x, 1) == KR_GROUPS - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  if (o < mr) {
-    float q = 0.f;
-#pragma unroll
-    for (int gg = 0; gg < KR_GROUPS; ++gg) q += __ldcg(gpart + rm.gbase + (long long)gg * mr + o);
-    const int k = o / md.m, c = o - k * md.m;
-    qout[md.q_off + (long long)k * md.qld + c] = q;
-  }
-  if (threadIdx.x == 0) counters[rm.cbase + blockIdx.x] = 0;
 }
 
 template <int R>
@@ -2554,18 +2444,12 @@ struct psgd_plan {
   mutable K3Maps maps{};
 
   // tall path
-  struct RowsGroup {  // one launch per R: q items, EF items, matrices
-    int R, qbeg, qend, ebeg, eend, mbeg, mend, xblocks;
+  struct RowsGroup {  // one k4_rows launch per R
+    int R, ebeg, eend;
   };
-  std::vector<RowsItem> kr_q, kr_e;
-  std::vector<RowsMat> kr_mats;
+  std::vector<RowsItem> kr_e;
   std::vector<RowsGroup> gkr;
-  long long kr_part_elems = 0, kr_gpart_elems = 0;
-  int kr_counters = 0;
-  RowsItem *d_kr_q = nullptr, *d_kr_e = nullptr;
-  RowsMat* d_kr_mats = nullptr;
-  float *d_kr_part = nullptr, *d_kr_gpart = nullptr;
-  int* d_kr_cnt = nullptr;
+  RowsItem* d_kr_e = nullptr;
   std::vector<int> tall_list, all_list;
   std::vector<RowItem> k4, k5;
   std::vector<Group> g4, g5;
@@ -2624,11 +2508,6 @@ int lanes_log2_for(int m, int max_lg) {
   return lg;
 }
 
-bool kr_q_on() {  // the row-oriented q pass (k3_rows) measured slower than k3_slab (LSTM 70 + 10 vs 51 us)
-  static const bool on = getenv("PSGD_ROWS2_Q") && getenv("PSGD_ROWS2_Q")[0] == '1';
-  return on;
-}
-
 bool k3_tileable(const MatDev& md) {
   static const bool off = getenv("PSGD_K3_TILE") && getenv("PSGD_K3_TILE")[0] == '0';
   return !off && md.tall && md.m % 4 == 0 && md.flat_off % 4 == 0 && md.m >= 128;
@@ -2641,7 +2520,7 @@ bool k4_tileable(const MatDev& md) {
 
 bool k4_tileable2(const MatDev& md) {  // two alignment classes (k4_tile2)
   static const bool off = getenv("PSGD_K4_TILE2") && getenv("PSGD_K4_TILE2")[0] == '0';
-  return !off && md.tall && !md.rows2 && md.m % 4 == 2 && md.flat_off % 4 == 0 && md.m >= 128;
+  return !off && md.tall == 1 && md.m % 4 == 2 && md.flat_off % 4 == 0 && md.m >= 128;
 }
 
 void build_tile_items(const std::vector<MatDev>& mats, std::vector<TileItem>& items, std::vector<Group>& groups) {
@@ -2671,7 +2550,7 @@ void build_row_items(const std::vector<MatDev>& mats, bool tall_only, std::vecto
     Group gp{r, (int)items.size(), 0, 0};
     for (int mi = 0; mi < (int)mats.size(); ++mi) {
       const MatDev& md = mats[mi];
-      if (md.r != r || (tall_only && (!md.tall || md.rows2))) continue;
+      if (md.r != r || (tall_only && md.tall != 1)) continue;
       if (tall_only && (k4_tileable(md) || k4_tileable2(md))) continue;  // K4 column tiles instead
       const int lg = lanes_log2_for(md.m, 5);
       const int rpp = 32 >> lg;
@@ -2791,33 +2670,19 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     pl->mats.push_back(md);
   }
   pl->flat_elems = std::max(4LL, fo);
-  {  // row-oriented q / EF kernels for tall matrices with m = 2 (mod 4), m <= 1024, r <= 4 (LSTM)
+  {  // the row-oriented EF pass (k4_rows) for tall matrices with m = 2 (mod 4), m <= 1024, r <= 4 (LSTM)
     static const bool off = getenv("PSGD_ROWS2") && getenv("PSGD_ROWS2")[0] == '0';
     for (auto& md : pl->mats)
-      md.rows2 = (!off && md.tall && md.m % 4 == 2 && md.m <= 4 * KR_THREADS && md.r <= 4) ? 1 : 0;
+      if (!off && md.tall && md.m % 4 == 2 && md.m <= 4 * KR_THREADS && md.r <= 4) md.tall = 2;
     for (int R : {1, 2, 4}) {
-      psgd_plan::RowsGroup gp{R, (int)pl->kr_q.size(), 0, (int)pl->kr_e.size(), 0, (int)pl->kr_mats.size(), 0, 0};
+      psgd_plan::RowsGroup gp{R, (int)pl->kr_e.size(), 0};
       for (int mi = 0; mi < nmat; ++mi) {
         const MatDev& md = pl->mats[mi];
-        if (!md.rows2 || rmax_of(md.r) != R) continue;
-        const long long mr = (long long)md.m * md.r;
-        const int nq = (md.n + KR_QROWS - 1) / KR_QROWS;
-        const int xb = (int)((mr + KR_THREADS - 1) / KR_THREADS);
-        pl->kr_mats.push_back({mi, nq, pl->kr_counters, 0, pl->kr_part_elems, pl->kr_gpart_elems});
-        for (int q = 0; q < nq; ++q)
-          pl->kr_q.push_back({mi, q * KR_QROWS, std::min(KR_QROWS, md.n - q * KR_QROWS), 0,
-                              pl->kr_part_elems + (long long)q * mr});
-        pl->kr_part_elems += (long long)nq * mr;
-        pl->kr_gpart_elems += (long long)KR_GROUPS * mr;
-        pl->kr_counters += xb;
-        gp.xblocks = std::max(gp.xblocks, xb);
-        static const int erows = getenv("PSGD_KR_EROWS") ? atoi(getenv("PSGD_KR_EROWS")) : KR_EROWS;
-        for (int r0 = 0; r0 < md.n; r0 += erows) pl->kr_e.push_back({mi, r0, std::min(erows, md.n - r0), 0, 0});
+        if (md.tall != 2 || rmax_of(md.r) != R) continue;
+        for (int r0 = 0; r0 < md.n; r0 += KR_EROWS) pl->kr_e.push_back({mi, r0, std::min(KR_EROWS, md.n - r0), 0});
       }
-      gp.qend = (int)pl->kr_q.size();
       gp.eend = (int)pl->kr_e.size();
-      gp.mend = (int)pl->kr_mats.size();
-      if (gp.mend > gp.mbeg) pl->gkr.push_back(gp);
+      if (gp.eend > gp.ebeg) pl->gkr.push_back(gp);
     }
   }
   {  // replacement columns depend on (n, j, attempt) only (linalg.py:54-58): one table per distinct n
@@ -2979,7 +2844,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       Group gp{r, (int)pl->k3.size(), 0, 0, tall};
       for (int mi = 0; mi < nmat; ++mi) {
         const MatDev& md = pl->mats[mi];
-        if (md.r != r || md.pipe || (md.rows2 && kr_q_on())) continue;
+        if (md.r != r || md.pipe) continue;
         const K3Cfg cf = k3_tall_config(md.n, md.m, r);
         if ((cf.nchunks > 1) != (tall == 1)) continue;
         if (tall && k3_tileable(md)) continue;  // K3 column tiles instead
@@ -3154,12 +3019,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_k3tp = take((size_t)std::max(1LL, pl->k3t_part_elems) * sizeof(float));
   const size_t o_k5 = take(pl->k5.size() * sizeof(RowItem));
   const size_t o_pipe = take(pl->pipe_items.size() * sizeof(PipeItem));
-  const size_t o_krq = take(pl->kr_q.size() * sizeof(RowsItem));
   const size_t o_kre = take(pl->kr_e.size() * sizeof(RowsItem));
-  const size_t o_krm = take(pl->kr_mats.size() * sizeof(RowsMat));
-  const size_t o_krp = take((size_t)std::max(1LL, pl->kr_part_elems) * sizeof(float));
-  const size_t o_krg = take((size_t)std::max(1LL, pl->kr_gpart_elems) * sizeof(float));
-  const size_t o_krc = take((size_t)std::max(1, pl->kr_counters) * sizeof(int));
   const size_t o_pctr = take(2 * sizeof(int));
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
   const size_t o_wsq = take((size_t)std::max(1LL, pl->wsq_elems) * sizeof(float));
@@ -3206,12 +3066,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_k3t_part = reinterpret_cast<float*>(b + o_k3tp);
   pl->d_k5 = reinterpret_cast<RowItem*>(b + o_k5);
   pl->d_pipe_items = reinterpret_cast<PipeItem*>(b + o_pipe);
-  pl->d_kr_q = reinterpret_cast<RowsItem*>(b + o_krq);
   pl->d_kr_e = reinterpret_cast<RowsItem*>(b + o_kre);
-  pl->d_kr_mats = reinterpret_cast<RowsMat*>(b + o_krm);
-  pl->d_kr_part = reinterpret_cast<float*>(b + o_krp);
-  pl->d_kr_gpart = reinterpret_cast<float*>(b + o_krg);
-  pl->d_kr_cnt = reinterpret_cast<int*>(b + o_krc);
   pl->d_pipe_ctr = reinterpret_cast<int*>(b + o_pctr);
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
   pl->d_wsq = reinterpret_cast<float*>(b + o_wsq);
@@ -3251,10 +3106,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_k3t_off, pl->k3t_off.data(), pl->k3t_off.size() * sizeof(long long));
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = up(pl->d_pipe_items, pl->pipe_items.data(), pl->pipe_items.size() * sizeof(PipeItem));
-  if (ce == cudaSuccess) ce = up(pl->d_kr_q, pl->kr_q.data(), pl->kr_q.size() * sizeof(RowsItem));
   if (ce == cudaSuccess) ce = up(pl->d_kr_e, pl->kr_e.data(), pl->kr_e.size() * sizeof(RowsItem));
-  if (ce == cudaSuccess) ce = up(pl->d_kr_mats, pl->kr_mats.data(), pl->kr_mats.size() * sizeof(RowsMat));
-  if (ce == cudaSuccess) ce = cudaMemset(pl->d_kr_cnt, 0, (size_t)std::max(1, pl->kr_counters) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_pipe_ctr, 0, 2 * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_split_cnt, 0, std::max<size_t>(16, pl->splits.size() * sizeof(int)));
@@ -3308,7 +3160,7 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
     k2_in_q_ef = ((small3 || (pl->nbias > 0 && !bias_k3 && !bias_pipe)) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 3);
     (void)bias_in_k3;
   }
-  o->launches_q_ef = k2_in_q_ef + (pl->pipe_items.empty() ? 0 : 1) + (kr_q_on() ? 3 : 1) * (int)pl->gkr.size() + nonempty(pl->g3) +
+  o->launches_q_ef = k2_in_q_ef + (pl->pipe_items.empty() ? 0 : 1) + (int)pl->gkr.size() + nonempty(pl->g3) +
                      nonempty(pl->g4) + nonempty(pl->g4t) +
                      nonempty(pl->g4t2) +
                      (pl->k3t.empty() ? 0 : 2);
@@ -3331,7 +3183,7 @@ int psgd_plan_matrix(const psgd_plan* pl, int32_t i, psgd_matrix_info* o) {
   o->n = md.n;
   o->m = md.m;
   o->r_eff = md.r;
-  o->tall = md.tall;
+  o->tall = md.tall ? 1 : 0;
   o->q_ld = md.qld;
   return PSGD_OK;
 }
@@ -3530,40 +3382,22 @@ int launch_pipe(const psgd_plan* pl, float* work, const float* phat, float* qout
 
 template <int R>
 int launch_rows_r(const psgd_plan* pl, const psgd_plan::RowsGroup& gp, float* work, float* e, const float* phat,
-                  float* qout, const int* status, cudaStream_t st, int phase) {
-  if (phase == 0) {
-    PSGD_CUDA_CHECK(launch_ex(k3_rows<R>, gp.qend - gp.qbeg, KR_THREADS, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
-                              (const RowsItem*)(pl->d_kr_q + gp.qbeg), (const float*)work, phat, pl->d_kr_part,
-                              status));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)gp.xblocks, KR_GROUPS, (unsigned)(gp.mend - gp.mbeg));
-    cfg.blockDim = dim3(KR_THREADS);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = PSGD_PDL ? 1 : 0;
-    PSGD_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k3_rows_reduce, (const MatDev*)pl->d_mats,
-                                       (const RowsMat*)(pl->d_kr_mats + gp.mbeg), (const float*)pl->d_kr_part,
-                                       pl->d_kr_gpart, pl->d_kr_cnt, qout, status));
-  } else {
-    PSGD_CUDA_CHECK(launch_ex(k4_rows<R>, gp.eend - gp.ebeg, KR_THREADS, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
-                              (const RowsItem*)(pl->d_kr_e + gp.ebeg), work, e, phat, (const float*)qout,
-                              pl->world == 1 ? 1 : 0, status));
-  }
+                  const float* q, const int* status, cudaStream_t st) {
+  PSGD_CUDA_CHECK(launch_ex(k4_rows<R>, gp.eend - gp.ebeg, KR_THREADS, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
+                            (const RowsItem*)(pl->d_kr_e + gp.ebeg), work, e, phat, q, pl->world == 1 ? 1 : 0,
+                            status));
   return PSGD_OK;
 }
 
-// phase 0: q of the rows matrices (partials + ordered reduction); phase 1: their EF pass
-int launch_rows(const psgd_plan* pl, float* work, float* e, const float* phat, float* qout, const int* status,
-                cudaStream_t st, int phase) {
+// the EF pass of the k4_rows matrices
+int launch_rows(const psgd_plan* pl, float* work, float* e, const float* phat, const float* q, const int* status,
+                cudaStream_t st) {
   for (const auto& gp : pl->gkr) {
     int rc;
     switch (gp.R) {
-      case 1: rc = launch_rows_r<1>(pl, gp, work, e, phat, qout, status, st, phase); break;
-      case 2: rc = launch_rows_r<2>(pl, gp, work, e, phat, qout, status, st, phase); break;
-      default: rc = launch_rows_r<4>(pl, gp, work, e, phat, qout, status, st, phase); break;
+      case 1: rc = launch_rows_r<1>(pl, gp, work, e, phat, q, status, st); break;
+      case 2: rc = launch_rows_r<2>(pl, gp, work, e, phat, q, status, st); break;
+      default: rc = launch_rows_r<4>(pl, gp, work, e, phat, q, status, st); break;
     }
     if (rc) return rc;
   }
@@ -3681,10 +3515,6 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
           (long long)pl->nbias, pl->nflags, (int)divisor};
   rc = launch_pipe(pl, work, p_hat, q_out, e, (int*)status, st, sg, gs);  // K3 pipeline (n <= 512)
   if (rc) return rc;
-  if (kr_q_on()) {
-    rc = launch_rows(pl, work, e, p_hat, q_out, (const int*)status, st, 0);  // tall, m = 2 mod 4: q
-    if (rc) return rc;
-  }
   for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab (after K2: delta is final)
     rc = dispatch_r<RunK3>(gp.r, pl, gp, work, p, (int)divisor, repl, p_hat, q_out, e, bias_out,
                            bias_done ? 0LL : (long long)pl->nbias, (int*)status, st);
@@ -3718,7 +3548,7 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
                                          (const int*)status));
     }
   }
-  rc = launch_rows(pl, work, e, p_hat, q_out, (const int*)status, st, 1);  // tall, m = 2 mod 4: EF pass
+  rc = launch_rows(pl, work, e, p_hat, q_out, (const int*)status, st);  // tall, m = 2 mod 4: EF pass
   if (rc) return rc;
   for (const Group& gp : pl->g4) {
     rc = dispatch_r<RunK4>(gp.r, pl, (const RowItem*)pl->d_k4, gp, work, e, (const float*)p_hat,
