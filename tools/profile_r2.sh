@@ -19,6 +19,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     python tools/prof_step.py --workload stress --rank 8 --steps 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k1_ef_p|k2_gs|k3_pipe" -s 2 -c 2 \
     -o $O/resnet18_full python tools/prof_step.py --steps 3 > $O/ncu_resnet.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k1_ef_p|k2_gram|k2_apply|k3_slab|k4_tile2" -s 6 -c 6 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k1_ef_p|k2_gram|k2_apply|k3_slab|k4_tile2|k4_rows" -s 6 -c 6 \
     -o $O/lstm_full python tools/prof_step.py --workload lstm --rank 4 --steps 3 > $O/ncu_lstm.log 2>&1
 echo done
