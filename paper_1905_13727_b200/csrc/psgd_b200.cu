@@ -494,6 +494,15 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
   }
 }
 
+#ifdef PSGD_K1_TIMES
+__device__ unsigned long long g_k1_times[3 * 1024];  // per CTA: start, end, chunks (diagnostic builds only)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int RM>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     k1_ef_p(const MatDev* __restrict__ mats, const Chunk1* __restrict__ chunks,
@@ -514,6 +523,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   int* sflag = reinterpret_cast<int*>(qempty + 2);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int cb = cta_beg[blockIdx.x], ce = cta_beg[blockIdx.x + 1];
+#ifdef PSGD_K1_TIMES
+  if (t == 0) {
+    g_k1_times[3 * blockIdx.x] = gtimer();
+    g_k1_times[3 * blockIdx.x + 2] = ce - cb;
+  }
+#endif
   if (t == 0) {
     for (int s = 0; s < L.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -624,6 +639,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if (bad) atomicOr(sflag, 1);
   bar_consumers();
   if (t == 0) P[flag_off + blockIdx.x] = *sflag ? 1.f : 0.f;  // rides in the P all-reduce (K2 reads it)
+#ifdef PSGD_K1_TIMES
+  if (t == 0) g_k1_times[3 * blockIdx.x + 1] = gtimer();
+#endif
 }
 
 // ============================================================================= K2
@@ -2618,6 +2636,13 @@ bool opt_fusable(const psgd_plan* pl);
 extern "C" {
 
 int32_t psgd_version(void) { return 3; }
+
+#ifdef PSGD_K1_TIMES
+int psgd_debug_k1_times(unsigned long long* out, int n) {  // diagnostic builds (tools/k1_tail.py) only
+  return cudaMemcpyFromSymbol(out, g_k1_times, sizeof(unsigned long long) * 3 * std::min(n, 1024)) == cudaSuccess
+             ? 0 : -2;
+}
+#endif
 
 const char* psgd_last_error(void) { return g_last_error.c_str(); }
 

@@ -1,4 +1,6 @@
-"""Per-CTA start/end of K1 (diagnostic build with -DPSGD_K1_TIMES): the tail K1 leaves."""
+"""Per-CTA start/end of K1: the tail K1 leaves.  Needs the diagnostic build
+    python -c "from paper_1905_13727_b200 import build as b; b.build(out='paper_1905_13727_b200/libpsgd_v_times.so', defines=['PSGD_K1_TIMES'])"
+"""
 import ctypes
 import os
 import sys
