@@ -1842,6 +1842,223 @@ __global__ void __launch_bounds__(KR_THREADS)
   }
 }
 
+// ============================================================================= tall q pass, row blocks
+// k3_rq — q_w = delta^T P-hat (compressors.py:339) of the k4_rows matrices (tall,
+// m = 2 mod 4, m <= 1024).  A block of whole rows is one contiguous span of delta,
+// so a persistent CTA (1 per SM, 16 consumer warps + 1 producer warp) streams its
+// static, contiguous range of row blocks with 1-D bulk TMA (cp.async.bulk) into a
+// 4-stage smem ring, the P-hat rows of each block beside it.  Thread (rg, tp) owns
+// the column pair tp of the rows rg, rg + RGn, ... and keeps its 2 x r partial q in
+// registers; after its last block of a matrix the CTA writes one partial (fixed
+// order over the row groups) into the matrix's slot list.  k3_rq_reduce then sums
+// the slots in row order (deterministic).  Delta is final when the kernel starts
+// (K2 ran after K1), so the ring is filled before griddepcontrol.wait; P-hat is
+// fetched after it.  The range is walked backwards: the last rows K1 wrote (still
+// in L2) are read first.
+constexpr int RQ_STAGES = 4;
+constexpr int RQ_STAGE_FLOATS = 12288;  // 48 KB of delta per stage
+constexpr int RQ_PST = 512;             // P-hat floats per stage
+struct RqChunk {
+  long long off;   // flat offset of the block's first element
+  long long slot;  // float offset of this CTA's partial of `mat` in the slot workspace
+  int mat, row0, nrows, flush;  // flush: the CTA's last block of `mat` in traversal order
+};
+struct RqLayout {
+  int off_p, off_red, off_bar, total;
+};
+
+template <int R>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    k3_rq(const MatDev* __restrict__ mats, const RqChunk* __restrict__ chunks, const int* __restrict__ cta_beg,
+          RqLayout L, const float* __restrict__ work, const float* __restrict__ Phat, float* __restrict__ wsq,
+          const float* __restrict__ P, float* __restrict__ bias_out, long long nbias, long long bias_off,
+          int divisor, int rev, int dpol, int* status) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* sdb = reinterpret_cast<float*>(smem_raw);
+  float* spb = reinterpret_cast<float*>(smem_raw + L.off_p);
+  float* red = reinterpret_cast<float*>(smem_raw + L.off_red);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
+  uint64_t* empty = full + RQ_STAGES;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int cb = cta_beg[blockIdx.x], ce = cta_beg[blockIdx.x + 1], nck = ce - cb;
+  if (t == 0) {
+    for (int s = 0; s < RQ_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_trigger();  // the slot reduction may stage in; it waits for this grid
+  auto chunk_at = [&](int j) { return chunks[rev ? ce - 1 - j : cb + j]; };
+
+  if (warp == kConsWarps) {  // ---------------- producer
+    if (lane == 0) {
+      const uint64_t pol = dpol == 0 ? pol_evict_first() : pol_evict_last();
+      const uint64_t polp = pol_evict_last();
+      auto p_span = [&](const RqChunk& ch, const MatDev& md, long long& a4) {
+        const long long pa = md.p_off + (long long)ch.row0 * md.r;
+        a4 = pa & ~3LL;
+        return (uint32_t)((((pa + (long long)ch.nrows * md.r + 3) & ~3LL) - a4) * 4);
+      };
+      const int pre = min(nck, RQ_STAGES);
+      for (int j = 0; j < nck; ++j) {
+        const int s = j % RQ_STAGES;
+        const uint32_t ph = (j / RQ_STAGES) & 1;
+        const RqChunk ch = chunk_at(j);
+        const MatDev md = mats[ch.mat];
+        mbar_wait(&empty[s], ph ^ 1);
+        const long long a4 = ch.off & ~3LL;
+        const long long b4 = (ch.off + (long long)ch.nrows * md.m + 3) & ~3LL;
+        const uint32_t bytes = (uint32_t)((b4 - a4) * 4);
+        long long pa4;
+        const uint32_t pbytes = p_span(ch, md, pa4);
+        mbar_expect_tx(&full[s], bytes + pbytes);
+        tma_load(sdb + s * RQ_STAGE_FLOATS, work + a4, bytes, &full[s], pol);
+        if (j >= pre) tma_load(spb + s * RQ_PST, Phat + pa4, pbytes, &full[s], polp);
+        if (j == pre - 1) {  // the ring is full of delta: wait for K2's P-hat, then its copies
+          pdl_wait();
+          for (int j2 = 0; j2 < pre; ++j2) {
+            const RqChunk c2 = chunk_at(j2);
+            const MatDev m2 = mats[c2.mat];
+            long long q4;
+            const uint32_t qb = p_span(c2, m2, q4);
+            tma_load(spb + j2 * RQ_PST, Phat + q4, qb, &full[j2], polp);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  pdl_wait();
+  const bool bad = (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) != 0;  // mutate nothing
+  if (!bad && nbias > 0) {  // bias mean (optimizer.py:111-113), when this launch is the one to write it
+    bool bb = false;
+    for (long long x = (long long)blockIdx.x * kCons + t; x < nbias; x += (long long)gridDim.x * kCons) {
+      const float v = P[bias_off + x];
+      bb |= !finite1(v);
+      bias_out[x] = divisor == 1 ? v : v / (float)divisor;
+    }
+    if (bb) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+  }
+  float acc[2][R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.f;
+  for (int j = 0; j < nck; ++j) {
+    const int s = j % RQ_STAGES;
+    const uint32_t ph = (j / RQ_STAGES) & 1;
+    const RqChunk ch = chunk_at(j);
+    const MatDev md = mats[ch.mat];
+    const int m = md.m, r = md.r, np = m >> 1;
+    const int TPR = min(kCons, (np + 31) & ~31), RGn = kCons / TPR;
+    const int rg = t / TPR, tp = t - rg * TPR;
+    const bool act = rg < RGn && tp < np;
+    mbar_wait(&full[s], ph);
+    if (!bad) {
+      const float* sd = sdb + s * RQ_STAGE_FLOATS + (int)(ch.off - (ch.off & ~3LL));
+      const long long pa = md.p_off + (long long)ch.row0 * r;
+      const float* sp = spb + s * RQ_PST + (int)(pa - (pa & ~3LL));
+      if (act) {
+        const float2* d2 = reinterpret_cast<const float2*>(sd) + tp;
+        int li = rg;
+#pragma unroll 2
+        for (; li < ch.nrows; li += RGn) {
+          const float2 d = d2[(li * m) >> 1];
+          const float* pr = sp + li * r;
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const float pk = k < r ? pr[k] : 0.f;
+            acc[0][k] = fmaf(d.x, pk, acc[0][k]);
+            acc[1][k] = fmaf(d.y, pk, acc[1][k]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (ch.flush) {  // the CTA's partial of this matrix: slot (k, c) at slot + k * m + c
+      if (!bad) {
+        float* slot = wsq + ch.slot;
+        if (RGn == 1) {
+          if (act)
+#pragma unroll
+            for (int k = 0; k < R; ++k)
+              if (k < r) *reinterpret_cast<float2*>(slot + (long long)k * m + 2 * tp) = make_float2(acc[0][k], acc[1][k]);
+        } else {  // fixed order over the row groups
+          if (act)
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              red[((rg * R + k) * np + tp) * 2] = acc[0][k];
+              red[((rg * R + k) * np + tp) * 2 + 1] = acc[1][k];
+            }
+          bar_consumers();
+          for (int o = t; o < np * r; o += kCons) {
+            const int k = o / np, c2 = o - k * np;
+            float sx = 0.f, sy = 0.f;
+            for (int g2 = 0; g2 < RGn; ++g2) {
+              sx += red[((g2 * R + k) * np + c2) * 2];
+              sy += red[((g2 * R + k) * np + c2) * 2 + 1];
+            }
+            *reinterpret_cast<float2*>(slot + (long long)k * m + 2 * c2) = make_float2(sx, sy);
+          }
+          bar_consumers();
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.f;
+    }
+  }
+}
+
+struct RqMat {
+  long long slot0;  // float offset of slot 0 in the workspace (slots of m x r floats, row order)
+  int mat, nslots;
+};
+
+// q_w of the k3_rq matrices: a CTA owns 32 consecutive outputs; its 8 warps sum the
+// slots g, g + 8, g + 16, ... (all loads in flight), then the 8 group sums are added
+// in group order (fixed order: deterministic)
+constexpr int RQR_GROUPS = 8;
+__global__ void __launch_bounds__(32 * RQR_GROUPS)
+    k3_rq_reduce(const MatDev* __restrict__ mats, const RqMat* __restrict__ rqm, const int2* __restrict__ blocks,
+                 const float* __restrict__ wsq, float* __restrict__ qout, const int* __restrict__ status) {
+  __shared__ float part[RQR_GROUPS][32];
+  pdl_wait();
+  pdl_trigger();
+  if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
+  const int2 b = blocks[blockIdx.x];
+  const RqMat rm = rqm[b.x];
+  const MatDev md = mats[rm.mat];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int o = b.y + lane;
+  const long long mr = (long long)md.m * md.r;
+  float s = 0.f;
+  if (o < mr) {
+    const float* src = wsq + rm.slot0 + o;
+    for (int j0 = g; j0 < rm.nslots; j0 += 16 * RQR_GROUPS) {
+      float y[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int j = j0 + u * RQR_GROUPS;
+        y[u] = j < rm.nslots ? __ldcg(src + (long long)j * mr) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += y[u];
+    }
+  }
+  part[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && o < mr) {
+    float t = 0.f;
+#pragma unroll
+    for (int g2 = 0; g2 < RQR_GROUPS; ++g2) t += part[g2][lane];
+    const int k = o / md.m, c = o - k * md.m;
+    qout[md.q_off + (long long)k * md.qld + c] = t;
+  }
+}
+
 // K4 / K5 row streaming.  MODE 0 (K4): e = delta - P-hat q^T (+ M-hat in place
 // when write_mhat).  MODE 1 (K5): M-hat = P-hat (q / div)^T; items with
 // row0 == 0 store Q-bar = q / div.
@@ -2468,6 +2685,20 @@ struct psgd_plan {
   std::vector<RowsItem> kr_e;
   std::vector<RowsGroup> gkr;
   RowsItem* d_kr_e = nullptr;
+  // k3_rq (q pass of the k4_rows matrices): row blocks, CTA ranges, slot lists, reduce blocks
+  std::vector<RqChunk> rq;
+  std::vector<int> rq_beg;
+  std::vector<RqMat> rq_mats;
+  std::vector<int2> rq_blocks;
+  RqLayout rql{};
+  int rq_rmax = 1, rq_rev = 1;
+  std::vector<char> rq_on;  // per matrix: q pass by k3_rq
+  long long rq_ws_elems = 0;
+  RqChunk* d_rq = nullptr;
+  int* d_rq_beg = nullptr;
+  RqMat* d_rq_mats = nullptr;
+  int2* d_rq_blocks = nullptr;
+  float* d_rq_ws = nullptr;
   std::vector<int> tall_list, all_list;
   std::vector<RowItem> k4, k5;
   std::vector<Group> g4, g5;
@@ -2710,6 +2941,56 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       if (gp.eend > gp.ebeg) pl->gkr.push_back(gp);
     }
   }
+  {  // k3_rq: the q pass of the k4_rows matrices, row blocks by bulk TMA (PSGD_K3RQ=0: k3_slab instead)
+    static const bool off = getenv("PSGD_K3RQ") && getenv("PSGD_K3RQ")[0] == '0';
+    static const bool rev = !(getenv("PSGD_RQ_REV") && getenv("PSGD_RQ_REV")[0] == '0');
+    pl->rq_rev = rev ? 1 : 0;
+    pl->rq_on.assign(std::max(1, nmat), 0);
+    std::vector<double> w;
+    for (int mi = 0; mi < nmat && !off; ++mi) {
+      const MatDev& md = pl->mats[mi];
+      if (md.tall != 2 || md.flat_off % 4 != 0 || md.m % 2 != 0) continue;
+      const int rows = std::max(1, std::min((RQ_STAGE_FLOATS - 8) / md.m, (RQ_PST - 8) / md.r));
+      for (int r0 = 0; r0 < md.n; r0 += rows) {
+        const int nr = std::min(rows, md.n - r0);
+        pl->rq.push_back({md.flat_off + (long long)r0 * md.m, 0, mi, r0, nr, 0});
+        w.push_back((double)nr * md.m);
+      }
+      pl->rq_on[mi] = 1;
+      pl->rq_rmax = std::max(pl->rq_rmax, rmax_of(md.r));
+    }
+    if (!pl->rq.empty()) {
+      pl->rq_beg = balance(w, pl->nsm);
+      const int nct = (int)pl->rq_beg.size() - 1;
+      std::vector<int> nslots(nmat, 0), sidx(pl->rq.size(), 0);
+      for (int b = 0; b < nct; ++b)
+        for (int k = pl->rq_beg[b]; k < pl->rq_beg[b + 1]; ++k) {
+          const bool first = k == pl->rq_beg[b] || pl->rq[k - 1].mat != pl->rq[k].mat;
+          const bool last = k + 1 == pl->rq_beg[b + 1] || pl->rq[k + 1].mat != pl->rq[k].mat;
+          sidx[k] = first ? nslots[pl->rq[k].mat]++ : sidx[k - 1];
+          pl->rq[k].flush = rev ? first : last;  // the run's last block in traversal order
+        }
+      std::vector<long long> slot0(nmat, 0);
+      for (int mi = 0; mi < nmat; ++mi) {
+        if (!nslots[mi]) continue;
+        const MatDev& md = pl->mats[mi];
+        slot0[mi] = pl->rq_ws_elems;
+        pl->rq_ws_elems += (long long)nslots[mi] * md.m * md.r;
+        const int ri = (int)pl->rq_mats.size();
+        pl->rq_mats.push_back({slot0[mi], mi, nslots[mi]});
+        for (int e0 = 0; e0 < md.m * md.r; e0 += 32) pl->rq_blocks.push_back(make_int2(ri, e0));
+      }
+      for (size_t k = 0; k < pl->rq.size(); ++k) {
+        const MatDev& md = pl->mats[pl->rq[k].mat];
+        pl->rq[k].slot = slot0[pl->rq[k].mat] + (long long)sidx[k] * md.m * md.r;
+      }
+      RqLayout& L = pl->rql;
+      L.off_p = RQ_STAGES * RQ_STAGE_FLOATS * 4;
+      L.off_red = L.off_p + RQ_STAGES * RQ_PST * 4;
+      L.off_bar = (L.off_red + kCons * 2 * pl->rq_rmax * 4 + 15) & ~15;
+      L.total = L.off_bar + 2 * RQ_STAGES * 8 + 16;
+    }
+  }
   {  // replacement columns depend on (n, j, attempt) only (linalg.py:54-58): one table per distinct n
     std::map<int, int> cols;
     for (auto& md : pl->mats) cols[md.n] = std::max(cols[md.n], md.r);
@@ -2873,6 +3154,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
         const K3Cfg cf = k3_tall_config(md.n, md.m, r);
         if ((cf.nchunks > 1) != (tall == 1)) continue;
         if (tall && k3_tileable(md)) continue;  // K3 column tiles instead
+        if (tall && pl->rq_on[mi]) continue;    // k3_rq row blocks instead
         const int CQ = 1 << cf.cql, C = CQ * cf.vec, RG = kThreads / CQ;
         const int nslab = (md.m + C - 1) / C;
         for (int s = 0; s < nslab; ++s) {
@@ -3049,6 +3331,11 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_gs = take((size_t)pl->p_elems * sizeof(double));
   const size_t o_wsq = take((size_t)std::max(1LL, pl->wsq_elems) * sizeof(float));
   const size_t o_cnt = take((size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
+  const size_t o_rq = take(pl->rq.size() * sizeof(RqChunk));
+  const size_t o_rqb = take(pl->rq_beg.size() * sizeof(int));
+  const size_t o_rqm = take(pl->rq_mats.size() * sizeof(RqMat));
+  const size_t o_rqk = take(pl->rq_blocks.size() * sizeof(int2));
+  const size_t o_rqw = take((size_t)std::max(1LL, pl->rq_ws_elems) * sizeof(float));
   cudaError_t ce = cudaMalloc(&pl->dev_block, off);
   if (ce != cudaSuccess) {
     delete pl;
@@ -3096,6 +3383,11 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_gsws = reinterpret_cast<double*>(b + o_gs);
   pl->d_wsq = reinterpret_cast<float*>(b + o_wsq);
   pl->d_counters = reinterpret_cast<int*>(b + o_cnt);
+  pl->d_rq = reinterpret_cast<RqChunk*>(b + o_rq);
+  pl->d_rq_beg = reinterpret_cast<int*>(b + o_rqb);
+  pl->d_rq_mats = reinterpret_cast<RqMat*>(b + o_rqm);
+  pl->d_rq_blocks = reinterpret_cast<int2*>(b + o_rqk);
+  pl->d_rq_ws = reinterpret_cast<float*>(b + o_rqw);
   auto up = [&](void* dst, const void* src, size_t bytes) {
     return bytes ? cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
   };
@@ -3132,6 +3424,10 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_k5, pl->k5.data(), pl->k5.size() * sizeof(RowItem));
   if (ce == cudaSuccess) ce = up(pl->d_pipe_items, pl->pipe_items.data(), pl->pipe_items.size() * sizeof(PipeItem));
   if (ce == cudaSuccess) ce = up(pl->d_kr_e, pl->kr_e.data(), pl->kr_e.size() * sizeof(RowsItem));
+  if (ce == cudaSuccess) ce = up(pl->d_rq, pl->rq.data(), pl->rq.size() * sizeof(RqChunk));
+  if (ce == cudaSuccess) ce = up(pl->d_rq_beg, pl->rq_beg.data(), pl->rq_beg.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_rq_mats, pl->rq_mats.data(), pl->rq_mats.size() * sizeof(RqMat));
+  if (ce == cudaSuccess) ce = up(pl->d_rq_blocks, pl->rq_blocks.data(), pl->rq_blocks.size() * sizeof(int2));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_pipe_ctr, 0, 2 * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_split_cnt, 0, std::max<size_t>(16, pl->splits.size() * sizeof(int)));
@@ -3180,7 +3476,7 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
     o->launches_orthogonalize = ((small || pl->nbias > 0) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 3);
     const bool gs3 = !pl->gs3_list.empty() && !pl->pipe_items.empty();
     const bool small3 = (gs3 ? pl->wlist3.size() + pl->clist3.size() : pl->wlist.size() + pl->clist.size()) > 0;
-    const bool bias_k3 = !small3 && !pl->gram_items.empty() && !pl->g3.empty();
+    const bool bias_k3 = !small3 && !pl->gram_items.empty() && (!pl->g3.empty() || !pl->rq.empty());
     const bool bias_pipe = gs3 && !small3 && !bias_k3;
     k2_in_q_ef = ((small3 || (pl->nbias > 0 && !bias_k3 && !bias_pipe)) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 3);
     (void)bias_in_k3;
@@ -3188,7 +3484,7 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->launches_q_ef = k2_in_q_ef + (pl->pipe_items.empty() ? 0 : 1) + (int)pl->gkr.size() + nonempty(pl->g3) +
                      nonempty(pl->g4) + nonempty(pl->g4t) +
                      nonempty(pl->g4t2) +
-                     (pl->k3t.empty() ? 0 : 2);
+                     (pl->k3t.empty() ? 0 : 2) + (pl->rq.empty() ? 0 : 2);
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
   o->launches_step_single = o->launches_ef_p + o->launches_q_ef;
@@ -3429,6 +3725,34 @@ int launch_rows(const psgd_plan* pl, float* work, float* e, const float* phat, c
   return PSGD_OK;
 }
 
+template <int R>
+int launch_rq_r(const psgd_plan* pl, const float* work, const float* phat, const float* p, float* bias_out,
+                long long nbias, int divisor, int* status, cudaStream_t st) {
+  auto kern = k3_rq<R>;
+  PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->rql.total));
+  static const int dpol = getenv("PSGD_RQ_POL") ? atoi(getenv("PSGD_RQ_POL")) : 1;
+  PSGD_CUDA_CHECK(launch_ex(kern, (int)pl->rq_beg.size() - 1, kTmaThreads, (size_t)pl->rql.total, st, PSGD_PDL != 0,
+                            (const MatDev*)pl->d_mats, (const RqChunk*)pl->d_rq, (const int*)pl->d_rq_beg, pl->rql,
+                            work, phat, pl->d_rq_ws, p, bias_out, nbias, (long long)pl->p_bias_off, divisor,
+                            pl->rq_rev, dpol, status));
+  return PSGD_OK;
+}
+
+int launch_rq(const psgd_plan* pl, const float* work, const float* phat, const float* p, float* bias_out,
+              long long nbias, int divisor, float* q_out, int* status, cudaStream_t st) {
+  int rc;
+  switch (pl->rq_rmax) {
+    case 1: rc = launch_rq_r<1>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
+    case 2: rc = launch_rq_r<2>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
+    default: rc = launch_rq_r<4>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
+  }
+  if (rc) return rc;
+  PSGD_CUDA_CHECK(launch_ex(k3_rq_reduce, (int)pl->rq_blocks.size(), 32 * RQR_GROUPS, 0, st, PSGD_PDL != 0,
+                            (const MatDev*)pl->d_mats, (const RqMat*)pl->d_rq_mats, (const int2*)pl->d_rq_blocks,
+                            (const float*)pl->d_rq_ws, q_out, (const int*)status));
+  return PSGD_OK;
+}
+
 bool check_dev(const psgd_plan* pl) {
   int dev = -1;
   cudaGetDevice(&dev);
@@ -3456,13 +3780,14 @@ int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, 
                               status));
   }
   if (!pl->gram_items.empty()) {
+    static const int xskip = getenv("PSGD_X_SKIP") ? atoi(getenv("PSGD_X_SKIP")) : 0;  // timing experiments only
     for (int pass = 1; pass <= 2; ++pass)  // pass 2 (re-orthogonalisation) exits at once unless pass 1 asks for it
-      PSGD_CUDA_CHECK(launch_ex(pass == 1 ? k2_gram<1> : k2_gram<2>, (int)pl->gram_items.size(), 256, 0, st,
+      if (!(xskip & pass)) PSGD_CUDA_CHECK(launch_ex(pass == 1 ? k2_gram<1> : k2_gram<2>, (int)pl->gram_items.size(), 256, 0, st,
                                 PSGD_PDL != 0,
                                 (const MatDev*)pl->d_mats, (const GramItem*)pl->d_gram_items, p, divisor, repl,
                                 pl->d_wsg, pl->d_wsT, pl->d_gram_cnt, (long long)pl->flag_off, pl->nflags,
                                 pl->d_gsws, phat, status));
-    PSGD_CUDA_CHECK(launch_ex(k2_apply, (int)pl->apply_mat.size(), 256, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
+    if (!(xskip & 4)) PSGD_CUDA_CHECK(launch_ex(k2_apply, (int)pl->apply_mat.size(), 256, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
                               (const int*)pl->d_gram_list, (const int*)pl->d_apply_mat,
                               (const int*)pl->d_apply_row0, p, divisor, (const double*)pl->d_wsT, phat,
                               (const int*)status));
@@ -3528,7 +3853,7 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
   // (not with the fused optimizer: measured 11 us slower there, 93 -> 104 us, profiles/r2/sweeps/opt_ab*.txt)
   const bool gs3 = !pl->gs3_list.empty() && !pl->pipe_items.empty() && sg.x == nullptr;
   const bool k2_small = (gs3 ? pl->wlist3.size() + pl->clist3.size() : pl->wlist.size() + pl->clist.size()) > 0;
-  const bool bias_in_k3 = !k2_small && !pl->gram_items.empty() && !pl->g3.empty();
+  const bool bias_in_k3 = !k2_small && !pl->gram_items.empty() && (!pl->g3.empty() || !pl->rq.empty());
   const bool bias_in_pipe = gs3 && !k2_small && !bias_in_k3;
   if (k2_small || !pl->gram_items.empty() || (pl->nbias > 0 && !bias_in_k3 && !bias_in_pipe)) {
     rc = launch_k2(pl, !bias_in_k3 && !bias_in_pipe, p, p_hat, divisor, repl, bias_out, (int*)status, st, gs3);
@@ -3540,6 +3865,12 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
           (long long)pl->nbias, pl->nflags, (int)divisor};
   rc = launch_pipe(pl, work, p_hat, q_out, e, (int*)status, st, sg, gs);  // K3 pipeline (n <= 512)
   if (rc) return rc;
+  if (!pl->rq.empty()) {  // q pass of the k4_rows matrices (row blocks), then the slot reduction
+    rc = launch_rq(pl, work, p_hat, p, bias_out, bias_done ? 0LL : (long long)pl->nbias, (int)divisor, q_out,
+                   (int*)status, st);
+    if (rc) return rc;
+    bias_done = true;
+  }
   for (const Group& gp : pl->g3) {  // K3: q (+ EF, M-hat) per slab (after K2: delta is final)
     rc = dispatch_r<RunK3>(gp.r, pl, gp, work, p, (int)divisor, repl, p_hat, q_out, e, bias_out,
                            bias_done ? 0LL : (long long)pl->nbias, (int*)status, st);
