@@ -1854,37 +1854,50 @@ __global__ void __launch_bounds__(KR_THREADS)
 // the slots in row order (deterministic).  Delta is final when the kernel starts
 // (K2 ran after K1), so the ring is filled before griddepcontrol.wait; P-hat is
 // fetched after it.  The range is walked backwards: the last rows K1 wrote (still
-// in L2) are read first.
-constexpr int RQ_STAGES = 4;
+// in L2) are read first.  For matrices orthogonalised in Gram space the kernel
+// stages the rows of P instead, and one warp makes k2_apply's P-hat = (P / W) T
+// (float64, stored for K4) a stage ahead of the 15 streaming warps, so q_ef has no
+// k2_apply launch.  3 stages (~172 KB): the CTA fits on an SM beside K2's CTAs and
+// starts streaming while they run (4 stages: 214 vs 206 us on LSTM, sweeps).
+constexpr int RQ_STAGES = 4;      // ring capacity; the plan uses PSGD_RQ_STAGES (default 3: the CTA then fits beside K2's, measured)
 constexpr int RQ_STAGE_FLOATS = 12288;  // 48 KB of delta per stage
 constexpr int RQ_PST = 512;             // P-hat floats per stage
 struct RqChunk {
   long long off;   // flat offset of the block's first element
   long long slot;  // float offset of this CTA's partial of `mat` in the slot workspace
   int mat, row0, nrows, flush;  // flush: the CTA's last block of `mat` in traversal order
+  int gidx, pad;  // gidx >= 0: P-hat = (P / W) T from the Gram-space T (k2_apply folded in); -1: staged P-hat
 };
 struct RqLayout {
-  int off_p, off_red, off_bar, total;
+  int stages, off_p, off_ph, off_red, off_bar, total;
 };
 
 template <int R>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     k3_rq(const MatDev* __restrict__ mats, const RqChunk* __restrict__ chunks, const int* __restrict__ cta_beg,
-          RqLayout L, const float* __restrict__ work, const float* __restrict__ Phat, float* __restrict__ wsq,
-          const float* __restrict__ P, float* __restrict__ bias_out, long long nbias, long long bias_off,
-          int divisor, int rev, int dpol, int* status) {
+          RqLayout L, const float* __restrict__ work, float* __restrict__ Phat, float* __restrict__ wsq,
+          const float* __restrict__ P, const double* __restrict__ wsT, float* __restrict__ bias_out, long long nbias,
+          long long bias_off, int divisor, int rev, int dpol, int* status) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* sdb = reinterpret_cast<float*>(smem_raw);
   float* spb = reinterpret_cast<float*>(smem_raw + L.off_p);
+  float* phb = reinterpret_cast<float*>(smem_raw + L.off_ph);  // stages x RQ_PST: P-hat rows made from P
   float* red = reinterpret_cast<float*>(smem_raw + L.off_red);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
-  uint64_t* empty = full + RQ_STAGES;
+  uint64_t* empty = full + L.stages;
+  uint64_t* pready = empty + L.stages;  // the P-hat rows of a stage are ready (transform warp)
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int cb = cta_beg[blockIdx.x], ce = cta_beg[blockIdx.x + 1], nck = ce - cb;
+  // the P-hat rows of a block: (P / W) T when the matrix went through Gram space (and the direct
+  // fallback did not write P-hat itself), else K2's P-hat (read after griddepcontrol.wait only)
+  auto from_p = [&](const RqChunk& ch) {
+    return ch.gidx >= 0 && wsT[(long long)ch.gidx * K2G_TS + K2G_DIRECT] == 0.0;
+  };
   if (t == 0) {
-    for (int s = 0; s < RQ_STAGES; ++s) {
+    for (int s = 0; s < L.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsWarps);
+      mbar_init(&pready[s], 1);
     }
     fence_mbar_init();
   }
@@ -1901,10 +1914,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         a4 = pa & ~3LL;
         return (uint32_t)((((pa + (long long)ch.nrows * md.r + 3) & ~3LL) - a4) * 4);
       };
-      const int pre = min(nck, RQ_STAGES);
+      const int pre = min(nck, L.stages);
       for (int j = 0; j < nck; ++j) {
-        const int s = j % RQ_STAGES;
-        const uint32_t ph = (j / RQ_STAGES) & 1;
+        const int s = j % L.stages;
+        const uint32_t ph = (j / L.stages) & 1;
         const RqChunk ch = chunk_at(j);
         const MatDev md = mats[ch.mat];
         mbar_wait(&empty[s], ph ^ 1);
@@ -1915,7 +1928,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const uint32_t pbytes = p_span(ch, md, pa4);
         mbar_expect_tx(&full[s], bytes + pbytes);
         tma_load(sdb + s * RQ_STAGE_FLOATS, work + a4, bytes, &full[s], pol);
-        if (j >= pre) tma_load(spb + s * RQ_PST, Phat + pa4, pbytes, &full[s], polp);
+        if (j >= pre) tma_load(spb + s * RQ_PST, (from_p(ch) ? P : Phat) + pa4, pbytes, &full[s], polp);
         if (j == pre - 1) {  // the ring is full of delta: wait for K2's P-hat, then its copies
           pdl_wait();
           for (int j2 = 0; j2 < pre; ++j2) {
@@ -1923,7 +1936,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const MatDev m2 = mats[c2.mat];
             long long q4;
             const uint32_t qb = p_span(c2, m2, q4);
-            tma_load(spb + j2 * RQ_PST, Phat + q4, qb, &full[j2], polp);
+            tma_load(spb + j2 * RQ_PST, (from_p(c2) ? P : Phat) + q4, qb, &full[j2], polp);
           }
         }
       }
@@ -1943,30 +1956,59 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
     if (bb) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
   }
+  // warps 0..14 stream the column pairs; warp 15 makes the P-hat rows of each stage (k2_apply's
+  // (P / W) T, float64) ahead of them and publishes them on pready
+  constexpr int XW = kConsWarps - 1, NCT = kCons - 32;
   float acc[2][R];
 #pragma unroll
   for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.f;
   for (int j = 0; j < nck; ++j) {
-    const int s = j % RQ_STAGES;
-    const uint32_t ph = (j / RQ_STAGES) & 1;
+    const int s = j % L.stages;
+    const uint32_t ph = (j / L.stages) & 1;
     const RqChunk ch = chunk_at(j);
     const MatDev md = mats[ch.mat];
     const int m = md.m, r = md.r, np = m >> 1;
-    const int TPR = min(kCons, (np + 31) & ~31), RGn = kCons / TPR;
+    const int TPR = min(NCT, (np + 31) & ~31), RGn = NCT / TPR;
     const int rg = t / TPR, tp = t - rg * TPR;
-    const bool act = rg < RGn && tp < np;
+    const bool act = warp < XW && rg < RGn && tp < np;
+    const long long pa = md.p_off + (long long)ch.row0 * r;
+    const float* sp = spb + s * RQ_PST + (int)(pa - (pa & ~3LL));
+    const bool fp = !bad && from_p(ch);
     mbar_wait(&full[s], ph);
-    if (!bad) {
-      const float* sd = sdb + s * RQ_STAGE_FLOATS + (int)(ch.off - (ch.off & ~3LL));
-      const long long pa = md.p_off + (long long)ch.row0 * r;
-      const float* sp = spb + s * RQ_PST + (int)(pa - (pa & ~3LL));
-      if (act) {
+    if (warp == XW) {
+      if (fp) {
+        const double* T = wsT + (long long)ch.gidx * K2G_TS;
+        const double inv_div = 1.0 / (double)divisor;
+        for (int li = lane; li < ch.nrows; li += 32) {
+          double x[R];
+#pragma unroll
+          for (int k = 0; k < R; ++k) x[k] = k < r ? (double)sp[li * r + k] * inv_div : 0.0;
+          float* dst = Phat + pa + (long long)li * r;
+#pragma unroll
+          for (int jj = 0; jj < R; ++jj) {
+            if (jj < r) {
+              double v = 0.0;
+#pragma unroll
+              for (int k = 0; k <= jj; ++k) v = fma(x[k], T[k * r + jj], v);
+              phb[s * RQ_PST + li * r + jj] = (float)v;
+              dst[jj] = (float)v;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pready[s]);
+    } else {
+      mbar_wait(&pready[s], ph);
+      if (!bad && act) {
+        const float* sd = sdb + s * RQ_STAGE_FLOATS + (int)(ch.off - (ch.off & ~3LL));
+        const float* pp = fp ? phb + s * RQ_PST : sp;
         const float2* d2 = reinterpret_cast<const float2*>(sd) + tp;
         int li = rg;
 #pragma unroll 2
         for (; li < ch.nrows; li += RGn) {
           const float2 d = d2[(li * m) >> 1];
-          const float* pr = sp + li * r;
+          const float* pr = pp + li * r;
 #pragma unroll
           for (int k = 0; k < R; ++k) {
             const float pk = k < r ? pr[k] : 0.f;
@@ -2664,6 +2706,8 @@ struct psgd_plan {
   int k2_wregion = 0, k2_wblocks = 0;
   std::vector<GramItem> gram_items;
   std::vector<int> apply_mat, apply_row0;   // k2_apply blocks
+  std::vector<int> apply_mat_q, apply_row0_q;  // the same without k3_rq's matrices (psgd_q_ef)
+  int *d_apply_mat_q = nullptr, *d_apply_row0_q = nullptr;
   long long wsg_elems = 0;
   std::vector<SlabItem> k3;          // fused and tall slabs, grouped by r
   std::vector<Group> g3;
@@ -2949,11 +2993,11 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     std::vector<double> w;
     for (int mi = 0; mi < nmat && !off; ++mi) {
       const MatDev& md = pl->mats[mi];
-      if (md.tall != 2 || md.flat_off % 4 != 0 || md.m % 2 != 0) continue;
+      if (md.tall != 2 || md.flat_off % 4 != 0 || md.m % 2 != 0 || md.m > 2 * (kCons - 32)) continue;
       const int rows = std::max(1, std::min((RQ_STAGE_FLOATS - 8) / md.m, (RQ_PST - 8) / md.r));
       for (int r0 = 0; r0 < md.n; r0 += rows) {
         const int nr = std::min(rows, md.n - r0);
-        pl->rq.push_back({md.flat_off + (long long)r0 * md.m, 0, mi, r0, nr, 0});
+        pl->rq.push_back({md.flat_off + (long long)r0 * md.m, 0, mi, r0, nr, 0, -1, 0});
         w.push_back((double)nr * md.m);
       }
       pl->rq_on[mi] = 1;
@@ -2985,10 +3029,13 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
         pl->rq[k].slot = slot0[pl->rq[k].mat] + (long long)sidx[k] * md.m * md.r;
       }
       RqLayout& L = pl->rql;
-      L.off_p = RQ_STAGES * RQ_STAGE_FLOATS * 4;
-      L.off_red = L.off_p + RQ_STAGES * RQ_PST * 4;
+      static const int nst = getenv("PSGD_RQ_STAGES") ? atoi(getenv("PSGD_RQ_STAGES")) : 3;
+      L.stages = std::max(2, std::min(RQ_STAGES, nst));
+      L.off_p = L.stages * RQ_STAGE_FLOATS * 4;
+      L.off_ph = L.off_p + L.stages * RQ_PST * 4;
+      L.off_red = L.off_ph + L.stages * RQ_PST * 4;
       L.off_bar = (L.off_red + kCons * 2 * pl->rq_rmax * 4 + 15) & ~15;
-      L.total = L.off_bar + 2 * RQ_STAGES * 8 + 16;
+      L.total = L.off_bar + 3 * L.stages * 8 + 16;
     }
   }
   {  // replacement columns depend on (n, j, attempt) only (linalg.py:54-58): one table per distinct n
@@ -3132,6 +3179,19 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
         pl->apply_mat.push_back(gidx);
         pl->apply_row0.push_back(r0);
       }
+    }
+  }
+  {  // k3_rq makes the P-hat of its Gram-space matrices itself: q_ef's k2_apply skips them
+    static const bool off = getenv("PSGD_RQ_APPLY") && getenv("PSGD_RQ_APPLY")[0] == '0';
+    for (auto& ch : pl->rq) {
+      const auto it = std::find(pl->gram_list.begin(), pl->gram_list.end(), ch.mat);
+      ch.gidx = (off || it == pl->gram_list.end()) ? -1 : (int)(it - pl->gram_list.begin());
+    }
+    for (size_t b2 = 0; b2 < pl->apply_mat.size(); ++b2) {
+      const int mi = pl->gram_list[pl->apply_mat[b2]];
+      if (!off && mi < (int)pl->rq_on.size() && pl->rq_on[mi]) continue;
+      pl->apply_mat_q.push_back(pl->apply_mat[b2]);
+      pl->apply_row0_q.push_back(pl->apply_row0[b2]);
     }
   }
   pl->k2_wblocks = ((int)pl->wlist.size() + K2_THREADS / 32 - 1) / (K2_THREADS / 32);
@@ -3310,6 +3370,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_gi = take(pl->gram_items.size() * sizeof(GramItem));
   const size_t o_am = take(pl->apply_mat.size() * sizeof(int));
   const size_t o_ar = take(pl->apply_row0.size() * sizeof(int));
+  const size_t o_amq = take(pl->apply_mat_q.size() * sizeof(int));
+  const size_t o_arq = take(pl->apply_row0_q.size() * sizeof(int));
   const size_t o_wg = take((size_t)std::max(1LL, pl->wsg_elems) * sizeof(double));
   const size_t o_wt = take(std::max<size_t>(1, pl->gram_list.size()) * K2G_TS * sizeof(double));
   const size_t o_gc = take(std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
@@ -3359,6 +3421,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_gram_items = reinterpret_cast<GramItem*>(b + o_gi);
   pl->d_apply_mat = reinterpret_cast<int*>(b + o_am);
   pl->d_apply_row0 = reinterpret_cast<int*>(b + o_ar);
+  pl->d_apply_mat_q = reinterpret_cast<int*>(b + o_amq);
+  pl->d_apply_row0_q = reinterpret_cast<int*>(b + o_arq);
   pl->d_wsg = reinterpret_cast<double*>(b + o_wg);
   pl->d_wsT = reinterpret_cast<double*>(b + o_wt);
   pl->d_gram_cnt = reinterpret_cast<int*>(b + o_gc);
@@ -3411,6 +3475,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_gram_items, pl->gram_items.data(), pl->gram_items.size() * sizeof(GramItem));
   if (ce == cudaSuccess) ce = up(pl->d_apply_mat, pl->apply_mat.data(), pl->apply_mat.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_apply_row0, pl->apply_row0.data(), pl->apply_row0.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_apply_mat_q, pl->apply_mat_q.data(), pl->apply_mat_q.size() * sizeof(int));
+  if (ce == cudaSuccess) ce = up(pl->d_apply_row0_q, pl->apply_row0_q.data(), pl->apply_row0_q.size() * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gram_cnt, 0, std::max<size_t>(1, pl->gram_list.size()) * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gs_flag, 0, (size_t)std::max(1, nmat) * 3 * sizeof(int) + 16);
   if (ce == cudaSuccess) ce = up(pl->d_k4, pl->k4.data(), pl->k4.size() * sizeof(RowItem));
@@ -3478,7 +3544,8 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
     const bool small3 = (gs3 ? pl->wlist3.size() + pl->clist3.size() : pl->wlist.size() + pl->clist.size()) > 0;
     const bool bias_k3 = !small3 && !pl->gram_items.empty() && (!pl->g3.empty() || !pl->rq.empty());
     const bool bias_pipe = gs3 && !small3 && !bias_k3;
-    k2_in_q_ef = ((small3 || (pl->nbias > 0 && !bias_k3 && !bias_pipe)) ? 1 : 0) + (pl->gram_items.empty() ? 0 : 3);
+    k2_in_q_ef = ((small3 || (pl->nbias > 0 && !bias_k3 && !bias_pipe)) ? 1 : 0) +
+                 (pl->gram_items.empty() ? 0 : 2 + (pl->apply_mat_q.empty() ? 0 : 1));
     (void)bias_in_k3;
   }
   o->launches_q_ef = k2_in_q_ef + (pl->pipe_items.empty() ? 0 : 1) + (int)pl->gkr.size() + nonempty(pl->g3) +
@@ -3726,19 +3793,20 @@ int launch_rows(const psgd_plan* pl, float* work, float* e, const float* phat, c
 }
 
 template <int R>
-int launch_rq_r(const psgd_plan* pl, const float* work, const float* phat, const float* p, float* bias_out,
+int launch_rq_r(const psgd_plan* pl, const float* work, float* phat, const float* p, float* bias_out,
                 long long nbias, int divisor, int* status, cudaStream_t st) {
   auto kern = k3_rq<R>;
   PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->rql.total));
   static const int dpol = getenv("PSGD_RQ_POL") ? atoi(getenv("PSGD_RQ_POL")) : 1;
   PSGD_CUDA_CHECK(launch_ex(kern, (int)pl->rq_beg.size() - 1, kTmaThreads, (size_t)pl->rql.total, st, PSGD_PDL != 0,
                             (const MatDev*)pl->d_mats, (const RqChunk*)pl->d_rq, (const int*)pl->d_rq_beg, pl->rql,
-                            work, phat, pl->d_rq_ws, p, bias_out, nbias, (long long)pl->p_bias_off, divisor,
+                            work, phat, pl->d_rq_ws, p, (const double*)pl->d_wsT, bias_out, nbias,
+                            (long long)pl->p_bias_off, divisor,
                             pl->rq_rev, dpol, status));
   return PSGD_OK;
 }
 
-int launch_rq(const psgd_plan* pl, const float* work, const float* phat, const float* p, float* bias_out,
+int launch_rq(const psgd_plan* pl, const float* work, float* phat, const float* p, float* bias_out,
               long long nbias, int divisor, float* q_out, int* status, cudaStream_t st) {
   int rc;
   switch (pl->rq_rmax) {
@@ -3760,7 +3828,8 @@ bool check_dev(const psgd_plan* pl) {
 }
 
 int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, int divisor,
-              const double* repl, float* bias_out, int* status, cudaStream_t st, bool skip_pipe = false) {
+              const double* repl, float* bias_out, int* status, cudaStream_t st, bool skip_pipe = false,
+              bool q_path = false) {
   // skip_pipe: the pipeline's matrices are orthogonalised inside k3_pipe
   const int nw = (int)(skip_pipe ? pl->wlist3 : pl->wlist).size();
   const int nci = (int)(skip_pipe ? pl->clist3 : pl->clist).size();
@@ -3787,10 +3856,13 @@ int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, 
                                 (const MatDev*)pl->d_mats, (const GramItem*)pl->d_gram_items, p, divisor, repl,
                                 pl->d_wsg, pl->d_wsT, pl->d_gram_cnt, (long long)pl->flag_off, pl->nflags,
                                 pl->d_gsws, phat, status));
-    if (!(xskip & 4)) PSGD_CUDA_CHECK(launch_ex(k2_apply, (int)pl->apply_mat.size(), 256, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
-                              (const int*)pl->d_gram_list, (const int*)pl->d_apply_mat,
-                              (const int*)pl->d_apply_row0, p, divisor, (const double*)pl->d_wsT, phat,
-                              (const int*)status));
+    // in psgd_q_ef, k3_rq makes the P-hat of its Gram-space matrices itself
+    const std::vector<int>& am = q_path ? pl->apply_mat_q : pl->apply_mat;
+    if (!am.empty() && !(xskip & 4))
+      PSGD_CUDA_CHECK(launch_ex(k2_apply, (int)am.size(), 256, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
+                                (const int*)pl->d_gram_list, (const int*)(q_path ? pl->d_apply_mat_q : pl->d_apply_mat),
+                                (const int*)(q_path ? pl->d_apply_row0_q : pl->d_apply_row0), p, divisor,
+                                (const double*)pl->d_wsT, phat, (const int*)status));
   }
   return PSGD_OK;
 }
@@ -3856,7 +3928,7 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
   const bool bias_in_k3 = !k2_small && !pl->gram_items.empty() && (!pl->g3.empty() || !pl->rq.empty());
   const bool bias_in_pipe = gs3 && !k2_small && !bias_in_k3;
   if (k2_small || !pl->gram_items.empty() || (pl->nbias > 0 && !bias_in_k3 && !bias_in_pipe)) {
-    rc = launch_k2(pl, !bias_in_k3 && !bias_in_pipe, p, p_hat, divisor, repl, bias_out, (int*)status, st, gs3);
+    rc = launch_k2(pl, !bias_in_k3 && !bias_in_pipe, p, p_hat, divisor, repl, bias_out, (int*)status, st, gs3, true);
     if (rc) return rc;
   }
   bool bias_done = !bias_in_k3;
