@@ -1869,8 +1869,9 @@ struct RqChunk {
   int gidx, pad;  // gidx >= 0: P-hat = (P / W) T from the Gram-space T (k2_apply folded in); -1: staged P-hat
 };
 struct RqLayout {
-  int stages, off_p, off_ph, off_red, off_bar, total;
+  int stages, off_p, off_ph, off_red, off_bar, off_ck, total;
 };
+constexpr int RQ_MAXCK = 64;  // block descriptors of a CTA staged in smem (more: read from global)
 
 template <int R>
 __global__ void __launch_bounds__(kTmaThreads, 1)
@@ -1886,6 +1887,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.off_bar);
   uint64_t* empty = full + L.stages;
   uint64_t* pready = empty + L.stages;  // the P-hat rows of a stage are ready (transform warp)
+  RqChunk* cks = reinterpret_cast<RqChunk*>(smem_raw + L.off_ck);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int cb = cta_beg[blockIdx.x], ce = cta_beg[blockIdx.x + 1], nck = ce - cb;
   // the P-hat rows of a block: (P / W) T when the matrix went through Gram space (and the direct
@@ -1901,9 +1903,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
     fence_mbar_init();
   }
+  auto chunk_g = [&](int j) { return chunks[rev ? ce - 1 - j : cb + j]; };
+  if (nck <= RQ_MAXCK && t < nck) cks[t] = chunk_g(t);  // no dependent global loads per block later
   __syncthreads();
   pdl_trigger();  // the slot reduction may stage in; it waits for this grid
-  auto chunk_at = [&](int j) { return chunks[rev ? ce - 1 - j : cb + j]; };
+  auto chunk_at = [&](int j) { return nck <= RQ_MAXCK ? cks[j] : chunk_g(j); };
 
   if (warp == kConsWarps) {  // ---------------- producer
     if (lane == 0) {
@@ -1915,11 +1919,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         return (uint32_t)((((pa + (long long)ch.nrows * md.r + 3) & ~3LL) - a4) * 4);
       };
       const int pre = min(nck, L.stages);
+      int cur = -1, fcur = -1;
+      bool fpc = false;
+      MatDev md{};
+      auto fp_of = [&](const RqChunk& c) {  // after griddepcontrol.wait only
+        if (c.mat != fcur) {
+          fcur = c.mat;
+          fpc = from_p(c);
+        }
+        return fpc;
+      };
       for (int j = 0; j < nck; ++j) {
         const int s = j % L.stages;
         const uint32_t ph = (j / L.stages) & 1;
         const RqChunk ch = chunk_at(j);
-        const MatDev md = mats[ch.mat];
+        if (ch.mat != cur) {
+          cur = ch.mat;
+          md = mats[ch.mat];
+        }
         mbar_wait(&empty[s], ph ^ 1);
         const long long a4 = ch.off & ~3LL;
         const long long b4 = (ch.off + (long long)ch.nrows * md.m + 3) & ~3LL;
@@ -1928,7 +1945,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const uint32_t pbytes = p_span(ch, md, pa4);
         mbar_expect_tx(&full[s], bytes + pbytes);
         tma_load(sdb + s * RQ_STAGE_FLOATS, work + a4, bytes, &full[s], pol);
-        if (j >= pre) tma_load(spb + s * RQ_PST, (from_p(ch) ? P : Phat) + pa4, pbytes, &full[s], polp);
+        if (j >= pre) tma_load(spb + s * RQ_PST, (fp_of(ch) ? P : Phat) + pa4, pbytes, &full[s], polp);
         if (j == pre - 1) {  // the ring is full of delta: wait for K2's P-hat, then its copies
           pdl_wait();
           for (int j2 = 0; j2 < pre; ++j2) {
@@ -1936,7 +1953,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const MatDev m2 = mats[c2.mat];
             long long q4;
             const uint32_t qb = p_span(c2, m2, q4);
-            tma_load(spb + j2 * RQ_PST, (from_p(c2) ? P : Phat) + q4, qb, &full[j2], polp);
+            tma_load(spb + j2 * RQ_PST, (fp_of(c2) ? P : Phat) + q4, qb, &full[j2], polp);
           }
         }
       }
@@ -1962,18 +1979,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   float acc[2][R];
 #pragma unroll
   for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.f;
+  int cur = -1;
+  bool fpm = false;
+  MatDev md{};
   for (int j = 0; j < nck; ++j) {
     const int s = j % L.stages;
     const uint32_t ph = (j / L.stages) & 1;
     const RqChunk ch = chunk_at(j);
-    const MatDev md = mats[ch.mat];
+    if (ch.mat != cur) {
+      cur = ch.mat;
+      md = mats[ch.mat];
+      fpm = !bad && from_p(ch);
+    }
     const int m = md.m, r = md.r, np = m >> 1;
     const int TPR = min(NCT, (np + 31) & ~31), RGn = NCT / TPR;
     const int rg = t / TPR, tp = t - rg * TPR;
     const bool act = warp < XW && rg < RGn && tp < np;
     const long long pa = md.p_off + (long long)ch.row0 * r;
     const float* sp = spb + s * RQ_PST + (int)(pa - (pa & ~3LL));
-    const bool fp = !bad && from_p(ch);
+    const bool fp = fpm;
     mbar_wait(&full[s], ph);
     if (warp == XW) {
       if (fp) {
@@ -3030,12 +3054,15 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       }
       RqLayout& L = pl->rql;
       static const int nst = getenv("PSGD_RQ_STAGES") ? atoi(getenv("PSGD_RQ_STAGES")) : 3;
-      L.stages = std::max(2, std::min(RQ_STAGES, nst));
-      L.off_p = L.stages * RQ_STAGE_FLOATS * 4;
-      L.off_ph = L.off_p + L.stages * RQ_PST * 4;
-      L.off_red = L.off_ph + L.stages * RQ_PST * 4;
-      L.off_bar = (L.off_red + kCons * 2 * pl->rq_rmax * 4 + 15) & ~15;
-      L.total = L.off_bar + 3 * L.stages * 8 + 16;
+      for (L.stages = std::max(2, std::min(RQ_STAGES, nst));; --L.stages) {
+        L.off_p = L.stages * RQ_STAGE_FLOATS * 4;
+        L.off_ph = L.off_p + L.stages * RQ_PST * 4;
+        L.off_red = L.off_ph + L.stages * RQ_PST * 4;
+        L.off_bar = (L.off_red + kCons * 2 * pl->rq_rmax * 4 + 15) & ~15;
+        L.off_ck = (L.off_bar + 3 * L.stages * 8 + 15) & ~15;
+        L.total = L.off_ck + RQ_MAXCK * (int)sizeof(RqChunk) + 16;
+        if (L.total <= 232448 - 1024 || L.stages == 2) break;  // 227 KB - static smem
+      }
     }
   }
   {  // replacement columns depend on (n, j, attempt) only (linalg.py:54-58): one table per distinct n
