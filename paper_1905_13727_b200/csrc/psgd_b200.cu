@@ -827,20 +827,17 @@ __global__ void __launch_bounds__(256)
   __shared__ double gpart[256];
   __shared__ double red[64];
   __shared__ int s_last, s_direct, s_refine;
+  const GramItem it = items[blockIdx.x];  // plan constants: read before the wait
+  const MatDev md = mats[it.mat];
   pdl_wait();
   pdl_trigger();  // the next pass / k2_apply may stage in; it waits for this grid itself
+  int fbad = 0;  // pass 1: a non-finite gradient on any worker (flags ride in P) — checked after the
+                 // block's first loads are in flight; nothing global is written before the check
   if (PASS == 1) {
-    int bad = 0;  // a non-finite gradient on any worker (flags ride in P): mutate nothing
-    for (int x = threadIdx.x; x < nflags; x += blockDim.x) bad |= P[flag_off + x] != 0.f;
-    if (__syncthreads_or(bad)) {
-      if (threadIdx.x == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
-      return;
-    }
+    for (int x = threadIdx.x; x < nflags; x += blockDim.x) fbad |= P[flag_off + x] != 0.f;
   } else if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) {
     return;
   }
-  const GramItem it = items[blockIdx.x];
-  const MatDev md = mats[it.mat];
   const int n = md.n, r = md.r;
   const int npairs = r * (r + 1) / 2;
   const double inv_div = 1.0 / (double)divisor;
@@ -887,6 +884,10 @@ __global__ void __launch_bounds__(256)
     if (pk >= 0)
 #pragma unroll 8
       for (int i = 0; i < K2G_TILE; ++i) acc = fma(X[i][pk], X[i][pl], acc);
+  }
+  if (PASS == 1 && __syncthreads_or(fbad)) {  // mutate nothing
+    if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
+    return;
   }
   if (PASS == 1 && __syncthreads_or(bad)) {  // linalg.py:35-36
     if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
@@ -1789,11 +1790,11 @@ __global__ void __launch_bounds__(KR_THREADS)
     k4_rows(const MatDev* __restrict__ mats, const RowsItem* __restrict__ items, float* __restrict__ work,
             float* __restrict__ e, const float* __restrict__ Phat, const float* __restrict__ qsrc, int write_mhat,
             const int* __restrict__ status) {
+  const RowsItem it = items[blockIdx.x];  // plan constants: read before the wait
+  const MatDev md = mats[it.mat];
   pdl_wait();
   pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
-  const RowsItem it = items[blockIdx.x];
-  const MatDev md = mats[it.mat];
   const int m = md.m, r = md.r, np = m >> 1, t = threadIdx.x;
   const bool ok0 = t < np, ok1 = t + KR_THREADS < np;
   float qv[2][2][R];  // q of the thread's four columns
@@ -2091,12 +2092,12 @@ __global__ void __launch_bounds__(32 * RQR_GROUPS)
     k3_rq_reduce(const MatDev* __restrict__ mats, const RqMat* __restrict__ rqm, const int2* __restrict__ blocks,
                  const float* __restrict__ wsq, float* __restrict__ qout, const int* __restrict__ status) {
   __shared__ float part[RQR_GROUPS][32];
+  const int2 b = blocks[blockIdx.x];  // plan constants: read before the wait
+  const RqMat rm = rqm[b.x];
+  const MatDev md = mats[rm.mat];
   pdl_wait();
   pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
-  const int2 b = blocks[blockIdx.x];
-  const RqMat rm = rqm[b.x];
-  const MatDev md = mats[rm.mat];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int o = b.y + lane;
   const long long mr = (long long)md.m * md.r;
