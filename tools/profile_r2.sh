@@ -2,7 +2,7 @@
 # Round-2 profiling pass (run under gpurun from the repo root): bench lines of every
 # workload, the reference arm, launch lists with DRAM bytes, and one ncu --set full
 # capture of each ResNet-18 / LSTM kernel.  Outputs under gpurun_out/r2prof/.
-O=gpurun_out/r2prof; mkdir -p $O
+O=gpurun_out/${PROF_TAG:-r2prof}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $O/gpu.txt 2>&1
 timeout 400 python bench.py > $O/bench_resnet18_r2.json 2> $O/bench_resnet18_r2.err
 timeout 400 python bench.py --rank 1 --no-cpu > $O/bench_resnet18_r1.json 2> $O/bench_resnet18_r1.err
@@ -19,6 +19,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     python tools/prof_step.py --workload stress --rank 8 --steps 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k1_ef_p|k2_gs|k3_pipe" -s 2 -c 2 \
     -o $O/resnet18_full python tools/prof_step.py --steps 3 > $O/ncu_resnet.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k1_ef_p|k2_gram|k2_apply|k3_slab|k4_tile2|k4_rows" -s 6 -c 6 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k1_ef_p|k2_gram|k3_rq|k4_rows" -s 6 -c 6 \
     -o $O/lstm_full python tools/prof_step.py --workload lstm --rank 4 --steps 3 > $O/ncu_lstm.log 2>&1
 echo done
