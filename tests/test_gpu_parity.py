@@ -200,3 +200,29 @@ def test_nonfinite_gradient_raises_and_leaves_state_untouched():
     with pytest.raises(NonFiniteGradient) as ei:
         eng.step()
     assert ei.value.param_name == "bias_vectors" and ei.value.worker == 0
+
+
+@pytest.mark.parametrize("rank,world", [(1, 1), (2, 2), (3, 1), (4, 1), (4, 3)])
+def test_row_block_q_pass_shapes(rank, world):
+    """k3_rq (the bulk-TMA row-block q pass of tall matrices with m = 2 mod 4,
+    m <= 960, r <= 4): several row groups per column pair (m = 98, 130, 2, 6),
+    Gram-space matrices whose P-hat k3_rq makes itself (n > 1024) and K2-MGS
+    matrices whose P-hat it stages (n <= 1024), odd n, many matrices per CTA."""
+    specs = [ParamSpec("g98", (1500, 98)), ParamSpec("b", (50,)), ParamSpec("o650", (3001, 650)),
+             ParamSpec("v130", (700, 130)), ParamSpec("m2", (1030, 2)), ParamSpec("m6", (2000, 6)),
+             ParamSpec("s18", (5000, 18)), ParamSpec("w", (64, 576))]
+    errs, _ = run_synced_step(specs, rank, world)
+    assert max(errs.values()) <= TOL, (rank, world, errs)
+
+
+def test_row_block_q_pass_bitwise_deterministic():
+    """Static row ranges per CTA and in-order slot sums: two runs from the same state agree bit for bit."""
+    specs = [ParamSpec("o650", (3001, 650)), ParamSpec("g98", (1500, 98)), ParamSpec("b", (7,))]
+    outs = []
+    for _ in range(2):
+        _, eng = run_synced_step(specs, 4, 1)
+        outs.append([eng.update_view(i).cpu().numpy().copy() for i in range(len(specs))] +
+                    [eng.q_view(i).cpu().numpy().copy() for i in (0, 1)] +
+                    [eng.error_view(i, 0).cpu().numpy().copy() for i in (0, 1)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
