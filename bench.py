@@ -430,14 +430,18 @@ def run_ours(a):
     achieved = dom_bytes / (kern_ms[dom] * 1e-3) / 1e9
     traffic, traffic_src = None, None
     prof_file = {("resnet18", 2): os.path.join("profiles", "ncu_summary.json"),
+                 ("resnet18", 1): os.path.join("profiles", "r2", "ncu_summary_r1.json"),
+                 ("resnet18", 4): os.path.join("profiles", "r2", "ncu_summary_r4.json"),
+                 ("stress", 8): os.path.join("profiles", "r2", "ncu_summary_stress.json"),
                  ("lstm", 4): os.path.join("profiles", "r2", "ncu_summary_lstm.json")}.get((a.workload, a.rank))
     try:  # dram bytes per launch of the same kernel from the committed ncu capture of this workload
         with open(os.path.join(ROOT, prof_file)) as f:
             prof = json.load(f)
-        for name, v in prof["kernels"].items():
-            if name.startswith("k1_ef_p"):
-                traffic = v["traffic_bytes"]
-                traffic_src = f"{prof_file} (ncu --set full, one launch)"
+        ks = [v["traffic_bytes"] for name, v in prof["kernels"].items()
+              if name.startswith("k1_ef_p") or name.startswith("k1_tile")]  # psgd_ef_p's launches
+        if ks:
+            traffic = float(sum(ks))
+            traffic_src = f"{prof_file} (ncu --set full, one launch of each psgd_ef_p kernel)"
     except Exception:
         pass
     b_alg = 24 * N + 20 * snr + 16 * smr
