@@ -56,7 +56,7 @@ constexpr int kTmaThreads = kCons + 32;  // + 1 producer warp
 constexpr int kRowItemElems = 4096;
 constexpr int kGsThreads = 1024;
 constexpr int kFusedNMax = 512;    // K3 fused path holds all rows of a slab
-constexpr int K1_STAGES = 3;       // max stages (the plan picks 2 or 3 and the stage size)
+constexpr int K1_STAGES = 8;       // max stages (the plan picks the ring depth and the stage size)
 constexpr int K1_CHUNK = 4608;     // floats of g (and of e) per chunk at the smallest stage
 constexpr int K1_QSLOT_CAP = 12288;  // floats of Q per smem slot (2 slots)
 constexpr int K1_QBIG_CAP = 18432;   // one large slot up to this (ResNet-18 r = 4: 4 x 4608); beyond: column tiles
@@ -255,6 +255,10 @@ __device__ __forceinline__ void load_q4(const float* __restrict__ q, int ld, boo
       if (aligned) {
         const float4 v = SMEM ? *reinterpret_cast<const float4*>(qk) : __ldg(reinterpret_cast<const float4*>(qk));
         qv[0][k] = v.x; qv[1][k] = v.y; qv[2][k] = v.z; qv[3][k] = v.w;
+      } else if ((reinterpret_cast<uintptr_t>(qk) & 7) == 0) {  // rows at 8 B (m = 2 mod 4, odd rows)
+        const float2 a = SMEM ? *reinterpret_cast<const float2*>(qk) : __ldg(reinterpret_cast<const float2*>(qk));
+        const float2 b = SMEM ? *reinterpret_cast<const float2*>(qk + 2) : __ldg(reinterpret_cast<const float2*>(qk + 2));
+        qv[0][k] = a.x; qv[1][k] = a.y; qv[2][k] = b.x; qv[3][k] = b.y;
       } else {
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) qv[jj][k] = SMEM ? qk[jj] : __ldg(qk + jj);
@@ -3109,7 +3113,8 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       if (md.qs) qslot = std::max(qslot, (long long)md.r * md.qld);
     }
     L.qslot_floats = (int)qslot;
-    L.stages = 2;
+    static const int nst = getenv("PSGD_K1_NST") ? atoi(getenv("PSGD_K1_NST")) : 2;
+    L.stages = std::max(2, std::min(K1_STAGES, nst));
     const long long room = 227LL * 1024 - L.nq * qslot * 4 - red_b - bar_b - 512;
     L.stage_floats = (int)std::min<long long>(16384 + 8, (room / (2LL * L.stages * 4)) & ~3LL);
     int off = 2 * L.stages * L.stage_floats * 4;
@@ -3141,7 +3146,10 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       int lg = 2;  // ~4 float4 per lane per row, 4..32 lanes
       while ((1 << lg) < (md.m + 15) / 16 && lg < 5) ++lg;
       int rows;
-      if (rows_fit >= (kCons >> lg)) {
+      static const bool partial = getenv("PSGD_K1_PARTIAL") && getenv("PSGD_K1_PARTIAL")[0] == '1';
+      if (partial && rows_fit < (kCons >> lg)) {  // experiment: a partial pass (idle warps), no multi-warp rows
+        rows = rows_fit;
+      } else if (rows_fit >= (kCons >> lg)) {
         rows = (rows_fit / (kCons >> lg)) * (kCons >> lg);
       } else {  // fewer rows than a pass: multi-warp rows, one reduction barrier per chunk
         int p2 = 1;
@@ -3843,7 +3851,8 @@ int launch_rq(const psgd_plan* pl, const float* work, float* phat, const float* 
     default: rc = launch_rq_r<4>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
   }
   if (rc) return rc;
-  PSGD_CUDA_CHECK(launch_ex(k3_rq_reduce, (int)pl->rq_blocks.size(), 32 * RQR_GROUPS, 0, st, PSGD_PDL != 0,
+  static const int xskip = getenv("PSGD_X_SKIP") ? atoi(getenv("PSGD_X_SKIP")) : 0;  // timing experiments only
+  if (!(xskip & 8)) PSGD_CUDA_CHECK(launch_ex(k3_rq_reduce, (int)pl->rq_blocks.size(), 32 * RQR_GROUPS, 0, st, PSGD_PDL != 0,
                             (const MatDev*)pl->d_mats, (const RqMat*)pl->d_rq_mats, (const int2*)pl->d_rq_blocks,
                             (const float*)pl->d_rq_ws, q_out, (const int*)status));
   return PSGD_OK;
@@ -4004,7 +4013,8 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
                                          (const int*)status));
     }
   }
-  rc = launch_rows(pl, work, e, p_hat, q_out, (const int*)status, st);  // tall, m = 2 mod 4: EF pass
+  static const int xskip = getenv("PSGD_X_SKIP") ? atoi(getenv("PSGD_X_SKIP")) : 0;  // timing experiments only
+  if (!(xskip & 16)) rc = launch_rows(pl, work, e, p_hat, q_out, (const int*)status, st);  // tall, m = 2 mod 4: EF pass
   if (rc) return rc;
   for (const Group& gp : pl->g4) {
     rc = dispatch_r<RunK4>(gp.r, pl, (const RowItem*)pl->d_k4, gp, work, e, (const float*)p_hat,

@@ -174,7 +174,7 @@ int main(int argc, char** argv) {
     float ms = timeit([&] { copy_stream<<<nsm * 8, 256>>>((const float4*)src, (float4*)dst, total / 16); });
     printf("LDG/STG copy (r+w)          : %.1f GB/s\n", 2.0 * total / ms / 1e6);
   }
-  for (int cb : {16384, 18432, 36864}) for (int st : {2, 3, 4, 6}) for (int ctas : {1, 2}) {
+  for (int cb : {16384, 36864, 49152}) for (int st : {2, 3, 4, 6}) for (int ctas : {1, 2}) {
     size_t smem = (size_t)st * cb + 2 * st * 8;
     if (smem * ctas > 220 * 1024) continue;
     cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
