@@ -366,8 +366,9 @@ struct WarpReducer {  // one warp, shuffles only
 // ============================================================================= K1
 // delta = g + e ; P[i,:] = sum_j delta[i,j] Q[j,:]   (optimizer.py:120, compressors.py:336)
 
-struct K1Layout {  // dynamic smem: g stages | e stages | Q slots | red | barriers
+struct K1Layout {  // dynamic smem: g stages | e stages | Q slots (| Q slots shifted by 2) | red | barriers
   int qslot_floats, nq;  // nq = 2 (double-buffered Q) or 1 (one large slot: m r up to ~128 KB)
+  int qshift;            // 1: each Q slot has a copy shifted by two floats (rows of m = 2 mod 4 at 8 B)
   int off_q, off_red, off_bar, total;
   int stages, stage_floats;  // chosen per plan: the largest stage that fits beside the Q slots
 };
@@ -375,6 +376,7 @@ struct K1Layout {  // dynamic smem: g stages | e stages | Q slots | red | barrie
 // One chunk: rows of the chunk to row groups of G = 2^lg consumer threads.
 template <int RM, bool QS>
 __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, const float* __restrict__ Qm,
+                                         const float* __restrict__ Qm2,
                                          const float* __restrict__ sg, const float* __restrict__ se,
                                          bool has_e, float* __restrict__ work, float* __restrict__ P,
                                          const SplitRow* __restrict__ splits, float* __restrict__ psplit,
@@ -415,7 +417,11 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
       const float4* __restrict__ e4 = reinterpret_cast<const float4*>(se + sm + head);
       float4* __restrict__ w4 = reinterpret_cast<float4*>(work + og + head);
       const float* __restrict__ qrow = Qm + ch.c0 + head;
-      const bool qal = ((ch.c0 + head) & 3) == 0;
+      bool qal = ((ch.c0 + head) & 3) == 0;
+      if (QS && Qm2 != nullptr && ((ch.c0 + head) & 3) == 2) {  // the shifted copy: 16-B aligned Q rows
+        qrow = Qm2 + ch.c0 + head - 2;
+        qal = true;
+      }
 #pragma unroll 2
       for (int c = gl; c < body4; c += G) {
         const float4 gv = g4[c];
@@ -616,6 +622,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       if (cur_qs) {
         ++qseq;
         mbar_wait(&qfull[qseq % L.nq], (qseq / L.nq) & 1);
+        if (L.qshift && (md.m & 3) == 2) {  // Q shifted by two floats: odd rows read it as float4
+          const float* src = qsl + (qseq % L.nq) * L.qslot_floats;
+          float* dst = qsl + (L.nq + qseq % L.nq) * L.qslot_floats;
+          const int nq = md.r * md.qld;
+          for (int x = t; x < nq; x += kCons) dst[x] = x + 2 < nq ? src[x + 2] : 0.f;
+          bar_consumers();  // every warp left the previous matrix (this slot's last user) before it
+        }
       }
     }
     mbar_wait(&full[s], ph);
@@ -628,14 +641,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 #else
     if (cur_qs)
 #endif
-      k1_chunk<RM, true>(ch, md, qsl + (qseq % L.nq) * L.qslot_floats, sg, se, e != nullptr, work, P, splits,
+      k1_chunk<RM, true>(ch, md, qsl + (qseq % L.nq) * L.qslot_floats,
+                         (L.qshift && (md.m & 3) == 2) ? qsl + (L.nq + qseq % L.nq) * L.qslot_floats : nullptr,
+                         sg, se, e != nullptr, work, P, splits,
                          psplit, split_cnt, rb, keep, bad);
 #ifndef PSGD_K1_NOCOMPUTE
     else
 #else
     else if (false)
 #endif
-      k1_chunk<RM, false>(ch, md, Q + md.q_off, sg, se, e != nullptr, work, P, splits, psplit, split_cnt,
+      k1_chunk<RM, false>(ch, md, Q + md.q_off, nullptr, sg, se, e != nullptr, work, P, splits, psplit, split_cnt,
                           rb, keep, bad);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -3113,12 +3128,17 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       if (md.qs) qslot = std::max(qslot, (long long)md.r * md.qld);
     }
     L.qslot_floats = (int)qslot;
+    static const bool qsh_off = getenv("PSGD_K1_QSHIFT") && getenv("PSGD_K1_QSHIFT")[0] == '0';
+    L.qshift = 0;
+    for (auto& md : pl->mats) L.qshift |= (!qsh_off && md.qs && (md.m & 3) == 2 && md.m >= 64) ? 1 : 0;
+    if (qslot > 4096) L.qshift = 0;  // the copies must stay small beside the ring (LSTM: 4 x 652 floats)
+    const int qcopies = L.qshift ? 2 : 1;
     static const int nst = getenv("PSGD_K1_NST") ? atoi(getenv("PSGD_K1_NST")) : 2;
     L.stages = std::max(2, std::min(K1_STAGES, nst));
-    const long long room = 227LL * 1024 - L.nq * qslot * 4 - red_b - bar_b - 512;
+    const long long room = 227LL * 1024 - qcopies * L.nq * qslot * 4 - red_b - bar_b - 512;
     L.stage_floats = (int)std::min<long long>(16384 + 8, (room / (2LL * L.stages * 4)) & ~3LL);
     int off = 2 * L.stages * L.stage_floats * 4;
-    L.off_q = off;   off += L.nq * L.qslot_floats * 4;
+    L.off_q = off;   off += qcopies * L.nq * L.qslot_floats * 4;
     L.off_red = off; off += (int)red_b;
     off = (off + 15) & ~15;
     L.off_bar = off; off += (int)bar_b;
