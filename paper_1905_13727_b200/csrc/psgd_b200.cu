@@ -1892,13 +1892,78 @@ struct RqLayout {
   int stages, off_p, off_ph, off_red, off_bar, off_ck, total;
 };
 constexpr int RQ_MAXCK = 64;  // block descriptors of a CTA staged in smem (more: read from global)
+struct RqMat {
+  long long slot0;  // float offset of slot 0 in the workspace (slots of m x r floats, row order)
+  int mat, nslots;
+};
+constexpr int RQR_GROUPS = 8;  // warps summing one 32-output block of q
+
+// q outputs [o0, o0 + 32) of matrix rm from its slots: warp g sums the slots g, g + 8, ... (16 loads in
+// flight), then the 8 group sums are added in group order (fixed order: deterministic).  `part` is
+// 8 x 32 floats of the calling 8-warp group; bar(): a barrier over exactly those 8 warps.
+template <class Bar>
+__device__ __forceinline__ void rq_reduce_block(const MatDev& md, const RqMat& rm, int o0, int g, int lane,
+                                                const float* __restrict__ wsq, float* __restrict__ qout,
+                                                float* part, const Bar& bar) {
+  const int o = o0 + lane;
+  const long long mr = (long long)md.m * md.r;
+  float s = 0.f;
+  if (o < mr) {
+    const float* src = wsq + rm.slot0 + o;
+    for (int j0 = g; j0 < rm.nslots; j0 += 16 * RQR_GROUPS) {
+      float y[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int j = j0 + u * RQR_GROUPS;
+        y[u] = j < rm.nslots ? __ldcg(src + (long long)j * mr) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += y[u];
+    }
+  }
+  part[g * 32 + lane] = s;
+  bar();
+  if (g == 0 && o < mr) {
+    float t = 0.f;
+#pragma unroll
+    for (int g2 = 0; g2 < RQR_GROUPS; ++g2) t += part[g2 * 32 + lane];
+    const int k = o / md.m, c = o - k * md.m;
+    qout[md.q_off + (long long)k * md.qld + c] = t;
+  }
+  bar();
+}
+
+// grid-wide barrier of a persistent launch (every CTA resident: grid <= SMs, 1 CTA/SM), called by one
+// thread per CTA after a CTA barrier; sense by generation.  A spin that does not end within ~2 s
+// raises PSGD_STATUS_GRID_TIMEOUT instead of hanging the GPU.
+__device__ __forceinline__ bool grid_sync(int* cnt, int* gen, int nblocks, int* status) {
+  const int g0 = ld_acquire(gen);
+  __threadfence();
+  if (atomicAdd(cnt, 1) == nblocks - 1) {
+    atomicExch(cnt, 0);
+    __threadfence();
+    atomicExch(gen, g0 + 1);
+    return true;
+  }
+  for (long long it = 0; ld_acquire(gen) == g0; ++it) {
+    if (it > (1LL << 24)) {
+      atomicOr(status, PSGD_STATUS_GRID_TIMEOUT);
+      return false;
+    }
+    __nanosleep(128);
+  }
+  __threadfence();
+  return true;
+}
 
 template <int R>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     k3_rq(const MatDev* __restrict__ mats, const RqChunk* __restrict__ chunks, const int* __restrict__ cta_beg,
           RqLayout L, const float* __restrict__ work, float* __restrict__ Phat, float* __restrict__ wsq,
           const float* __restrict__ P, const double* __restrict__ wsT, float* __restrict__ bias_out, long long nbias,
-          long long bias_off, int divisor, int rev, int dpol, int* status) {
+          long long bias_off, int divisor, int rev, int dpol, const RqMat* __restrict__ rqm,
+          const int2* __restrict__ rblocks, int nrblocks, float* __restrict__ qout, int* __restrict__ gsync,
+          int* status) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* sdb = reinterpret_cast<float*>(smem_raw);
   float* spb = reinterpret_cast<float*>(smem_raw + L.off_p);
@@ -2096,53 +2161,37 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.f;
     }
   }
+  if (nrblocks == 0) return;  // slots summed by k3_rq_reduce
+  // every CTA's slots are written: grid barrier, then CTA b sums the 32-output blocks b, b + grid, ...
+  // with its two 8-warp groups (named barriers 2 and 3)
+  __shared__ int s_ok;
+  bar_consumers();
+  if (t == 0) s_ok = grid_sync(gsync, gsync + 1, gridDim.x, status) ? 1 : 0;
+  bar_consumers();
+  if (bad || !s_ok) return;
+  const int grp = warp >> 3, g = warp & 7;
+  float* part = red + grp * RQR_GROUPS * 32;
+  auto gbar = [&] { asm volatile("bar.sync %0, 256;" ::"r"(2 + grp) : "memory"); };
+  for (int bi = blockIdx.x * 2 + grp; bi < nrblocks; bi += gridDim.x * 2) {
+    const int2 b = rblocks[bi];
+    const RqMat rm = rqm[b.x];
+    rq_reduce_block(mats[rm.mat], rm, b.y, g, lane, wsq, qout, part, gbar);
+  }
 }
 
-struct RqMat {
-  long long slot0;  // float offset of slot 0 in the workspace (slots of m x r floats, row order)
-  int mat, nslots;
-};
 
-// q_w of the k3_rq matrices: a CTA owns 32 consecutive outputs; its 8 warps sum the
-// slots g, g + 8, g + 16, ... (all loads in flight), then the 8 group sums are added
-// in group order (fixed order: deterministic)
-constexpr int RQR_GROUPS = 8;
+// q_w of the k3_rq matrices (when the q pass does not reduce its slots itself): a CTA per 32 outputs
 __global__ void __launch_bounds__(32 * RQR_GROUPS)
     k3_rq_reduce(const MatDev* __restrict__ mats, const RqMat* __restrict__ rqm, const int2* __restrict__ blocks,
                  const float* __restrict__ wsq, float* __restrict__ qout, const int* __restrict__ status) {
-  __shared__ float part[RQR_GROUPS][32];
+  __shared__ float part[RQR_GROUPS * 32];
   const int2 b = blocks[blockIdx.x];  // plan constants: read before the wait
   const RqMat rm = rqm[b.x];
   const MatDev md = mats[rm.mat];
   pdl_wait();
   pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int o = b.y + lane;
-  const long long mr = (long long)md.m * md.r;
-  float s = 0.f;
-  if (o < mr) {
-    const float* src = wsq + rm.slot0 + o;
-    for (int j0 = g; j0 < rm.nslots; j0 += 16 * RQR_GROUPS) {
-      float y[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int j = j0 + u * RQR_GROUPS;
-        y[u] = j < rm.nslots ? __ldcg(src + (long long)j * mr) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 16; ++u) s += y[u];
-    }
-  }
-  part[g][lane] = s;
-  __syncthreads();
-  if (g == 0 && o < mr) {
-    float t = 0.f;
-#pragma unroll
-    for (int g2 = 0; g2 < RQR_GROUPS; ++g2) t += part[g2][lane];
-    const int k = o / md.m, c = o - k * md.m;
-    qout[md.q_off + (long long)k * md.qld + c] = t;
-  }
+  rq_reduce_block(md, rm, b.y, threadIdx.x >> 5, threadIdx.x & 31, wsq, qout, part, [] { __syncthreads(); });
 }
 
 // K4 / K5 row streaming.  MODE 0 (K4): e = delta - P-hat q^T (+ M-hat in place
@@ -2780,6 +2829,8 @@ struct psgd_plan {
   std::vector<int2> rq_blocks;
   RqLayout rql{};
   int rq_rmax = 1, rq_rev = 1;
+  int rq_inkernel = 0;        // 1: k3_rq sums the slots itself after a grid barrier (no k3_rq_reduce launch)
+  int* d_rq_sync = nullptr;   // grid barrier: count, generation
   std::vector<char> rq_on;  // per matrix: q pass by k3_rq
   long long rq_ws_elems = 0;
   RqChunk* d_rq = nullptr;
@@ -3033,6 +3084,10 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     static const bool off = getenv("PSGD_K3RQ") && getenv("PSGD_K3RQ")[0] == '0';
     static const bool rev = !(getenv("PSGD_RQ_REV") && getenv("PSGD_RQ_REV")[0] == '0');
     pl->rq_rev = rev ? 1 : 0;
+    // PSGD_RQ_INK=1: slots summed inside k3_rq after a grid barrier — measured slower than the
+    // PDL-chained k3_rq_reduce (LSTM 185.7 vs 182.6 us, profiles/r2/sweeps/swk1b.txt)
+    static const bool ink_on = getenv("PSGD_RQ_INK") && getenv("PSGD_RQ_INK")[0] == '1';
+    pl->rq_inkernel = ink_on ? 1 : 0;
     pl->rq_on.assign(std::max(1, nmat), 0);
     std::vector<double> w;
     for (int mi = 0; mi < nmat && !off; ++mi) {
@@ -3454,6 +3509,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_rqm = take(pl->rq_mats.size() * sizeof(RqMat));
   const size_t o_rqk = take(pl->rq_blocks.size() * sizeof(int2));
   const size_t o_rqw = take((size_t)std::max(1LL, pl->rq_ws_elems) * sizeof(float));
+  const size_t o_rqs = take(2 * sizeof(int));
   cudaError_t ce = cudaMalloc(&pl->dev_block, off);
   if (ce != cudaSuccess) {
     delete pl;
@@ -3508,6 +3564,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_rq_mats = reinterpret_cast<RqMat*>(b + o_rqm);
   pl->d_rq_blocks = reinterpret_cast<int2*>(b + o_rqk);
   pl->d_rq_ws = reinterpret_cast<float*>(b + o_rqw);
+  pl->d_rq_sync = reinterpret_cast<int*>(b + o_rqs);
   auto up = [&](void* dst, const void* src, size_t bytes) {
     return bytes ? cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
   };
@@ -3552,6 +3609,7 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_rq_blocks, pl->rq_blocks.data(), pl->rq_blocks.size() * sizeof(int2));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_pipe_ctr, 0, 2 * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
+  if (ce == cudaSuccess) ce = cudaMemset(pl->d_rq_sync, 0, 2 * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_split_cnt, 0, std::max<size_t>(16, pl->splits.size() * sizeof(int)));
   if (ce != cudaSuccess) {
     cudaFree(pl->dev_block);
@@ -3607,7 +3665,7 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->launches_q_ef = k2_in_q_ef + (pl->pipe_items.empty() ? 0 : 1) + (int)pl->gkr.size() + nonempty(pl->g3) +
                      nonempty(pl->g4) + nonempty(pl->g4t) +
                      nonempty(pl->g4t2) +
-                     (pl->k3t.empty() ? 0 : 2) + (pl->rq.empty() ? 0 : 2);
+                     (pl->k3t.empty() ? 0 : 2) + (pl->rq.empty() ? 0 : (pl->rq_inkernel ? 1 : 2));
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
   o->launches_step_single = o->launches_ef_p + o->launches_q_ef;
@@ -3850,7 +3908,7 @@ int launch_rows(const psgd_plan* pl, float* work, float* e, const float* phat, c
 
 template <int R>
 int launch_rq_r(const psgd_plan* pl, const float* work, float* phat, const float* p, float* bias_out,
-                long long nbias, int divisor, int* status, cudaStream_t st) {
+                long long nbias, int divisor, float* q_out, int* status, cudaStream_t st) {
   auto kern = k3_rq<R>;
   PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->rql.total));
   static const int dpol = getenv("PSGD_RQ_POL") ? atoi(getenv("PSGD_RQ_POL")) : 1;
@@ -3858,7 +3916,8 @@ int launch_rq_r(const psgd_plan* pl, const float* work, float* phat, const float
                             (const MatDev*)pl->d_mats, (const RqChunk*)pl->d_rq, (const int*)pl->d_rq_beg, pl->rql,
                             work, phat, pl->d_rq_ws, p, (const double*)pl->d_wsT, bias_out, nbias,
                             (long long)pl->p_bias_off, divisor,
-                            pl->rq_rev, dpol, status));
+                            pl->rq_rev, dpol, (const RqMat*)pl->d_rq_mats, (const int2*)pl->d_rq_blocks,
+                            pl->rq_inkernel ? (int)pl->rq_blocks.size() : 0, q_out, pl->d_rq_sync, status));
   return PSGD_OK;
 }
 
@@ -3866,13 +3925,13 @@ int launch_rq(const psgd_plan* pl, const float* work, float* phat, const float* 
               long long nbias, int divisor, float* q_out, int* status, cudaStream_t st) {
   int rc;
   switch (pl->rq_rmax) {
-    case 1: rc = launch_rq_r<1>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
-    case 2: rc = launch_rq_r<2>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
-    default: rc = launch_rq_r<4>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
+    case 1: rc = launch_rq_r<1>(pl, work, phat, p, bias_out, nbias, divisor, q_out, status, st); break;
+    case 2: rc = launch_rq_r<2>(pl, work, phat, p, bias_out, nbias, divisor, q_out, status, st); break;
+    default: rc = launch_rq_r<4>(pl, work, phat, p, bias_out, nbias, divisor, q_out, status, st); break;
   }
   if (rc) return rc;
   static const int xskip = getenv("PSGD_X_SKIP") ? atoi(getenv("PSGD_X_SKIP")) : 0;  // timing experiments only
-  if (!(xskip & 8)) PSGD_CUDA_CHECK(launch_ex(k3_rq_reduce, (int)pl->rq_blocks.size(), 32 * RQR_GROUPS, 0, st, PSGD_PDL != 0,
+  if (!(xskip & 8) && !pl->rq_inkernel) PSGD_CUDA_CHECK(launch_ex(k3_rq_reduce, (int)pl->rq_blocks.size(), 32 * RQR_GROUPS, 0, st, PSGD_PDL != 0,
                             (const MatDev*)pl->d_mats, (const RqMat*)pl->d_rq_mats, (const int2*)pl->d_rq_blocks,
                             (const float*)pl->d_rq_ws, q_out, (const int*)status));
   return PSGD_OK;
