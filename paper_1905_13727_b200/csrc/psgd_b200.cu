@@ -867,7 +867,6 @@ struct GramItem {
 };
 
 constexpr int K2G_ROWS = 128;
-constexpr int K2G_TILE = 64;
 constexpr int K2G_TS = PSGD_MAX_RANK * PSGD_MAX_RANK + 8;  // doubles per matrix in wsT: T, then flags
 constexpr int K2G_DIRECT = PSGD_MAX_RANK * PSGD_MAX_RANK;  // flag: P-hat written by the direct fallback
 constexpr int K2G_REFINE = K2G_DIRECT + 1;                 // flag: pass 2 needed
@@ -880,7 +879,7 @@ __global__ void __launch_bounds__(256)
             int divisor, const double* __restrict__ repl, double* __restrict__ wsg, double* __restrict__ wsT,
             int* __restrict__ counters, long long flag_off, int nflags, double* __restrict__ scratch,
             float* __restrict__ Phat, int* status) {
-  __shared__ double X[K2G_TILE][PSGD_MAX_RANK + 1];
+  __shared__ double X[K2G_ROWS][PSGD_MAX_RANK + 1];
   __shared__ double G[PSGD_MAX_RANK][PSGD_MAX_RANK + 1];
   __shared__ double T1s[PSGD_MAX_RANK * PSGD_MAX_RANK];
   __shared__ double cvec[PSGD_MAX_RANK];
@@ -915,36 +914,43 @@ __global__ void __launch_bounds__(256)
     pk = k;
     pl = k + p;
   }
+  // the block's rows in one pass of loads (one memory round trip), then every thread sums its
+  // pair over a stride of rows and the row groups are added in order (fixed order)
   double acc = 0.0;
   int bad = 0;
-  for (int r0 = it.row0; r0 < it.row0 + it.nrows; r0 += K2G_TILE) {
-    __syncthreads();  // X (and T1s on the first tile) ready / free
+  const int NGp = npairs > 0 ? 256 / npairs : 1;
+  for (int r0 = it.row0; r0 < it.row0 + it.nrows; r0 += K2G_ROWS) {
+    const int nr = min(K2G_ROWS, it.row0 + it.nrows - r0);
+    __syncthreads();  // X (and T1s on the first block) ready / free
     if (PASS == 1) {
-      for (int idx = t; idx < K2G_TILE * r; idx += 256) {
-        const int i = idx / r, k = idx - i * r, row = r0 + i;
-        double v = 0.0;
-        if (row < it.row0 + it.nrows) {
-          const float f = P[md.p_off + (long long)row * r + k];
-          bad |= !finite1(f);
-          v = (double)f * inv_div;
-        }
-        X[i][k] = v;
+      for (int idx = t; idx < nr * r; idx += 256) {
+        const int i = idx / r, k = idx - i * r;
+        const float f = P[md.p_off + (long long)(r0 + i) * r + k];
+        bad |= !finite1(f);
+        X[i][k] = (double)f * inv_div;
       }
     } else {  // Y = X T1, row by row
-      for (int idx = t; idx < K2G_TILE * r; idx += 256) {
-        const int i = idx / r, k = idx - i * r, row = r0 + i;
+      for (int idx = t; idx < nr * r; idx += 256) {
+        const int i = idx / r, k = idx - i * r;
+        const float* pr = P + md.p_off + (long long)(r0 + i) * r;
         double v = 0.0;
-        if (row < it.row0 + it.nrows) {
-          const float* pr = P + md.p_off + (long long)row * r;
-          for (int l = 0; l <= k; ++l) v = fma((double)pr[l] * inv_div, T1s[l * r + k], v);
-        }
+        for (int l = 0; l <= k; ++l) v = fma((double)pr[l] * inv_div, T1s[l * r + k], v);
         X[i][k] = v;
       }
     }
     __syncthreads();
+    const int p = t % npairs, q = t / npairs;
+    if (npairs > 0 && q < NGp) {
+      int kk = 0, pp = p;
+      while (pp >= r - kk) { pp -= r - kk; ++kk; }
+      const int ll = kk + pp;
+      double a = 0.0;
+      for (int i = q; i < nr; i += NGp) a = fma(X[i][kk], X[i][ll], a);
+      gpart[q * npairs + p] = a;
+    }
+    __syncthreads();
     if (pk >= 0)
-#pragma unroll 8
-      for (int i = 0; i < K2G_TILE; ++i) acc = fma(X[i][pk], X[i][pl], acc);
+      for (int qq = 0; qq < NGp; ++qq) acc += gpart[qq * npairs + t];
   }
   if (PASS != 2 && __syncthreads_or(fbad)) {  // mutate nothing
     if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
@@ -3338,10 +3344,11 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     } else {
       const int gidx = (int)pl->gram_list.size();
       pl->gram_list.push_back(mi);
-      const int nblk = (md.n + K2G_ROWS - 1) / K2G_ROWS;
+      static const int grows = getenv("PSGD_K2G_ROWS") ? std::max(64, atoi(getenv("PSGD_K2G_ROWS"))) : K2G_ROWS;
+      const int nblk = (md.n + grows - 1) / grows;
       const int npairs = md.r * (md.r + 1) / 2;
       for (int b2 = 0; b2 < nblk; ++b2)
-        pl->gram_items.push_back({mi, b2 * K2G_ROWS, std::min(K2G_ROWS, md.n - b2 * K2G_ROWS), b2, nblk, gidx,
+        pl->gram_items.push_back({mi, b2 * grows, std::min(grows, md.n - b2 * grows), b2, nblk, gidx,
                                   pl->wsg_elems});
       pl->wsg_elems += (long long)nblk * npairs;
       for (int r0 = 0; r0 < md.n; r0 += 256) {
