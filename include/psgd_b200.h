@@ -44,7 +44,6 @@ extern "C" {
 #define PSGD_STATUS_NONFINITE_GRAD  1  /* optimizer.py:72-76 NonFiniteGradient */
 #define PSGD_STATUS_NONFINITE_P     2  /* linalg.py:35-36 via orthogonalize(as_matrix) */
 #define PSGD_STATUS_REPLACEMENT     4  /* linalg.py:82-88 needed more replacement draws than the table holds */
-#define PSGD_STATUS_GRID_TIMEOUT    8  /* internal: a grid-wide barrier timed out (no reference counterpart) */
 
 #define PSGD_MAX_RANK   16
 #define PSGD_MAX_TREE   64

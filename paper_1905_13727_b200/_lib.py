@@ -19,7 +19,6 @@ PSGD_ENOMEM = -3
 STATUS_NONFINITE_GRAD = 1
 STATUS_NONFINITE_P = 2
 STATUS_REPLACEMENT = 4
-STATUS_GRID_TIMEOUT = 8  # internal: a persistent kernel's grid barrier timed out
 
 MAX_RANK = 16
 MAX_TREE = 64

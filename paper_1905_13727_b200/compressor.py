@@ -86,8 +86,6 @@ def _raise_status(st):
         raise ContractViolation("orthogonalize input contains non-finite entries")
     if st & _lib.STATUS_REPLACEMENT:
         raise RuntimeError(f"Gram-Schmidt needed more than {_lib.REPL_ATTEMPTS} replacement draws for a column")
-    if st & _lib.STATUS_GRID_TIMEOUT:
-        raise RuntimeError("internal error: a grid-wide barrier of the q pass timed out")
 
 
 def _plan(n, m, rank, world, device):
@@ -480,8 +478,6 @@ class _Rounds:
             raise ContractViolation("orthogonalize input contains non-finite entries")
         if st & _lib.STATUS_REPLACEMENT:
             raise RuntimeError(f"Gram-Schmidt needed more than {_lib.REPL_ATTEMPTS} replacement draws for a column")
-        if st & _lib.STATUS_GRID_TIMEOUT:
-            raise RuntimeError("internal error: a grid-wide barrier of the q pass timed out")
 
 
 class BestApproximation(Compressor):

@@ -369,7 +369,6 @@ struct WarpReducer {  // one warp, shuffles only
 struct K1Layout {  // dynamic smem: g stages | e stages | Q slots (| Q slots shifted by 2) | red | barriers
   int qslot_floats, nq;  // nq = 2 (double-buffered Q) or 1 (one large slot: m r up to ~128 KB)
   int qshift;            // 1: each Q slot has a copy shifted by two floats (rows of m = 2 mod 4 at 8 B)
-  int off_g;             // > 0: 16 x 32 doubles for the Gram partials of the Gram-space matrices (W = 1)
   int off_q, off_red, off_bar, total;
   int stages, stage_floats;  // chosen per plan: the largest stage that fits beside the Q slots
 };
@@ -382,7 +381,7 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
                                          bool has_e, float* __restrict__ work, float* __restrict__ P,
                                          const SplitRow* __restrict__ splits, float* __restrict__ psplit,
                                          int* __restrict__ split_cnt, float* __restrict__ red, uint64_t keep,
-                                         bool& bad, bool gram, int gk, int gl2, double& gacc) {
+                                         bool& bad) {
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int r = md.r, m = md.m;
   const int lg = md.lg1;
@@ -455,15 +454,6 @@ __device__ __forceinline__ void k1_chunk(const Chunk1& ch, const MatDev& md, con
             bad |= !finite1(acc[q]);  // a non-finite delta poisons its P row (inf*0 = NaN too)
           }
       }
-      if (gram && active && gk >= 0) {  // the Gram pair (gk, gl2) of this lane, float64 (k2_gram pass 1's sum)
-        float vk = 0.f, vl = 0.f;  // every lane of the group holds the same (butterfly) row of P
-#pragma unroll
-        for (int q = 0; q < RM; ++q) {
-          if (q == gk) vk = acc[q];
-          if (q == gl2) vl = acc[q];
-        }
-        gacc = fma((double)vk, (double)vl, gacc);
-      }
     } else {  // multi-warp rows: per-warp partials, combined once per chunk below
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1)
@@ -530,7 +520,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const float* __restrict__ g, const float* __restrict__ e, float* __restrict__ work,
             const float* __restrict__ Q, float* __restrict__ P, float* __restrict__ psplit,
             int* __restrict__ split_cnt, const float* __restrict__ bias_g, long long nbias,
-            long long bias_off, long long flag_off, int* status, double* __restrict__ gram_ws) {
+            long long bias_off, long long flag_off, int* status) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* sgb = reinterpret_cast<float*>(smem_raw);
   float* seb = sgb + L.stages * L.stage_floats;
@@ -616,30 +606,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   bool cur_qs = false;
   Chunk1 nx = chunks[cb < ce ? cb : 0];
   MatDev md{};
-  // W = 1: the float64 Gram partial P^T P of this CTA's rows of each Gram-space matrix (slot ch.pad in
-  // gram_ws), lane p of a row group owning pair p; summed over the warps in fixed order at the end of
-  // the CTA's run of the matrix, so k2_gram pass 1 does not re-read P (pass 3 finishes from these)
-  double gacc = 0.0;
-  int gslot = -1, gk = -1, gl2 = -1, gnp = 0, gG = 32;
-  double* gred = reinterpret_cast<double*>(smem_raw + L.off_g);
-  auto gram_flush = [&]() {
-    gred[warp * 32 + lane] = gacc;
-    bar_consumers();
-    if (t < gnp) {
-      double sum = 0.0;
-      for (int w = 0; w < kConsWarps; ++w)
-        for (int j = 0; j < 32 / gG; ++j) sum += gred[w * 32 + j * gG + t];
-      gram_ws[gslot + t] = sum;
-    }
-    bar_consumers();
-    gacc = 0.0;
-  };
   for (int k = cb; k < ce; ++k) {
     const int s = (k - cb) % L.stages;
     const uint32_t ph = ((k - cb) / L.stages) & 1;
     const Chunk1 ch = nx;
     if (k + 1 < ce) nx = chunks[k + 1];  // next descriptor in flight
-    if (gram_ws != nullptr && gslot >= 0 && (ch.mat != cur || ch.pad != gslot)) gram_flush();
     if (ch.mat != cur) {
       if (cur >= 0 && cur_qs) {
         __syncwarp();
@@ -648,18 +619,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       md = mats[ch.mat];
       cur = ch.mat;
       cur_qs = md.qs != 0;
-      gslot = gram_ws != nullptr ? ch.pad : -1;
-      if (gslot >= 0) {  // pair of this lane within its row group (k <= l), as k2_gram enumerates them
-        gG = 1 << md.lg1;
-        gnp = md.r * (md.r + 1) / 2;
-        int pp = lane & (gG - 1), kk = 0;
-        gk = gl2 = -1;
-        if (pp < gnp) {
-          while (pp >= md.r - kk) { pp -= md.r - kk; ++kk; }
-          gk = kk;
-          gl2 = kk + pp;
-        }
-      }
       if (cur_qs) {
         ++qseq;
         mbar_wait(&qfull[qseq % L.nq], (qseq / L.nq) & 1);
@@ -685,18 +644,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       k1_chunk<RM, true>(ch, md, qsl + (qseq % L.nq) * L.qslot_floats,
                          (L.qshift && (md.m & 3) == 2) ? qsl + (L.nq + qseq % L.nq) * L.qslot_floats : nullptr,
                          sg, se, e != nullptr, work, P, splits,
-                         psplit, split_cnt, rb, keep, bad, gslot >= 0, gk, gl2, gacc);
+                         psplit, split_cnt, rb, keep, bad);
 #ifndef PSGD_K1_NOCOMPUTE
     else
 #else
     else if (false)
 #endif
       k1_chunk<RM, false>(ch, md, Q + md.q_off, nullptr, sg, se, e != nullptr, work, P, splits, psplit, split_cnt,
-                          rb, keep, bad, gslot >= 0, gk, gl2, gacc);
+                          rb, keep, bad);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  if (gram_ws != nullptr && gslot >= 0) gram_flush();
   if (bad) atomicOr(sflag, 1);
   bar_consumers();
   if (t == 0) P[flag_off + blockIdx.x] = *sflag ? 1.f : 0.f;  // rides in the P all-reduce (K2 reads it)
@@ -893,7 +851,7 @@ __global__ void __launch_bounds__(256)
   pdl_trigger();  // the next pass / k2_apply may stage in; it waits for this grid itself
   int fbad = 0;  // pass 1: a non-finite gradient on any worker (flags ride in P) — checked after the
                  // block's first loads are in flight; nothing global is written before the check
-  if (PASS != 2) {
+  if (PASS == 1) {
     for (int x = threadIdx.x; x < nflags; x += blockDim.x) fbad |= P[flag_off + x] != 0.f;
   } else if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) {
     return;
@@ -952,23 +910,21 @@ __global__ void __launch_bounds__(256)
     if (pk >= 0)
       for (int qq = 0; qq < NGp; ++qq) acc += gpart[qq * npairs + t];
   }
-  if (PASS != 2 && __syncthreads_or(fbad)) {  // mutate nothing
+  if (PASS == 1 && __syncthreads_or(fbad)) {  // mutate nothing
     if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_GRAD);
     return;
   }
   if (PASS == 1 && __syncthreads_or(bad)) {  // linalg.py:35-36
     if (t == 0) atomicOr(status, PSGD_STATUS_NONFINITE_P);
   }
-  if (PASS != 3) {  // pass 3: the partials are K1's (one per K1 CTA of the matrix); this CTA finishes
-    if (pk >= 0) wsg[it.gbase + (long long)it.blk * npairs + t] = acc;
-    __threadfence();
-    __syncthreads();
-    if (t == 0) s_last = atomicAdd(counters + it.gidx, 1) == it.nblk - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (t == 0) counters[it.gidx] = 0;
-  }
+  if (pk >= 0) wsg[it.gbase + (long long)it.blk * npairs + t] = acc;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) s_last = atomicAdd(counters + it.gidx, 1) == it.nblk - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (t == 0) counters[it.gidx] = 0;
   if (ld_acquire(status) & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;  // block-uniform
   {  // fixed order: thread groups take blocks q, q + NG, ...; then groups in order
     const int NG = 256 / npairs;
@@ -1024,7 +980,7 @@ __global__ void __launch_bounds__(256)
         __syncwarp();
       }
       if (j > 0) nrm = sqrt(fmax(gdot(cvec, cvec), 0.0));
-      if (PASS != 2 && (nrm < 1e-12 * (before + 1.0) || nrm < kGramTrust * before)) {
+      if (PASS == 1 && (nrm < 1e-12 * (before + 1.0) || nrm < kGramTrust * before)) {
         direct = true;  // degenerate (linalg.py:82) or beyond what Gram space resolves
         break;
       }
@@ -1039,7 +995,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   __syncthreads();
-  if (PASS != 2 && s_direct) {  // the reference's direct MGS on X (column-major scratch)
+  if (PASS == 1 && s_direct) {  // the reference's direct MGS on X (column-major scratch)
     double* x = scratch + md.p_off;
     for (int idx = t; idx < n * r; idx += 256) {
       const int i = idx / r, j = idx - i * r;
@@ -1060,7 +1016,7 @@ __global__ void __launch_bounds__(256)
   for (int x = t; x < r * r; x += 256) {  // T row-major [k][j]: P-hat column j = sum_k X[:, k] T[k][j]
     const int k = x / r, j = x - k * r;
     double v;
-    if (PASS != 2) {
+    if (PASS == 1) {
       v = Tm[j][k];
     } else {  // T = T1 T2
       v = 0.0;
@@ -1068,7 +1024,7 @@ __global__ void __launch_bounds__(256)
     }
     Tg[x] = v;
   }
-  if (PASS != 2 && t == 0) {
+  if (PASS == 1 && t == 0) {
     Tg[K2G_DIRECT] = 0.0;
     Tg[K2G_REFINE] = s_refine ? 1.0 : 0.0;
   }
@@ -1942,78 +1898,13 @@ struct RqLayout {
   int stages, off_p, off_ph, off_red, off_bar, off_ck, total;
 };
 constexpr int RQ_MAXCK = 64;  // block descriptors of a CTA staged in smem (more: read from global)
-struct RqMat {
-  long long slot0;  // float offset of slot 0 in the workspace (slots of m x r floats, row order)
-  int mat, nslots;
-};
-constexpr int RQR_GROUPS = 8;  // warps summing one 32-output block of q
-
-// q outputs [o0, o0 + 32) of matrix rm from its slots: warp g sums the slots g, g + 8, ... (16 loads in
-// flight), then the 8 group sums are added in group order (fixed order: deterministic).  `part` is
-// 8 x 32 floats of the calling 8-warp group; bar(): a barrier over exactly those 8 warps.
-template <class Bar>
-__device__ __forceinline__ void rq_reduce_block(const MatDev& md, const RqMat& rm, int o0, int g, int lane,
-                                                const float* __restrict__ wsq, float* __restrict__ qout,
-                                                float* part, const Bar& bar) {
-  const int o = o0 + lane;
-  const long long mr = (long long)md.m * md.r;
-  float s = 0.f;
-  if (o < mr) {
-    const float* src = wsq + rm.slot0 + o;
-    for (int j0 = g; j0 < rm.nslots; j0 += 16 * RQR_GROUPS) {
-      float y[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int j = j0 + u * RQR_GROUPS;
-        y[u] = j < rm.nslots ? __ldcg(src + (long long)j * mr) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 16; ++u) s += y[u];
-    }
-  }
-  part[g * 32 + lane] = s;
-  bar();
-  if (g == 0 && o < mr) {
-    float t = 0.f;
-#pragma unroll
-    for (int g2 = 0; g2 < RQR_GROUPS; ++g2) t += part[g2 * 32 + lane];
-    const int k = o / md.m, c = o - k * md.m;
-    qout[md.q_off + (long long)k * md.qld + c] = t;
-  }
-  bar();
-}
-
-// grid-wide barrier of a persistent launch (every CTA resident: grid <= SMs, 1 CTA/SM), called by one
-// thread per CTA after a CTA barrier; sense by generation.  A spin that does not end within ~2 s
-// raises PSGD_STATUS_GRID_TIMEOUT instead of hanging the GPU.
-__device__ __forceinline__ bool grid_sync(int* cnt, int* gen, int nblocks, int* status) {
-  const int g0 = ld_acquire(gen);
-  __threadfence();
-  if (atomicAdd(cnt, 1) == nblocks - 1) {
-    atomicExch(cnt, 0);
-    __threadfence();
-    atomicExch(gen, g0 + 1);
-    return true;
-  }
-  for (long long it = 0; ld_acquire(gen) == g0; ++it) {
-    if (it > (1LL << 24)) {
-      atomicOr(status, PSGD_STATUS_GRID_TIMEOUT);
-      return false;
-    }
-    __nanosleep(128);
-  }
-  __threadfence();
-  return true;
-}
 
 template <int R>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     k3_rq(const MatDev* __restrict__ mats, const RqChunk* __restrict__ chunks, const int* __restrict__ cta_beg,
           RqLayout L, const float* __restrict__ work, float* __restrict__ Phat, float* __restrict__ wsq,
           const float* __restrict__ P, const double* __restrict__ wsT, float* __restrict__ bias_out, long long nbias,
-          long long bias_off, int divisor, int rev, int dpol, const RqMat* __restrict__ rqm,
-          const int2* __restrict__ rblocks, int nrblocks, float* __restrict__ qout, int* __restrict__ gsync,
-          int* status) {
+          long long bias_off, int divisor, int rev, int dpol, int* status) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* sdb = reinterpret_cast<float*>(smem_raw);
   float* spb = reinterpret_cast<float*>(smem_raw + L.off_p);
@@ -2211,37 +2102,53 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       for (int k = 0; k < R; ++k) acc[0][k] = acc[1][k] = 0.f;
     }
   }
-  if (nrblocks == 0) return;  // slots summed by k3_rq_reduce
-  // every CTA's slots are written: grid barrier, then CTA b sums the 32-output blocks b, b + grid, ...
-  // with its two 8-warp groups (named barriers 2 and 3)
-  __shared__ int s_ok;
-  bar_consumers();
-  if (t == 0) s_ok = grid_sync(gsync, gsync + 1, gridDim.x, status) ? 1 : 0;
-  bar_consumers();
-  if (bad || !s_ok) return;
-  const int grp = warp >> 3, g = warp & 7;
-  float* part = red + grp * RQR_GROUPS * 32;
-  auto gbar = [&] { asm volatile("bar.sync %0, 256;" ::"r"(2 + grp) : "memory"); };
-  for (int bi = blockIdx.x * 2 + grp; bi < nrblocks; bi += gridDim.x * 2) {
-    const int2 b = rblocks[bi];
-    const RqMat rm = rqm[b.x];
-    rq_reduce_block(mats[rm.mat], rm, b.y, g, lane, wsq, qout, part, gbar);
-  }
 }
 
+struct RqMat {
+  long long slot0;  // float offset of slot 0 in the workspace (slots of m x r floats, row order)
+  int mat, nslots;
+};
 
-// q_w of the k3_rq matrices (when the q pass does not reduce its slots itself): a CTA per 32 outputs
+// q_w of the k3_rq matrices: a CTA owns 32 consecutive outputs; its 8 warps sum the
+// slots g, g + 8, g + 16, ... (all loads in flight), then the 8 group sums are added
+// in group order (fixed order: deterministic)
+constexpr int RQR_GROUPS = 8;
 __global__ void __launch_bounds__(32 * RQR_GROUPS)
     k3_rq_reduce(const MatDev* __restrict__ mats, const RqMat* __restrict__ rqm, const int2* __restrict__ blocks,
                  const float* __restrict__ wsq, float* __restrict__ qout, const int* __restrict__ status) {
-  __shared__ float part[RQR_GROUPS * 32];
+  __shared__ float part[RQR_GROUPS][32];
   const int2 b = blocks[blockIdx.x];  // plan constants: read before the wait
   const RqMat rm = rqm[b.x];
   const MatDev md = mats[rm.mat];
   pdl_wait();
   pdl_trigger();
   if (*status & (PSGD_STATUS_NONFINITE_GRAD | PSGD_STATUS_NONFINITE_P)) return;
-  rq_reduce_block(md, rm, b.y, threadIdx.x >> 5, threadIdx.x & 31, wsq, qout, part, [] { __syncthreads(); });
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int o = b.y + lane;
+  const long long mr = (long long)md.m * md.r;
+  float s = 0.f;
+  if (o < mr) {
+    const float* src = wsq + rm.slot0 + o;
+    for (int j0 = g; j0 < rm.nslots; j0 += 16 * RQR_GROUPS) {
+      float y[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int j = j0 + u * RQR_GROUPS;
+        y[u] = j < rm.nslots ? __ldcg(src + (long long)j * mr) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += y[u];
+    }
+  }
+  part[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && o < mr) {
+    float t = 0.f;
+#pragma unroll
+    for (int g2 = 0; g2 < RQR_GROUPS; ++g2) t += part[g2][lane];
+    const int k = o / md.m, c = o - k * md.m;
+    qout[md.q_off + (long long)k * md.qld + c] = t;
+  }
 }
 
 // K4 / K5 row streaming.  MODE 0 (K4): e = delta - P-hat q^T (+ M-hat in place
@@ -2848,9 +2755,6 @@ struct psgd_plan {
   int *d_small_list3 = nullptr, *d_gs3_list = nullptr, *d_gs3_ready = nullptr;
   int k2_wregion = 0, k2_wblocks = 0;
   std::vector<GramItem> gram_items;
-  std::vector<GramItem> gram3_items;  // W = 1: pass 3 (one CTA per Gram matrix) from K1's partials
-  GramItem* d_gram3_items = nullptr;
-  int k1gram = 0;
   std::vector<int> apply_mat, apply_row0;   // k2_apply blocks
   std::vector<int> apply_mat_q, apply_row0_q;  // the same without k3_rq's matrices (psgd_q_ef)
   int *d_apply_mat_q = nullptr, *d_apply_row0_q = nullptr;
@@ -2882,8 +2786,6 @@ struct psgd_plan {
   std::vector<int2> rq_blocks;
   RqLayout rql{};
   int rq_rmax = 1, rq_rev = 1;
-  int rq_inkernel = 0;        // 1: k3_rq sums the slots itself after a grid barrier (no k3_rq_reduce launch)
-  int* d_rq_sync = nullptr;   // grid barrier: count, generation
   std::vector<char> rq_on;  // per matrix: q pass by k3_rq
   long long rq_ws_elems = 0;
   RqChunk* d_rq = nullptr;
@@ -3137,10 +3039,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     static const bool off = getenv("PSGD_K3RQ") && getenv("PSGD_K3RQ")[0] == '0';
     static const bool rev = !(getenv("PSGD_RQ_REV") && getenv("PSGD_RQ_REV")[0] == '0');
     pl->rq_rev = rev ? 1 : 0;
-    // PSGD_RQ_INK=1: slots summed inside k3_rq after a grid barrier — measured slower than the
-    // PDL-chained k3_rq_reduce (LSTM 185.7 vs 182.6 us, profiles/r2/sweeps/swk1b.txt)
-    static const bool ink_on = getenv("PSGD_RQ_INK") && getenv("PSGD_RQ_INK")[0] == '1';
-    pl->rq_inkernel = ink_on ? 1 : 0;
     pl->rq_on.assign(std::max(1, nmat), 0);
     std::vector<double> w;
     for (int mi = 0; mi < nmat && !off; ++mi) {
@@ -3243,24 +3141,13 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
     const int qcopies = L.qshift ? 2 : 1;
     static const int nst = getenv("PSGD_K1_NST") ? atoi(getenv("PSGD_K1_NST")) : 2;
     L.stages = std::max(2, std::min(K1_STAGES, nst));
-    // PSGD_K1_GRAM=1: K1 accumulates the Gram partials of the Gram-space matrices at W = 1 and k2_gram
-    // pass 3 finishes them (no pass-1 re-read of P) — correct (110/110 GPU tests) but measured slower:
-    // K1 +5 us, q_ef -4 us (LSTM 185.2 vs 183.5 us, profiles/r2/sweeps/swk1b.txt); off by default
-    static const bool k1g_off = !(getenv("PSGD_K1_GRAM") && getenv("PSGD_K1_GRAM")[0] == '1');
-    bool maybe_gram = false;  // same rule as the K2 lists below (Gram space beyond the smem MGS)
-    for (auto& md : pl->mats)
-      maybe_gram |= (long long)md.n * md.r > K2_WARP_DOUBLES && !((long long)md.n * md.r <= K2_SMEM_DOUBLES && md.n <= 1024);
-    const long long g_b = (!k1g_off && world == 1 && maybe_gram) ? (long long)kConsWarps * 32 * 8 : 0;
-    const long long room = 227LL * 1024 - qcopies * L.nq * qslot * 4 - red_b - bar_b - g_b - 512;
+    const long long room = 227LL * 1024 - qcopies * L.nq * qslot * 4 - red_b - bar_b - 512;
     L.stage_floats = (int)std::min<long long>(16384 + 8, (room / (2LL * L.stages * 4)) & ~3LL);
     int off = 2 * L.stages * L.stage_floats * 4;
     L.off_q = off;   off += qcopies * L.nq * L.qslot_floats * 4;
     L.off_red = off; off += (int)red_b;
     off = (off + 15) & ~15;
     L.off_bar = off; off += (int)bar_b;
-    off = (off + 15) & ~15;
-    L.off_g = g_b ? off : 0;
-    off += (int)g_b;
     L.total = off;
   }
   // ---- K1 chunks: whole rows, <= stage_floats - 8 floats; 2^lg1 lanes per row so
@@ -3354,43 +3241,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
       for (int r0 = 0; r0 < md.n; r0 += 256) {
         pl->apply_mat.push_back(gidx);
         pl->apply_row0.push_back(r0);
-      }
-    }
-  }
-  for (auto& c : pl->k1) c.pad = -1;
-  if (pl->k1l.off_g > 0 && !pl->gram_list.empty()) {  // K1 accumulates P^T P of the Gram-space matrices
-    bool ok = true;
-    for (int mi : pl->gram_list) {
-      const MatDev& md = pl->mats[mi];
-      ok &= md.nck > 0 && md.lg1 <= 5 && md.r * (md.r + 1) / 2 <= (1 << md.lg1);
-    }
-    for (auto& c : pl->k1) ok &= c.split < 0;
-    if (ok) {
-      pl->k1gram = 1;
-      std::vector<int> nslots(pl->gram_list.size(), 0);
-      std::vector<long long> base(pl->gram_list.size(), 0);
-      std::vector<int> gid(std::max(1, nmat), -1);
-      for (size_t gi = 0; gi < pl->gram_list.size(); ++gi) gid[pl->gram_list[gi]] = (int)gi;
-      const int nct = (int)pl->k1_beg.size() - 1;
-      std::vector<int> sidx(pl->k1.size(), -1);
-      for (int b2 = 0; b2 < nct; ++b2)
-        for (int k = pl->k1_beg[b2]; k < pl->k1_beg[b2 + 1]; ++k) {
-          const int g = gid[pl->k1[k].mat];
-          if (g < 0) continue;
-          const bool first = k == pl->k1_beg[b2] || pl->k1[k - 1].mat != pl->k1[k].mat;
-          sidx[k] = first ? nslots[g]++ : sidx[k - 1];
-        }
-      for (size_t gi = 0; gi < pl->gram_list.size(); ++gi) {
-        const MatDev& md = pl->mats[pl->gram_list[gi]];
-        base[gi] = pl->wsg_elems;
-        pl->wsg_elems += (long long)nslots[gi] * (md.r * (md.r + 1) / 2);
-        pl->gram3_items.push_back({pl->gram_list[gi], 0, 0, 0, nslots[gi], (int)gi, base[gi]});
-      }
-      for (size_t k = 0; k < pl->k1.size(); ++k) {
-        const int g = gid[pl->k1[k].mat];
-        if (g < 0) continue;
-        const MatDev& md = pl->mats[pl->k1[k].mat];
-        pl->k1[k].pad = (int)(base[g] + (long long)sidx[k] * (md.r * (md.r + 1) / 2));
       }
     }
   }
@@ -3581,7 +3431,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_g3r = take((size_t)std::max(1, nmat) * sizeof(int));
   const size_t o_gl = take(pl->gram_list.size() * sizeof(int));
   const size_t o_gi = take(pl->gram_items.size() * sizeof(GramItem));
-  const size_t o_g3i = take(pl->gram3_items.size() * sizeof(GramItem));
   const size_t o_am = take(pl->apply_mat.size() * sizeof(int));
   const size_t o_ar = take(pl->apply_row0.size() * sizeof(int));
   const size_t o_amq = take(pl->apply_mat_q.size() * sizeof(int));
@@ -3612,7 +3461,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   const size_t o_rqm = take(pl->rq_mats.size() * sizeof(RqMat));
   const size_t o_rqk = take(pl->rq_blocks.size() * sizeof(int2));
   const size_t o_rqw = take((size_t)std::max(1LL, pl->rq_ws_elems) * sizeof(float));
-  const size_t o_rqs = take(2 * sizeof(int));
   cudaError_t ce = cudaMalloc(&pl->dev_block, off);
   if (ce != cudaSuccess) {
     delete pl;
@@ -3634,7 +3482,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_gs3_ready = reinterpret_cast<int*>(b + o_g3r);
   pl->d_gram_list = reinterpret_cast<int*>(b + o_gl);
   pl->d_gram_items = reinterpret_cast<GramItem*>(b + o_gi);
-  pl->d_gram3_items = reinterpret_cast<GramItem*>(b + o_g3i);
   pl->d_apply_mat = reinterpret_cast<int*>(b + o_am);
   pl->d_apply_row0 = reinterpret_cast<int*>(b + o_ar);
   pl->d_apply_mat_q = reinterpret_cast<int*>(b + o_amq);
@@ -3668,7 +3515,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   pl->d_rq_mats = reinterpret_cast<RqMat*>(b + o_rqm);
   pl->d_rq_blocks = reinterpret_cast<int2*>(b + o_rqk);
   pl->d_rq_ws = reinterpret_cast<float*>(b + o_rqw);
-  pl->d_rq_sync = reinterpret_cast<int*>(b + o_rqs);
   auto up = [&](void* dst, const void* src, size_t bytes) {
     return bytes ? cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
   };
@@ -3690,7 +3536,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_gs3_list, pl->gs3_list.data(), pl->gs3_list.size() * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_gs3_ready, 0, (size_t)std::max(1, nmat) * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_gram_items, pl->gram_items.data(), pl->gram_items.size() * sizeof(GramItem));
-  if (ce == cudaSuccess) ce = up(pl->d_gram3_items, pl->gram3_items.data(), pl->gram3_items.size() * sizeof(GramItem));
   if (ce == cudaSuccess) ce = up(pl->d_apply_mat, pl->apply_mat.data(), pl->apply_mat.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_apply_row0, pl->apply_row0.data(), pl->apply_row0.size() * sizeof(int));
   if (ce == cudaSuccess) ce = up(pl->d_apply_mat_q, pl->apply_mat_q.data(), pl->apply_mat_q.size() * sizeof(int));
@@ -3714,7 +3559,6 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
   if (ce == cudaSuccess) ce = up(pl->d_rq_blocks, pl->rq_blocks.data(), pl->rq_blocks.size() * sizeof(int2));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_pipe_ctr, 0, 2 * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_counters, 0, (size_t)std::max(1, pl->n_tall_slabs) * sizeof(int));
-  if (ce == cudaSuccess) ce = cudaMemset(pl->d_rq_sync, 0, 2 * sizeof(int));
   if (ce == cudaSuccess) ce = cudaMemset(pl->d_split_cnt, 0, std::max<size_t>(16, pl->splits.size() * sizeof(int)));
   if (ce != cudaSuccess) {
     cudaFree(pl->dev_block);
@@ -3770,7 +3614,7 @@ int psgd_plan_get_info(const psgd_plan* pl, psgd_plan_info* o) {
   o->launches_q_ef = k2_in_q_ef + (pl->pipe_items.empty() ? 0 : 1) + (int)pl->gkr.size() + nonempty(pl->g3) +
                      nonempty(pl->g4) + nonempty(pl->g4t) +
                      nonempty(pl->g4t2) +
-                     (pl->k3t.empty() ? 0 : 2) + (pl->rq.empty() ? 0 : (pl->rq_inkernel ? 1 : 2));
+                     (pl->k3t.empty() ? 0 : 2) + (pl->rq.empty() ? 0 : 2);
   (void)any_fused;
   o->launches_decompress = nonempty(pl->g5);
   o->launches_step_single = o->launches_ef_p + o->launches_q_ef;
@@ -3854,7 +3698,7 @@ int run_k1(const psgd_plan* pl, const float* g, const float* e, float* work, con
                             (const MatDev*)pl->d_mats, (const Chunk1*)pl->d_k1, (const int*)pl->d_k1_beg,
                             (const SplitRow*)pl->d_splits, pl->k1l, g, e, work, q, p, pl->d_psplit,
                             pl->d_split_cnt, bias_g, (long long)pl->nbias, (long long)pl->p_bias_off,
-                            (long long)pl->flag_off, status, pl->k1gram ? pl->d_wsg : (double*)nullptr));
+                            (long long)pl->flag_off, status));
   return PSGD_OK;
 }
 
@@ -4013,7 +3857,7 @@ int launch_rows(const psgd_plan* pl, float* work, float* e, const float* phat, c
 
 template <int R>
 int launch_rq_r(const psgd_plan* pl, const float* work, float* phat, const float* p, float* bias_out,
-                long long nbias, int divisor, float* q_out, int* status, cudaStream_t st) {
+                long long nbias, int divisor, int* status, cudaStream_t st) {
   auto kern = k3_rq<R>;
   PSGD_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl->rql.total));
   static const int dpol = getenv("PSGD_RQ_POL") ? atoi(getenv("PSGD_RQ_POL")) : 1;
@@ -4021,8 +3865,7 @@ int launch_rq_r(const psgd_plan* pl, const float* work, float* phat, const float
                             (const MatDev*)pl->d_mats, (const RqChunk*)pl->d_rq, (const int*)pl->d_rq_beg, pl->rql,
                             work, phat, pl->d_rq_ws, p, (const double*)pl->d_wsT, bias_out, nbias,
                             (long long)pl->p_bias_off, divisor,
-                            pl->rq_rev, dpol, (const RqMat*)pl->d_rq_mats, (const int2*)pl->d_rq_blocks,
-                            pl->rq_inkernel ? (int)pl->rq_blocks.size() : 0, q_out, pl->d_rq_sync, status));
+                            pl->rq_rev, dpol, status));
   return PSGD_OK;
 }
 
@@ -4030,13 +3873,13 @@ int launch_rq(const psgd_plan* pl, const float* work, float* phat, const float* 
               long long nbias, int divisor, float* q_out, int* status, cudaStream_t st) {
   int rc;
   switch (pl->rq_rmax) {
-    case 1: rc = launch_rq_r<1>(pl, work, phat, p, bias_out, nbias, divisor, q_out, status, st); break;
-    case 2: rc = launch_rq_r<2>(pl, work, phat, p, bias_out, nbias, divisor, q_out, status, st); break;
-    default: rc = launch_rq_r<4>(pl, work, phat, p, bias_out, nbias, divisor, q_out, status, st); break;
+    case 1: rc = launch_rq_r<1>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
+    case 2: rc = launch_rq_r<2>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
+    default: rc = launch_rq_r<4>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
   }
   if (rc) return rc;
   static const int xskip = getenv("PSGD_X_SKIP") ? atoi(getenv("PSGD_X_SKIP")) : 0;  // timing experiments only
-  if (!(xskip & 8) && !pl->rq_inkernel) PSGD_CUDA_CHECK(launch_ex(k3_rq_reduce, (int)pl->rq_blocks.size(), 32 * RQR_GROUPS, 0, st, PSGD_PDL != 0,
+  if (!(xskip & 8)) PSGD_CUDA_CHECK(launch_ex(k3_rq_reduce, (int)pl->rq_blocks.size(), 32 * RQR_GROUPS, 0, st, PSGD_PDL != 0,
                             (const MatDev*)pl->d_mats, (const RqMat*)pl->d_rq_mats, (const int2*)pl->d_rq_blocks,
                             (const float*)pl->d_rq_ws, q_out, (const int*)status));
   return PSGD_OK;
@@ -4072,17 +3915,11 @@ int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, 
   if (!pl->gram_items.empty()) {
     static const int xskip = getenv("PSGD_X_SKIP") ? atoi(getenv("PSGD_X_SKIP")) : 0;  // timing experiments only
     for (int pass = 1; pass <= 2; ++pass)  // pass 2 (re-orthogonalisation) exits at once unless pass 1 asks for it
-      if (!(xskip & pass)) {
-        // q path at W = 1: pass 1 is K1's partials + pass 3 (one CTA per matrix sums them and runs the MGS)
-        const bool p3 = pass == 1 && q_path && pl->k1gram;
-        PSGD_CUDA_CHECK(launch_ex(p3 ? k2_gram<3> : (pass == 1 ? k2_gram<1> : k2_gram<2>),
-                                p3 ? (int)pl->gram3_items.size() : (int)pl->gram_items.size(), 256, 0, st,
+      if (!(xskip & pass)) PSGD_CUDA_CHECK(launch_ex(pass == 1 ? k2_gram<1> : k2_gram<2>, (int)pl->gram_items.size(), 256, 0, st,
                                 PSGD_PDL != 0,
-                                (const MatDev*)pl->d_mats, (const GramItem*)(p3 ? pl->d_gram3_items : pl->d_gram_items),
-                                p, divisor, repl,
+                                (const MatDev*)pl->d_mats, (const GramItem*)pl->d_gram_items, p, divisor, repl,
                                 pl->d_wsg, pl->d_wsT, pl->d_gram_cnt, (long long)pl->flag_off, pl->nflags,
                                 pl->d_gsws, phat, status));
-      }
     // in psgd_q_ef, k3_rq makes the P-hat of its Gram-space matrices itself
     const std::vector<int>& am = q_path ? pl->apply_mat_q : pl->apply_mat;
     if (!am.empty() && !(xskip & 4))

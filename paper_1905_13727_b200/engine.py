@@ -348,8 +348,6 @@ class PowerSGDEngine:
             raise ContractViolation("orthogonalize input contains non-finite entries")
         if st & _lib.STATUS_REPLACEMENT:
             raise RuntimeError(f"Gram-Schmidt needed more than {_lib.REPL_ATTEMPTS} replacement draws for a column")
-        if st & _lib.STATUS_GRID_TIMEOUT:
-            raise RuntimeError("internal error: a grid-wide barrier of the q pass timed out")
 
     def _first_nonfinite(self):
         """(param name, worker) of the first non-finite gradient, worker-major as
