@@ -3878,8 +3878,7 @@ int launch_rq(const psgd_plan* pl, const float* work, float* phat, const float* 
     default: rc = launch_rq_r<4>(pl, work, phat, p, bias_out, nbias, divisor, status, st); break;
   }
   if (rc) return rc;
-  static const int xskip = getenv("PSGD_X_SKIP") ? atoi(getenv("PSGD_X_SKIP")) : 0;  // timing experiments only
-  if (!(xskip & 8)) PSGD_CUDA_CHECK(launch_ex(k3_rq_reduce, (int)pl->rq_blocks.size(), 32 * RQR_GROUPS, 0, st, PSGD_PDL != 0,
+  PSGD_CUDA_CHECK(launch_ex(k3_rq_reduce, (int)pl->rq_blocks.size(), 32 * RQR_GROUPS, 0, st, PSGD_PDL != 0,
                             (const MatDev*)pl->d_mats, (const RqMat*)pl->d_rq_mats, (const int2*)pl->d_rq_blocks,
                             (const float*)pl->d_rq_ws, q_out, (const int*)status));
   return PSGD_OK;
@@ -3913,16 +3912,15 @@ int launch_k2(const psgd_plan* pl, bool with_bias, const float* p, float* phat, 
                               status));
   }
   if (!pl->gram_items.empty()) {
-    static const int xskip = getenv("PSGD_X_SKIP") ? atoi(getenv("PSGD_X_SKIP")) : 0;  // timing experiments only
-    for (int pass = 1; pass <= 2; ++pass)  // pass 2 (re-orthogonalisation) exits at once unless pass 1 asks for it
-      if (!(xskip & pass)) PSGD_CUDA_CHECK(launch_ex(pass == 1 ? k2_gram<1> : k2_gram<2>, (int)pl->gram_items.size(), 256, 0, st,
+      for (int pass = 1; pass <= 2; ++pass)  // pass 2 (re-orthogonalisation) exits at once unless pass 1 asks for it
+      PSGD_CUDA_CHECK(launch_ex(pass == 1 ? k2_gram<1> : k2_gram<2>, (int)pl->gram_items.size(), 256, 0, st,
                                 PSGD_PDL != 0,
                                 (const MatDev*)pl->d_mats, (const GramItem*)pl->d_gram_items, p, divisor, repl,
                                 pl->d_wsg, pl->d_wsT, pl->d_gram_cnt, (long long)pl->flag_off, pl->nflags,
                                 pl->d_gsws, phat, status));
     // in psgd_q_ef, k3_rq makes the P-hat of its Gram-space matrices itself
     const std::vector<int>& am = q_path ? pl->apply_mat_q : pl->apply_mat;
-    if (!am.empty() && !(xskip & 4))
+    if (!am.empty())
       PSGD_CUDA_CHECK(launch_ex(k2_apply, (int)am.size(), 256, 0, st, PSGD_PDL != 0, (const MatDev*)pl->d_mats,
                                 (const int*)pl->d_gram_list, (const int*)(q_path ? pl->d_apply_mat_q : pl->d_apply_mat),
                                 (const int*)(q_path ? pl->d_apply_row0_q : pl->d_apply_row0), p, divisor,
@@ -4040,8 +4038,7 @@ int q_ef_impl(const psgd_plan* pl, float* work, const float* p, int32_t divisor,
                                          (const int*)status));
     }
   }
-  static const int xskip = getenv("PSGD_X_SKIP") ? atoi(getenv("PSGD_X_SKIP")) : 0;  // timing experiments only
-  if (!(xskip & 16)) rc = launch_rows(pl, work, e, p_hat, q_out, (const int*)status, st);  // tall, m = 2 mod 4: EF pass
+  rc = launch_rows(pl, work, e, p_hat, q_out, (const int*)status, st);  // tall, m = 2 mod 4: EF pass
   if (rc) return rc;
   for (const Group& gp : pl->g4) {
     rc = dispatch_r<RunK4>(gp.r, pl, (const RowItem*)pl->d_k4, gp, work, e, (const float*)p_hat,
