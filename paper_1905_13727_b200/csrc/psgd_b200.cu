@@ -3078,6 +3078,37 @@ int psgd_plan_create(int32_t nmat, const int64_t* n, const int64_t* m, int32_t r
         const MatDev& md = pl->mats[pl->rq[k].mat];
         pl->rq[k].slot = slot0[pl->rq[k].mat] + (long long)sidx[k] * md.m * md.r;
       }
+      {  // K4 (k4_rows) items in the order the q pass left delta in L2: k3_rq walked every CTA range
+         // backwards, so the starts of the ranges were read last — interleave the ranges, starts first
+        static const bool k4o_off = getenv("PSGD_K4_ORDER") && getenv("PSGD_K4_ORDER")[0] == '0';
+        std::vector<int> rng_of(pl->rq.size());
+        std::vector<long long> pos_of(pl->rq.size());
+        for (int b2 = 0; b2 < nct; ++b2) {
+          long long acc = 0;
+          for (int k = pl->rq_beg[b2]; k < pl->rq_beg[b2 + 1]; ++k) {
+            rng_of[k] = b2;
+            pos_of[k] = acc;
+            acc += pl->rq[k].nrows;
+          }
+        }
+        std::map<std::pair<int, int>, int> chunk_at_row;  // (mat, row0) of each block
+        for (size_t k = 0; k < pl->rq.size(); ++k) chunk_at_row[{pl->rq[k].mat, pl->rq[k].row0}] = (int)k;
+        for (auto& gp : pl->gkr) {
+          if (k4o_off || !rev) break;
+          std::vector<std::pair<std::pair<long long, int>, RowsItem>> keyed;
+          bool all = true;
+          for (int x = gp.ebeg; x < gp.eend; ++x) {
+            const RowsItem& it = pl->kr_e[x];
+            auto f = chunk_at_row.upper_bound({it.mat, it.r0});
+            if (f == chunk_at_row.begin() || (--f)->first.first != it.mat) { all = false; break; }
+            const int k = f->second;
+            keyed.push_back({{pos_of[k] + (it.r0 - pl->rq[k].row0), rng_of[k]}, it});
+          }
+          if (!all) continue;
+          std::stable_sort(keyed.begin(), keyed.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+          for (int x = gp.ebeg; x < gp.eend; ++x) pl->kr_e[x] = keyed[x - gp.ebeg].second;
+        }
+      }
       RqLayout& L = pl->rql;
       static const int nst = getenv("PSGD_RQ_STAGES") ? atoi(getenv("PSGD_RQ_STAGES")) : 3;
       for (L.stages = std::max(2, std::min(RQ_STAGES, nst));; --L.stages) {
